@@ -1,0 +1,159 @@
+"""CPU oracle — TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s `cpu_baseline` /
+`--impl reference` legs may import this package.  The product package
+`paper_1910_10032_b200` never imports it and shares no code with it.
+
+`wfst_oracle.c` is the serial token-passing Viterbi beam search of PAPER.md §3
+(Fig. 1) under the readings R1-R12 listed in
+DESIGN.md §3; this module only builds it with gcc and marshals arguments.
+Pins (tests/test_oracle_*.py): fp64 trellis Bellman-Ford and exhaustive path
+enumeration (tests/bruteforce.py), SPEC worked examples, invariants.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "wfst_oracle.c")
+_LIB = os.path.join(_HERE, "libwfst_oracle.so")
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-pthread"]
+
+RC = {0: "OK", 1: "INVALID", 5: "PDF_RANGE", 6: "CAPACITY", 7: "NO_SURVIVOR", 9: "OOM"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, rc: int, what: str = ""):
+        super().__init__(f"oracle {what}: {RC.get(rc, rc)}")
+        self.rc = rc
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(build())
+        P, I32, I64, F32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
+        L.oracle_graph_new.argtypes = [I32, I32, I64, P, P, P, P, P, P, C.POINTER(C.c_void_p)]
+        L.oracle_graph_free.argtypes = [P]
+        L.oracle_graph_perm.argtypes = [P, P]
+        L.oracle_graph_max_pdf.argtypes = [P]
+        L.oracle_graph_max_pdf.restype = I32
+        L.oracle_decode.argtypes = [P, P, I64, I32, I32, F32, I32, P, P, P, I32, P, P, I32, P,
+                                    P, P, P, P, P, P, I64, P]
+        L.oracle_decode_batch.argtypes = [P, P, I32, I32, I32, F32, I32, I32, P, P, P, P, P, I32, P]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class OracleResult:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+    def __repr__(self):
+        return f"OracleResult(cost={self.cost}, reached_final={self.reached_final}, olabels={self.olabels})"
+
+
+class OracleGraph:
+    """The oracle's own canonical CSR of a graph given as plain arrays."""
+
+    def __init__(self, g):
+        self.g = g
+        L = lib()
+        self._arr = [np.ascontiguousarray(x) for x in
+                     (g.src.astype(np.int32), g.dst.astype(np.int32), g.ilabel.astype(np.int32),
+                      g.olabel.astype(np.int32), g.weight.astype(np.float32), g.final.astype(np.float32))]
+        h = C.c_void_p()
+        rc = L.oracle_graph_new(g.n_states, g.start, g.n_arcs, *[_p(a) for a in self._arr], C.byref(h))
+        if rc:
+            raise OracleError(rc, "graph_new")
+        self.h = h
+        self.max_pdf = L.oracle_graph_max_pdf(h)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.oracle_graph_free(self.h)
+            self.h = None
+
+    def perm(self) -> np.ndarray:
+        out = np.empty(self.g.n_arcs, dtype=np.int64)
+        lib().oracle_graph_perm(self.h, _p(out))
+        return out
+
+    def decode(self, ll: np.ndarray, beam: float, max_active: int = 0, survivors: bool = False,
+               surv_cap: int | None = None) -> OracleResult:
+        """ll: float32 [T][P] (or a [T][...][P] view whose frame stride is given by ll.strides)."""
+        ll = np.asarray(ll, dtype=np.float32)
+        if ll.ndim != 2:
+            raise ValueError("ll must be [T][P]")
+        if ll.strides[1] != 4:
+            ll = np.ascontiguousarray(ll)
+        T, P = ll.shape
+        stride = ll.strides[0] // 4
+        cost = np.zeros(1, np.float32)
+        rf = np.zeros(1, np.int32)
+        cap = 4 * (T + 1) + 64
+        arcs = np.zeros(cap, np.int32)
+        n_arcs = np.zeros(1, np.int32)
+        ol = np.zeros(cap, np.int32)
+        n_ol = np.zeros(1, np.int32)
+        fst = np.zeros((max(T, 1), 3), np.float32)
+        fcn = np.zeros((max(T, 1), 5), np.int64)
+        relax = np.zeros(1, np.int64)
+        sn = sst = sar = sco = None
+        scap = 0
+        if survivors:
+            scap = surv_cap or max(1, (T + 1) * self.g.n_states)
+            sn = np.zeros(T + 1, np.int32)
+            sst = np.zeros(scap, np.int32)
+            sar = np.zeros(scap, np.int32)
+            sco = np.zeros(scap, np.float32)
+        rc = lib().oracle_decode(self.h, _p(ll) if T else None, stride, T, P, float(beam),
+                                 int(max_active), _p(cost), _p(rf), _p(arcs), cap, _p(n_arcs),
+                                 _p(ol), cap, _p(n_ol), _p(fst), _p(fcn), _p(sn), _p(sst), _p(sar),
+                                 _p(sco), scap, _p(relax))
+        if rc:
+            raise OracleError(rc, "decode")
+        res = OracleResult(cost=float(cost[0]), cost32=cost[0], reached_final=int(rf[0]),
+                           arcs=arcs[: n_arcs[0]].copy(), olabels=ol[: n_ol[0]].copy(),
+                           frame_stats=fst[:T].copy(), frame_counts=fcn[:T].copy(),
+                           eps_relax=int(relax[0]))
+        if survivors:
+            offs = np.concatenate([[0], np.cumsum(sn)])
+            res.layers = [(sst[offs[k]:offs[k + 1]].copy(), sar[offs[k]:offs[k + 1]].copy(),
+                           sco[offs[k]:offs[k + 1]].copy()) for k in range(T + 1)]
+        return res
+
+    def decode_batch(self, ll: np.ndarray, beam: float, max_active: int, n_threads: int,
+                     arcs_cap: int = 0):
+        """ll: float32 [T][B][P] contiguous.  Returns (cost, reached, rc, arcs_count, arcs, n_arcs)."""
+        ll = np.ascontiguousarray(ll, dtype=np.float32)
+        T, B, P = ll.shape
+        cost = np.zeros(B, np.float32)
+        reached = np.zeros(B, np.int32)
+        rc = np.zeros(B, np.int32)
+        cnt = np.zeros(B, np.int64)
+        arcs = np.zeros((B, arcs_cap), np.int32) if arcs_cap else None
+        n_arcs = np.zeros(B, np.int32) if arcs_cap else None
+        r = lib().oracle_decode_batch(self.h, _p(ll), T, B, P, float(beam), int(max_active),
+                                      int(n_threads), _p(cost), _p(reached), _p(rc), _p(cnt),
+                                      _p(arcs), arcs_cap, _p(n_arcs))
+        if r:
+            raise OracleError(r, "decode_batch")
+        return cost, reached, rc, cnt, arcs, n_arcs

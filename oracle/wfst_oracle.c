@@ -1,0 +1,450 @@
+/*
+ * oracle/wfst_oracle.c -- CPU ORACLE.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  The product path
+ * (paper_1910_10032_b200/) never links, imports or calls it, and shares no
+ * code, header, table or helper with it.
+ *
+ * What it computes: serial frame-synchronous token-passing Viterbi beam
+ * search over a WFST (§3, "for each frame ... processes
+ * emitting arcs (those arcs with non-null labels) conditioned on frame
+ * values, processes any chains of non-emitting arcs, and finally performs
+ * pruning"), in the step order of Fig. 1 (Expand -> Set Beam via
+ * max-active -> Contract -> Non-emitting -> representatives for the next
+ * frame), one-best output by traceback.  The readings R1-R12 it implements
+ * are listed in DESIGN.md §3 (taken from SURVEY.md §8.4):
+ *   R1  fp32, fixed order: emitting c' = (c + w) - L[t][pdf]; eps c' = c + w;
+ *       final c + F.  Built with -ffp-contract=off (no FMA).
+ *   R2  emitting <=> ilabel != 0, pdf = ilabel - 1.
+ *   R3  init: token (start, 0, arc -1), eps-closure with keep(c) = c < beam.
+ *   R4  emitting candidates, one per destination state, min by (cost, arc).
+ *   R5  best = min candidate cost, beam_cut = fl(best + beam), keep c < beam_cut.
+ *   R6  exact max-active: if n = #{c < beam_cut} > alpha, k = alpha-th
+ *       smallest of those costs, keep(c) = c < beam_cut && c <= k.
+ *   R7  eps-closure under the FIXED keep() of the frame, worklist to the
+ *       least fixed point; relaxations whose result fails keep() are dropped.
+ *   R8  survivors = states whose final entry passes keep(): one token per
+ *       state (the representative).
+ *   R9  ties broken by (cost, canonical arc id).
+ *   R10 finals: argmin c + F over final survivors; else argmin c, flag 0.
+ *   R11 traceback by back-pointers: emitting arc -> previous layer,
+ *       eps arc -> same layer.
+ * Canonical arc ids: arcs stably bucketed by (src, emitting-first) in input
+ * order ("within a span, emitting arcs precede non-emitting").
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { O_OK = 0, O_INVALID = 1, O_PDF_RANGE = 5, O_CAPACITY = 6, O_NO_SURVIVOR = 7, O_OOM = 9 };
+
+typedef struct {
+  int32_t Q, start;
+  int64_t E;
+  int64_t *first;   /* [Q+1] canonical arc offsets                        */
+  int32_t *n_emit;  /* [Q] emitting arcs of the state (they come first)   */
+  int32_t *src, *dst, *ilabel, *olabel; /* [E] canonical order           */
+  float *weight;    /* [E]                                                */
+  float *final;     /* [Q] +inf = non-final                               */
+  int64_t *perm;    /* canonical arc i = input arc perm[i]                */
+  int32_t max_pdf;
+} OGraph;
+
+void oracle_graph_free(void *gp) {
+  OGraph *g = (OGraph *)gp;
+  if (!g) return;
+  free(g->first); free(g->n_emit); free(g->src); free(g->dst); free(g->ilabel);
+  free(g->olabel); free(g->weight); free(g->final); free(g->perm); free(g);
+}
+
+int oracle_graph_new(int32_t Q, int32_t start, int64_t E, const int32_t *src, const int32_t *dst,
+                     const int32_t *ilabel, const int32_t *olabel, const float *weight,
+                     const float *final, void **out) {
+  if (Q <= 0 || start < 0 || start >= Q || E < 0 || !out) return O_INVALID;
+  OGraph *g = (OGraph *)calloc(1, sizeof(OGraph));
+  if (!g) return O_OOM;
+  g->Q = Q; g->start = start; g->E = E; g->max_pdf = -1;
+  g->first = (int64_t *)calloc((size_t)Q + 1, sizeof(int64_t));
+  g->n_emit = (int32_t *)calloc((size_t)Q, sizeof(int32_t));
+  size_t e1 = (size_t)(E > 0 ? E : 1);
+  g->src = (int32_t *)malloc(e1 * 4); g->dst = (int32_t *)malloc(e1 * 4);
+  g->ilabel = (int32_t *)malloc(e1 * 4); g->olabel = (int32_t *)malloc(e1 * 4);
+  g->weight = (float *)malloc(e1 * 4); g->final = (float *)malloc((size_t)Q * 4);
+  g->perm = (int64_t *)malloc(e1 * 8);
+  int64_t *cur_e = (int64_t *)malloc((size_t)Q * 8), *cur_n = (int64_t *)malloc((size_t)Q * 8);
+  if (!g->first || !g->n_emit || !g->src || !g->dst || !g->ilabel || !g->olabel || !g->weight ||
+      !g->final || !g->perm || !cur_e || !cur_n) {
+    free(cur_e); free(cur_n); oracle_graph_free(g); return O_OOM;
+  }
+  int32_t *n_all = (int32_t *)calloc((size_t)Q, 4);
+  for (int64_t i = 0; i < E; i++) {
+    if (src[i] < 0 || src[i] >= Q || dst[i] < 0 || dst[i] >= Q || ilabel[i] < 0) {
+      free(n_all); free(cur_e); free(cur_n); oracle_graph_free(g); return O_INVALID;
+    }
+    n_all[src[i]]++;
+    if (ilabel[i] != 0) g->n_emit[src[i]]++;
+  }
+  for (int32_t q = 0; q < Q; q++) g->first[q + 1] = g->first[q] + n_all[q];
+  for (int32_t q = 0; q < Q; q++) { cur_e[q] = g->first[q]; cur_n[q] = g->first[q] + g->n_emit[q]; }
+  for (int64_t i = 0; i < E; i++) {          /* stable bucket: emitting first */
+    int32_t s = src[i];
+    int64_t k = ilabel[i] != 0 ? cur_e[s]++ : cur_n[s]++;
+    g->src[k] = s; g->dst[k] = dst[i]; g->ilabel[k] = ilabel[i]; g->olabel[k] = olabel[i];
+    g->weight[k] = weight[i] + 0.0f;        /* canonical +0 */
+    g->perm[k] = i;
+    if (ilabel[i] - 1 > g->max_pdf) g->max_pdf = ilabel[i] - 1;
+  }
+  for (int32_t q = 0; q < Q; q++) g->final[q] = final[q];
+  free(n_all); free(cur_e); free(cur_n);
+  *out = g;
+  return O_OK;
+}
+
+int oracle_graph_perm(void *gp, int64_t *perm_out) {
+  OGraph *g = (OGraph *)gp;
+  memcpy(perm_out, g->perm, (size_t)g->E * 8);
+  return O_OK;
+}
+
+int32_t oracle_graph_max_pdf(void *gp) { return ((OGraph *)gp)->max_pdf; }
+
+/* (cost, arc) lexicographic "less"; arc -1 (the start token) sorts last (R9). */
+static int lex_less(float c1, int32_t a1, float c2, int32_t a2) {
+  if (c1 < c2) return 1;
+  if (c1 > c2) return 0;
+  return (uint32_t)a1 < (uint32_t)a2;
+}
+
+static int cmp_float(const void *x, const void *y) {
+  float a = *(const float *)x, b = *(const float *)y;
+  return (a > b) - (a < b);
+}
+
+static int cmp_int(const void *x, const void *y) {
+  int32_t a = *(const int32_t *)x, b = *(const int32_t *)y;
+  return (a > b) - (a < b);
+}
+
+typedef struct {       /* one layer of survivors, sorted by state */
+  int32_t n;
+  int32_t *state, *arc;
+  float *cost;
+} Layer;
+
+typedef struct {
+  const OGraph *g;
+  /* dense per-state scratch */
+  float *dcost; int32_t *darc; uint8_t *seen, *inq;
+  int32_t *touched, n_touched;
+  int32_t *queue;  /* FIFO of capacity Q (each state queued at most once at a time) */
+  float *tmp;      /* costs for max-active selection */
+  Layer *layers;   /* T+1 */
+  int32_t n_layers;
+} Work;
+
+static void work_free(Work *w) {
+  free(w->dcost); free(w->darc); free(w->seen); free(w->inq); free(w->touched);
+  free(w->queue); free(w->tmp);
+  if (w->layers)
+    for (int32_t k = 0; k < w->n_layers; k++) {
+      free(w->layers[k].state); free(w->layers[k].arc); free(w->layers[k].cost);
+    }
+  free(w->layers);
+}
+
+/* keep() of R5/R6: c < beam_cut && (no alpha || c <= kalpha) */
+typedef struct { float beam_cut, kalpha; int use_alpha; } Keep;
+static int keep(const Keep *k, float c) { return c < k->beam_cut && (!k->use_alpha || c <= k->kalpha); }
+
+static void touch(Work *w, int32_t q, float c, int32_t a) {
+  w->seen[q] = 1; w->dcost[q] = c; w->darc[q] = a; w->touched[w->n_touched++] = q;
+}
+
+/* R7: eps-closure to the least fixed point under a fixed keep().  Returns the
+ * number of eps arc relaxations performed (implementation-dependent count). */
+static int64_t eps_closure(Work *w, const Keep *k) {
+  const OGraph *g = w->g;
+  int64_t relax = 0;
+  int32_t head = 0, tail = 0, Q = g->Q;  /* circular FIFO, <= Q entries */
+  int32_t cnt = 0;
+  for (int32_t i = 0; i < w->n_touched; i++) {
+    int32_t q = w->touched[i];
+    if (keep(k, w->dcost[q]) && g->first[q] + g->n_emit[q] < g->first[q + 1]) {
+      w->queue[tail] = q; tail = (tail + 1) % Q; cnt++; w->inq[q] = 1;
+    }
+  }
+  while (cnt > 0) {
+    int32_t p = w->queue[head]; head = (head + 1) % Q; cnt--; w->inq[p] = 0;
+    float cp = w->dcost[p];
+    if (!keep(k, cp)) continue;
+    for (int64_t e = g->first[p] + g->n_emit[p]; e < g->first[p + 1]; e++) {
+      float c = cp + g->weight[e];
+      relax++;
+      if (!keep(k, c)) continue;
+      int32_t q = g->dst[e];
+      if (!w->seen[q]) {
+        touch(w, q, c, (int32_t)e);
+      } else if (lex_less(c, (int32_t)e, w->dcost[q], w->darc[q])) {
+        w->dcost[q] = c; w->darc[q] = (int32_t)e;
+      } else {
+        continue;
+      }
+      if (!w->inq[q] && g->first[q] + g->n_emit[q] < g->first[q + 1]) {
+        w->queue[tail] = q; tail = (tail + 1) % Q; cnt++; w->inq[q] = 1;
+      }
+    }
+  }
+  return relax;
+}
+
+/* R8: survivors of the layer, sorted by state; clears the scratch. */
+static int make_layer(Work *w, const Keep *k, Layer *L, int64_t *eps_deg_sum) {
+  const OGraph *g = w->g;
+  int32_t n = 0;
+  for (int32_t i = 0; i < w->n_touched; i++)
+    if (keep(k, w->dcost[w->touched[i]])) n++;
+  L->n = n;
+  L->state = (int32_t *)malloc((size_t)(n ? n : 1) * 4);
+  L->arc = (int32_t *)malloc((size_t)(n ? n : 1) * 4);
+  L->cost = (float *)malloc((size_t)(n ? n : 1) * 4);
+  if (!L->state || !L->arc || !L->cost) return O_OOM;
+  int32_t j = 0;
+  for (int32_t i = 0; i < w->n_touched; i++) {
+    int32_t q = w->touched[i];
+    if (keep(k, w->dcost[q])) L->state[j++] = q;
+  }
+  qsort(L->state, (size_t)n, 4, cmp_int);
+  int64_t es = 0;
+  for (int32_t i = 0; i < n; i++) {
+    int32_t q = L->state[i];
+    L->arc[i] = w->darc[q]; L->cost[i] = w->dcost[q];
+    es += (g->first[q + 1] - g->first[q]) - g->n_emit[q];
+  }
+  if (eps_deg_sum) *eps_deg_sum = es;
+  for (int32_t i = 0; i < w->n_touched; i++) w->seen[w->touched[i]] = 0;
+  w->n_touched = 0;
+  return O_OK;
+}
+
+static int32_t layer_find(const Layer *L, int32_t q) {
+  int32_t lo = 0, hi = L->n - 1;
+  while (lo <= hi) {
+    int32_t m = (lo + hi) / 2;
+    if (L->state[m] == q) return m;
+    if (L->state[m] < q) lo = m + 1; else hi = m - 1;
+  }
+  return -1;
+}
+
+/*
+ * Decode one stream.  ll points at frame 0's row; frame t's row is
+ * ll + t*ll_stride (P floats, pdf-indexed).  beam may be +inf; max_active
+ * <= 0 means unbounded.  Outputs (all nullable except cost/reached_final):
+ *   arcs[arcs_cap], *n_arcs     canonical arc ids of the best path
+ *   olabels[ol_cap], *n_ol      its non-zero olabels
+ *   fstats[T*3]                 per frame: best, beam_cut, kalpha (+inf if unused)
+ *   fcounts[T*5]                per frame: n_cand, n_inbeam, n_surv,
+ *                               emitting arcs expanded, eps arcs of survivors
+ *   surv_n[T+1]                 survivors per layer (layer 0 = after init)
+ *   surv_state/arc/cost[surv_cap] concatenated layers, sorted by state
+ */
+int oracle_decode(void *gp, const float *ll, int64_t ll_stride, int32_t T, int32_t P, float beam,
+                  int32_t max_active, float *cost, int32_t *reached_final, int32_t *arcs,
+                  int32_t arcs_cap, int32_t *n_arcs, int32_t *olabels, int32_t ol_cap,
+                  int32_t *n_ol, float *fstats, int64_t *fcounts, int32_t *surv_n,
+                  int32_t *surv_state, int32_t *surv_arc, float *surv_cost, int64_t surv_cap,
+                  int64_t *eps_relax_total) {
+  const OGraph *g = (const OGraph *)gp;
+  if (!g || T < 0 || (T > 0 && (!ll || P <= 0)) || !cost || !reached_final) return O_INVALID;
+  if (T > 0 && P <= g->max_pdf) return O_PDF_RANGE;
+  int32_t Q = g->Q;
+  Work w;
+  memset(&w, 0, sizeof w);
+  w.g = g;
+  w.dcost = (float *)malloc((size_t)Q * 4); w.darc = (int32_t *)malloc((size_t)Q * 4);
+  w.seen = (uint8_t *)calloc((size_t)Q, 1); w.inq = (uint8_t *)calloc((size_t)Q, 1);
+  w.touched = (int32_t *)malloc((size_t)Q * 4); w.queue = (int32_t *)malloc((size_t)Q * 4);
+  w.tmp = (float *)malloc((size_t)Q * 4);
+  w.layers = (Layer *)calloc((size_t)T + 1, sizeof(Layer));
+  w.n_layers = T + 1;
+  int rc = O_OK;
+  int64_t relax_total = 0;
+  if (!w.dcost || !w.darc || !w.seen || !w.inq || !w.touched || !w.queue || !w.tmp || !w.layers) {
+    rc = O_OOM; goto done;
+  }
+
+  /* R3: start token and the initial eps-closure, keep(c) = c < fl(0 + beam) */
+  {
+    Keep k0 = {0.0f + beam, INFINITY, 0};
+    touch(&w, g->start, 0.0f, -1);
+    relax_total += eps_closure(&w, &k0);
+    rc = make_layer(&w, &k0, &w.layers[0], NULL);
+    if (rc) goto done;
+  }
+
+  for (int32_t t = 0; t < T; t++) {
+    const float *row = ll + (int64_t)t * ll_stride;
+    const Layer *prev = &w.layers[t];
+    int64_t n_emit_arcs = 0;
+    /* R4: emitting arcs of every survivor, conditioned on the frame */
+    for (int32_t i = 0; i < prev->n; i++) {
+      int32_t p = prev->state[i];
+      float cp = prev->cost[i];
+      for (int64_t a = g->first[p]; a < g->first[p] + g->n_emit[p]; a++) {
+        float c = (cp + g->weight[a]) - row[g->ilabel[a] - 1];
+        int32_t q = g->dst[a];
+        n_emit_arcs++;
+        if (!w.seen[q]) touch(&w, q, c, (int32_t)a);
+        else if (lex_less(c, (int32_t)a, w.dcost[q], w.darc[q])) { w.dcost[q] = c; w.darc[q] = (int32_t)a; }
+      }
+    }
+    if (w.n_touched == 0) { rc = O_NO_SURVIVOR; goto done; }
+    /* R5: beam against the stream's best candidate (Fig. 1 "Set Beam") */
+    float best = INFINITY;
+    for (int32_t i = 0; i < w.n_touched; i++)
+      if (w.dcost[w.touched[i]] < best) best = w.dcost[w.touched[i]];
+    Keep k = {best + beam, INFINITY, 0};
+    int32_t n_in = 0;
+    for (int32_t i = 0; i < w.n_touched; i++)
+      if (w.dcost[w.touched[i]] < k.beam_cut) w.tmp[n_in++] = w.dcost[w.touched[i]];
+    /* R6: exact max-active (alpha-th smallest in-beam cost) */
+    if (max_active > 0 && n_in > max_active) {
+      qsort(w.tmp, (size_t)n_in, 4, cmp_float);
+      k.kalpha = w.tmp[max_active - 1];
+      k.use_alpha = 1;
+    }
+    int32_t n_cand = w.n_touched;
+    /* R7: eps chains to convergence under the fixed cutoff */
+    relax_total += eps_closure(&w, &k);
+    int64_t eps_deg = 0;
+    rc = make_layer(&w, &k, &w.layers[t + 1], &eps_deg);
+    if (rc) goto done;
+    if (fstats) {
+      fstats[3 * t] = best; fstats[3 * t + 1] = k.beam_cut;
+      fstats[3 * t + 2] = k.use_alpha ? k.kalpha : INFINITY;
+    }
+    if (fcounts) {
+      fcounts[5 * t] = n_cand; fcounts[5 * t + 1] = n_in; fcounts[5 * t + 2] = w.layers[t + 1].n;
+      fcounts[5 * t + 3] = n_emit_arcs; fcounts[5 * t + 4] = eps_deg;
+    }
+  }
+
+  /* R10: final costs */
+  {
+    const Layer *L = &w.layers[T];
+    int32_t bi = -1; float bc = INFINITY; int32_t ba = -1;
+    for (int32_t i = 0; i < L->n; i++) {
+      float F = g->final[L->state[i]];
+      if (!(F < INFINITY)) continue;
+      float c = L->cost[i] + F;
+      if (bi < 0 || lex_less(c, L->arc[i], bc, ba)) { bi = i; bc = c; ba = L->arc[i]; }
+    }
+    *reached_final = bi >= 0;
+    if (bi < 0)
+      for (int32_t i = 0; i < L->n; i++)
+        if (bi < 0 || lex_less(L->cost[i], L->arc[i], bc, ba)) { bi = i; bc = L->cost[i]; ba = L->arc[i]; }
+    if (bi < 0) { rc = O_NO_SURVIVOR; goto done; }
+    *cost = bc;
+    /* R11: traceback */
+    int32_t layer = T, q = L->state[bi], n = 0, no = 0;
+    int64_t guard = ((int64_t)T + 1) * ((int64_t)Q + 1);
+    int32_t cap_path = 1024;
+    int32_t *path = (int32_t *)malloc((size_t)cap_path * 4);
+    while (path) {
+      int32_t j = layer_find(&w.layers[layer], q);
+      if (j < 0 || guard-- <= 0) { free(path); path = NULL; rc = O_INVALID; break; }
+      int32_t a = w.layers[layer].arc[j];
+      if (a < 0) break;
+      if (n == cap_path) {
+        cap_path *= 2;
+        int32_t *np_ = (int32_t *)realloc(path, (size_t)cap_path * 4);
+        if (!np_) { free(path); path = NULL; rc = O_OOM; break; }
+        path = np_;
+      }
+      path[n++] = a;
+      q = g->src[a];
+      if (g->ilabel[a] != 0) layer--;
+    }
+    if (!path) goto done;
+    if (n_arcs) *n_arcs = n;
+    for (int32_t i = 0; i < n; i++) {
+      int32_t a = path[n - 1 - i];
+      if (arcs && i < arcs_cap) arcs[i] = a;
+      if (g->olabel[a] != 0) {
+        if (olabels && no < ol_cap) olabels[no] = g->olabel[a];
+        no++;
+      }
+    }
+    if (n_ol) *n_ol = no;
+    free(path);
+    if ((arcs && n > arcs_cap) || (olabels && no > ol_cap)) rc = O_CAPACITY;
+  }
+  if (surv_n) {
+    int64_t off = 0;
+    for (int32_t k = 0; k <= T; k++) {
+      const Layer *L = &w.layers[k];
+      surv_n[k] = L->n;
+      for (int32_t i = 0; i < L->n; i++, off++) {
+        if (off >= surv_cap) continue;
+        if (surv_state) surv_state[off] = L->state[i];
+        if (surv_arc) surv_arc[off] = L->arc[i];
+        if (surv_cost) surv_cost[off] = L->cost[i];
+      }
+    }
+    if (off > surv_cap && (surv_state || surv_arc || surv_cost)) rc = rc ? rc : O_CAPACITY;
+  }
+  if (eps_relax_total) *eps_relax_total = relax_total;
+done:
+  work_free(&w);
+  return rc;
+}
+
+/* ---- multi-core driver for cpu_baseline: streams split over pthreads ---- */
+typedef struct {
+  void *g; const float *ll; int64_t ll_stride; int32_t T, P; float beam; int32_t max_active;
+  int32_t B, n_thr, tid;
+  float *cost; int32_t *reached; int32_t *rc; int64_t *emit_arcs;
+  int32_t *arcs; int32_t arcs_cap; int32_t *n_arcs;
+} BatchArg;
+
+static void *batch_worker(void *p) {
+  BatchArg *a = (BatchArg *)p;
+  int64_t *fc = (int64_t *)malloc((size_t)(a->T > 0 ? a->T : 1) * 5 * 8);
+  for (int32_t b = a->tid; b < a->B; b += a->n_thr) {
+    memset(fc, 0, (size_t)(a->T > 0 ? a->T : 1) * 5 * 8);
+    a->rc[b] = oracle_decode(a->g, a->ll + (int64_t)b * a->P, a->ll_stride, a->T, a->P, a->beam,
+                             a->max_active, &a->cost[b], &a->reached[b],
+                             a->arcs ? a->arcs + (int64_t)b * a->arcs_cap : NULL, a->arcs_cap,
+                             a->n_arcs ? &a->n_arcs[b] : NULL, NULL, 0, NULL, NULL, fc, NULL, NULL,
+                             NULL, NULL, 0, NULL);
+    int64_t s = 0;
+    for (int32_t t = 0; t < a->T; t++) s += fc[5 * t + 3] + fc[5 * t + 4];
+    a->emit_arcs[b] = s;
+  }
+  free(fc);
+  return NULL;
+}
+
+/* ll layout [T][B][P]; stream b row t at ll + (t*B + b)*P. */
+int oracle_decode_batch(void *g, const float *ll, int32_t T, int32_t B, int32_t P, float beam,
+                        int32_t max_active, int32_t n_threads, float *cost, int32_t *reached,
+                        int32_t *rc, int64_t *arcs_count, int32_t *arcs, int32_t arcs_cap,
+                        int32_t *n_arcs) {
+  if (n_threads < 1) n_threads = 1;
+  if (n_threads > B) n_threads = B > 0 ? B : 1;
+  pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)n_threads);
+  BatchArg *args = (BatchArg *)malloc(sizeof(BatchArg) * (size_t)n_threads);
+  if (!th || !args) { free(th); free(args); return O_OOM; }
+  for (int32_t i = 0; i < n_threads; i++) {
+    BatchArg a = {g, ll, (int64_t)B * P, T, P, beam, max_active, B, n_threads, i,
+                  cost, reached, rc, arcs_count, arcs, arcs_cap, n_arcs};
+    args[i] = a;
+    pthread_create(&th[i], NULL, batch_worker, &args[i]);
+  }
+  for (int32_t i = 0; i < n_threads; i++) pthread_join(th[i], NULL);
+  free(th); free(args);
+  return O_OK;
+}
