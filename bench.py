@@ -110,12 +110,30 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# ------------------------------------------------------------------------- multi-GPU host logic
+def rank_streams(rank: int, world: int, per_rank: int) -> range:
+    """Global stream ids of a rank (weak scaling: every rank decodes its own per_rank streams;
+    inputs are keyed by global id, so a stream's result does not depend on the split)."""
+    assert 0 <= rank < world
+    return range(rank * per_rank, (rank + 1) * per_rank)
+
+
+def reduce_over_ranks(dist, device, ms: float, arcs: float):
+    """Max of the timed region and sum of arcs over ranks (the only collective, off the data path)."""
+    import torch
+    t = torch.tensor([ms, arcs], dtype=torch.float64, device=device)
+    m = t.clone()
+    dist.all_reduce(m, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(m[0].item()), float(t[1].item())
+
+
 # ------------------------------------------------------------------------- workload
-def make_workload(cfg: str, preset: str, rank: int = 0):
+def make_workload(cfg: str, preset: str, rank: int = 0, world: int = 1):
     c = I.CONFIGS[cfg]
     g = I.config_graph(cfg)
     B, T, P = c["streams"], c["frames"], c["n_pdfs"]
-    stream0 = rank * B
+    stream0 = rank_streams(rank, world, B).start
     planted = I.planted_walks(g, B, T, seed=c["ll_seed"], stream0=stream0)
     return dict(cfg=cfg, c=c, graph=g, B=B, T=T, P=P, stream0=stream0, planted=planted,
                 preset=I.preset(preset), preset_name=preset, beam=c["beam"], alpha=c["max_active"])
@@ -164,7 +182,7 @@ def gpu_arm(args):
     if world > 1:
         dist.barrier()
 
-    wl = make_workload(args.config, args.preset, rank)
+    wl = make_workload(args.config, args.preset, rank, world)
     T, B, P = wl["T"], wl["B"], wl["P"]
     G = W.Graph.from_arrays(wl["graph"], device=local)
     ginfo = G.info()
@@ -201,12 +219,7 @@ def gpu_arm(args):
     kern_ms = [a.elapsed_time(b) for a, b in kev]
     st = D.stats()
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_max = float(tt.item())
-        tot = torch.tensor([st["emit_arcs"] + st["eps_arcs"]], dtype=torch.float64, device=dev)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        arcs_all = float(tot.item())
+        ms_max, arcs_all = reduce_over_ranks(dist, dev, ms, float(st["emit_arcs"] + st["eps_arcs"]))
     else:
         ms_max = ms
         arcs_all = float(st["emit_arcs"] + st["eps_arcs"])
@@ -240,9 +253,7 @@ def gpu_arm(args):
         torch.cuda.synchronize(dev)
         ems = e0.elapsed_time(e1)
         if world > 1:
-            tt = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
+            ems, _ = reduce_over_ranks(dist, dev, ems, 0.0)
         d2h = B * (4 + 4 + 4 + 4 + 4 + 2 * cap * 4)
         e2e = {"value": e2e_steps * B * T * FRAME_S * world / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": T * B * P * 4 * world, "d2h_bytes_per_step": d2h * world,
