@@ -63,7 +63,7 @@ struct KParams {
   int32_t* slotrec;   // [lane][FCAP]     slot -> survivor index
   int2* fslot;        // [lane][FCAP]     survivor index -> {slot, arc}
   u64* ovf;           // [lane][C_ovf]    global overflow token table
-  int4* wl;           // [lane][2][FCAP]  epsilon worklists {slot, state, eps begin, eps degree}
+  int2* wl;           // [lane][2][FCAP]  epsilon worklists {slot, state}
   int2* rec;          // [lane][R_cap]    traceback records {arc, prev}
   float* rec_cost;    // [lane][R_cap]    (debug) survivor cost
   float* fstats;      // [lane][TMAX][3]
@@ -207,7 +207,7 @@ struct Frame {
   int32_t* slotrec;
   int2* fslot;
   u64* ovf;
-  int4* wl[2];
+  int2* wl[2];
   int2* rec;
   float* rec_cost;
 
@@ -251,9 +251,10 @@ struct Frame {
     return s + p.C;
   }
 
-  __device__ __forceinline__ void add_claim(int slot, uint32_t q) {
+  // claim entry = {slot, state | has_eps << 31}
+  __device__ __forceinline__ void add_claim(int slot, uint32_t q, uint32_t eps_flag) {
     int idx = atomicAdd(&S.n_claim, 1);
-    if (idx < p.FCAP) claim[idx] = make_int2(slot, (int)q);
+    if (idx < p.FCAP) claim[idx] = make_int2(slot, (int)(q | (eps_flag << 31)));
     else S.status = WFST_ERR_CAPACITY;
   }
 
@@ -348,7 +349,7 @@ struct Frame {
           if (slot < 0) continue;
           if (claimed) {
             atomicAdd(&hist[bin], 1);
-            add_claim(slot, q);
+            add_claim(slot, q, (uint32_t)arc.w >> 31);
           }
           if (improved) {
             wslot[r] = slot;
@@ -375,6 +376,15 @@ struct Frame {
     const int tid = threadIdx.x;
     const float beam_cut = S.beam_cut;
     const int n_claim = min(S.n_claim, p.FCAP);
+    if (p.alpha <= 0 || n_claim <= p.alpha) {   // max-active cannot bind: n_in <= n_claim
+      if (tid == 0) {
+        S.n_in = -1;
+        S.use_alpha = 0;
+        S.kalpha = INFINITY;
+      }
+      __syncthreads();
+      return;
+    }
     long long cnt = 0;
     for (int i = tid; i < n_claim; i += BS) {
       float c = key_cost(read_slot(claim[i].x));
@@ -434,13 +444,11 @@ struct Frame {
       const int n_claim = min(S.n_claim, p.FCAP);
       for (int i = tid; i < n_claim; i += BS) {
         int2 cl = claim[i];
+        if (cl.y >= 0) continue;                  // state has no epsilon arcs
         float c = key_cost(read_slot(cl.x));
         if (!keep(c)) continue;
-        int4 si = __ldg(p.state_info + cl.y);
-        if (si.z > si.y) {
-          int idx = atomicAdd(&S.n_wl, 1);
-          wl[0][idx] = make_int4(cl.x, cl.y, si.y, si.z - si.y);
-        }
+        int idx = atomicAdd(&S.n_wl, 1);
+        wl[0][idx] = make_int2(cl.x, cl.y & 0x7FFFFFFF);
       }
     }
     __syncthreads();
@@ -451,16 +459,17 @@ struct Frame {
       if (n_wl == 0) break;
       if (tid == 0) S.n_wl_next = 0;
       __syncthreads();
-      const int4* W = wl[cur];
-      int4* Wn = wl[cur ^ 1];
+      const int2* W = wl[cur];
+      int2* Wn = wl[cur ^ 1];
       for (int cb = 0; cb < n_wl; cb += BS) {
         int i = cb + tid, deg = 0, eb = 0, slot = 0;
         float cost = 0.f;
         if (i < n_wl) {
-          int4 e = W[i];
+          int2 e = W[i];
           slot = e.x;
-          eb = e.z;
-          deg = e.w;
+          int4 si = __ldg(p.state_info + e.y);
+          eb = si.y;
+          deg = si.z - si.y;
           cost = key_cost(read_slot(slot));
         }
         int A;
@@ -493,15 +502,15 @@ struct Frame {
               bool claimed, improved;
               int sl = insert(q, key, claimed, improved);
               if (sl >= 0) {
-                if (claimed) add_claim(sl, q);
+                const uint32_t has_eps = (uint32_t)arc.w >> 31;
+                if (claimed) add_claim(sl, q, has_eps);
                 if (improved) {
                   wslot = sl;
                   wkey = key;
                   wprev = kEpsFlag | s_aux[k];
-                  int4 si = __ldg(p.state_info + q);
-                  if (si.z > si.y) {
+                  if (has_eps) {
                     int idx = atomicAdd(&S.n_wl_next, 1);
-                    if (idx < p.FCAP) Wn[idx] = make_int4(sl, (int)q, si.y, si.z - si.y);
+                    if (idx < p.FCAP) Wn[idx] = make_int2(sl, (int)q);
                     else S.status = WFST_ERR_CAPACITY;
                   }
                 }
@@ -535,6 +544,7 @@ struct Frame {
     float mn = INFINITY;
     for (int i = tid; i < n_claim; i += BS) {
       int2 cl = claim[i];
+      cl.y &= 0x7FFFFFFF;
       u64 v = read_slot(cl.x);
       if (cl.x < p.C) tab[cl.x] = kEmpty; else ovf[cl.x - p.C] = kEmpty;
       float c = key_cost(v);
@@ -656,7 +666,12 @@ struct Frame {
     const int tid = threadIdx.x;
     if (tid == 0) {
       LaneState& L = S.L;
-      L = LaneState{};
+      // a new utterance: keep the lifetime counters, clear the decode state
+      L.n_front = 0;
+      L.cur = 0;
+      L.frames = 0;
+      L.layer_base = 0;
+      L.rec_used = 0;
       L.status = WFST_OK;
       L.initialized = 1;
       L.front_best = 0.0f;
@@ -668,7 +683,8 @@ struct Frame {
       u64 key = make_key(0.0f, (uint32_t)p.start, kArcNone);
       int slot = insert((uint32_t)p.start, key, claimed, improved);
       if (slot >= 0) {
-        add_claim(slot, (uint32_t)p.start);
+        int4 si = __ldg(p.state_info + p.start);
+        add_claim(slot, (uint32_t)p.start, si.z > si.y ? 1u : 0u);
         prevg[slot] = -1;
       }
       S.best_ord = ord_of(0.0f);
@@ -861,7 +877,7 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ lanes, i
   }
   int nol = 0;
   for (int k = 0; k < len && k < cap; k++) {
-    int32_t ol = __ldg(&p.arcs[arcs_out[(size_t)li * cap + k]].w);
+    int32_t ol = __ldg(&p.arcs[arcs_out[(size_t)li * cap + k]].w) & 0x7FFFFFFF;
     if (ol != 0) {
       if (nol < cap) olab_out[(size_t)li * cap + nol] = ol;
       nol++;
@@ -1020,7 +1036,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   size_t i_slotrec = add(L * FC * 4);
   size_t i_fslot = add(L * FC * sizeof(int2));
   size_t i_ovf = add(L * (size_t)d->C_ovf * 8);
-  size_t i_wl = add(L * 2 * FC * sizeof(int4));
+  size_t i_wl = add(L * 2 * FC * sizeof(int2));
   size_t i_rec = add(L * (size_t)d->R_cap * sizeof(int2));
   size_t i_rcost = d->o.debug_costs ? add(L * (size_t)d->R_cap * 4) : (size_t)-1;
   size_t i_fst = add(L * (size_t)d->TMAX * 3 * 4);
@@ -1061,7 +1077,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.slotrec = (int32_t*)(base + parts[i_slotrec].off);
   kp.fslot = (int2*)(base + parts[i_fslot].off);
   kp.ovf = (u64*)(base + parts[i_ovf].off);
-  kp.wl = (int4*)(base + parts[i_wl].off);
+  kp.wl = (int2*)(base + parts[i_wl].off);
   kp.rec = (int2*)(base + parts[i_rec].off);
   kp.rec_cost = i_rcost != (size_t)-1 ? (float*)(base + parts[i_rcost].off) : nullptr;
   kp.fstats = (float*)(base + parts[i_fst].off);

@@ -114,6 +114,7 @@ wfst_status build_graph(int32_t Q, int32_t start, int64_t E, const int32_t* src,
     if (src[i] < 0 || src[i] >= Q || dst[i] < 0 || dst[i] >= Q)
       return fail(WFST_ERR_GRAPH_INVALID, "arc " + std::to_string(i) + ": dangling state id");
     if (ilabel[i] < 0) return fail(WFST_ERR_GRAPH_INVALID, "arc " + std::to_string(i) + ": negative ilabel");
+    if (olabel[i] < 0) return fail(WFST_ERR_GRAPH_INVALID, "arc " + std::to_string(i) + ": negative olabel");
     if (std::isnan(weight[i]) || std::isinf(weight[i]))
       return fail(WFST_ERR_GRAPH_INVALID, "arc " + std::to_string(i) + ": non-finite weight");
     n_all[src[i]]++;
@@ -160,6 +161,12 @@ wfst_status build_graph(int32_t Q, int32_t start, int64_t E, const int32_t* src,
     r.z = ilabel[i] - 1;  // -1 for epsilon
     r.w = olabel[i];
     arcs[k] = r;
+  }
+  // bit 31 of the olabel field: "the destination state has epsilon arcs" (lets the kernel
+  // build epsilon worklists without gathering state records)
+  for (int64_t k = 0; k < E; k++) {
+    int32_t d = arcs[k].x;
+    if (n_all[d] > n_emit[d]) arcs[k].w |= (int32_t)0x80000000;
   }
   if (eps_has_nonpositive_cycle(Q, first, n_emit, g->h_dst.data(), cw.data())) {
     delete g;
