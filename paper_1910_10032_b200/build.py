@@ -15,7 +15,8 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libwfst_gpu.so")
 SOURCES = ["graph.cu", "decoder.cu", "synth.cu"]
-HEADERS = [os.path.join(ROOT, "include", "wfst_gpu.h"), os.path.join(CSRC, "wfst_internal.h")]
+HEADERS = [os.path.join(ROOT, "include", "wfst_gpu.h"), os.path.join(CSRC, "wfst_internal.h"),
+           os.path.join(CSRC, "frame_kernel.cuh")]
 NVCC = os.environ.get("NVCC", "nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "--fmad=false",

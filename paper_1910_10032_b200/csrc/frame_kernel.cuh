@@ -1,0 +1,1000 @@
+// frame_kernel.cuh -- device code of the decoder (rows a1-a7 of SURVEY §8); included by decoder.cu.
+//
+// One persistent CTA per SM owns one lane (stream) at a time and runs whole frames with CTA
+// barriers only between phases: warp-centric load-balanced emitting expansion, running
+// best + beam and exact max-active, epsilon closure to a fixed point under the
+// fixed cutoff, contraction into a cost-ordered frontier of one representative per
+// state with traceback records.  Lanes are re-queued every K frames.
+// DESIGN.md §5 explains the layout.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "wfst_internal.h"
+
+namespace wfst_dev {
+
+typedef unsigned long long u64;
+using wfst::kArcMask;
+using wfst::kArcNone;
+
+constexpr u64 kEmpty = 0xFFFFFFFFFFFFFFFFull;
+constexpr int kNB = 1024;          // cost bins of the max-active bound
+constexpr int kMaxProbeS = 32;     // buckets probed in the on-chip table before overflowing
+constexpr int kMaxProbeG = 512;    // buckets probed in the global overflow table
+constexpr int32_t kEpsFlag = (int32_t)0x80000000;
+constexpr int kModeFrames = 0, kModeInit = 1;
+constexpr int kBig = 64;           // tokens with more emitting arcs are expanded CTA-wide
+constexpr int kBigCap = 256;
+constexpr int kNBuck = 16;         // cost buckets ordering the next frontier
+
+struct LaneState {
+  int32_t status;       // wfst_status, sticky
+  int32_t initialized;
+  int32_t n_front;      // survivors in the current frontier
+  int32_t cur;          // frontier buffer holding them
+  int32_t frames;       // frames decoded in this utterance
+  int32_t layer_base;   // record index of the current layer's first survivor
+  int32_t rec_used;
+  float front_best;     // min cost of the current survivors
+  u64 emit_arcs, eps_arcs, eps_relax, cand, surv, ovf, alpha_frames, frames_total;
+};
+
+struct KParams {
+  const int4* __restrict__ state_info;   // {e_begin, e_end, eps_end, final bits}
+  const int4* __restrict__ arcs;         // {dst, weight bits, pdf, olabel | dst_has_eps << 31}
+  int32_t start;
+  const float* ll;
+  int32_t T, B, P;
+  const int32_t* lanes;   // batch index -> lane id
+  int32_t mode, K, n_items;
+  int32_t* q_head;
+  int32_t* lane_round;
+  float beam;
+  int32_t alpha;
+  int32_t C, NBK, C_ovf, FCAP, LOGCAP;
+  int64_t R_cap;
+  int32_t TMAX;
+  LaneState* lanes_st;
+  int4* front;        // [lane][2][FCAP]  {state, cost bits, e_begin, n_emit}, cost-ordered
+  uint32_t* claim;    // [lane][FCAP]     slot | has_eps << 31, one per distinct state
+  u64* win;           // [lane][FCAP]     per slot: (arc << 32) | back-pointer of the winner
+  int4* log;          // [lane][LOGCAP]   improvements {slot, ord(cost), arc, back-pointer}
+  int32_t* slotrec;   // [lane][FCAP]     slot -> survivor index
+  int4* tmpA;         // [lane][FCAP]     contraction scratch {state, cost, e_begin, n_emit}
+  int4* tmpB;         // [lane][FCAP]     contraction scratch {slot, arc, prev, bucket}
+  u64* ovf;           // [lane][C_ovf]    global overflow token table
+  uint32_t* wl;       // [lane][2][FCAP]  epsilon worklists (slots)
+  int32_t* epsfix;    // [lane][FCAP]     survivor positions whose back-pointer is an eps slot
+  int2* rec;          // [lane][R_cap]    traceback records {arc, prev}
+  float* rec_cost;    // [lane][R_cap]    (debug) survivor cost
+  float* fstats;      // [lane][TMAX][3]
+  long long* fcounts; // [lane][TMAX][5]
+  int2* layer_info;   // [lane][TMAX+1]   {record base, survivors}
+};
+
+struct SmemCtl {
+  int32_t item, lane, b, status;
+  uint32_t best_ord;
+  int32_t theta;
+  int32_t n_claim, n_claim_emit, n_ovf, n_surv, n_in, n_wl, n_wl_next, n_log, n_big, n_fix;
+  float beam_cut, kalpha, ref, inv_w, min_surv, bk_ref, bk_inv;
+  int32_t use_alpha;
+  int32_t radix_prefix, radix_k;
+  long long emit_arcs, eps_deg, eps_relax;
+  int32_t bucket_base[kNBuck];
+  int32_t warp_tmp[32];
+  long long warp_tmp64[32];
+  int32_t big[kBigCap];
+  LaneState L;
+};
+
+// ---------------- primitives ----------------
+__device__ __forceinline__ uint32_t ord_of(float c) {
+  uint32_t b = __float_as_uint(c);
+  return b ^ ((b & 0x80000000u) ? 0xFFFFFFFFu : 0x80000000u);
+}
+__device__ __forceinline__ float float_of_ord(uint32_t o) {
+  uint32_t b = (o & 0x80000000u) ? (o ^ 0x80000000u) : ~o;
+  return __uint_as_float(b);
+}
+__device__ __forceinline__ uint32_t bucket_of(uint32_t q, uint32_t nb) { return __umulhi(q * 0x9E3779B1u, nb); }
+__device__ __forceinline__ float key_cost(u64 k) { return float_of_ord((uint32_t)(k >> 32)); }
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ u64 lds64(uint32_t a) {
+  u64 v;
+  asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void lds64x2(uint32_t a, u64& x, u64& y) {
+  asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void sts64(uint32_t a, u64 v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 atom_cas_s(uint32_t a, u64 cmp, u64 v) {
+  u64 old;
+  asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "r"(a), "l"(cmp), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ u64 atom_min_s(uint32_t a, u64 v) {
+  u64 old;
+  asm volatile("atom.shared.min.u64 %0, [%1], %2;" : "=l"(old) : "r"(a), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ int atom_add_s(uint32_t a, int v) {
+  int old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void atom_min_s32(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_s(uint32_t a, int v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int lds32(uint32_t a) {
+  int v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 ldg_volatile64(const u64* p) { return *(const volatile u64*)p; }
+
+// monotone cost -> bin map, used both to count and to reject
+__device__ __forceinline__ int bin_of(float c, float ref, float inv_w) {
+  float x = __fmul_rn(__fsub_rn(c, ref), inv_w);
+  x = fminf(fmaxf(x, 0.0f), (float)(kNB - 1));
+  return (int)x;
+}
+
+// Insert (state q, key = ord(cost) << 32 | q) into a table of nb buckets of 4 slots.
+// Returns the slot, or -1 when the probe limit is reached.  claimed: the slot was empty.
+// logit: the key is <= the slot value it met (an improvement or a tie -- both are logged so
+// the winner's (arc, back-pointer) can be chosen after the frame, R9).  strict: key < old.
+__device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q, u64 key, bool& claimed,
+                                        bool& logit, bool& strict) {
+  uint32_t b = bucket_of(q, nb);
+  claimed = logit = strict = false;
+#pragma unroll 1
+  for (int p = 0; p < kMaxProbeS; ++p) {
+    const uint32_t ba = tab_sa + b * 32u;
+    u64 x[4];
+    lds64x2(ba, x[0], x[1]);
+    lds64x2(ba + 16, x[2], x[3]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((uint32_t)x[j] == q && x[j] != kEmpty) {
+        u64 old = atom_min_s(ba + 8 * j, key);
+        logit = key <= old;
+        strict = key < old;
+        return (int)(b * 4 + j);
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (x[j] == kEmpty) {
+        u64 old = atom_cas_s(ba + 8 * j, kEmpty, key);
+        if (old == kEmpty) {
+          claimed = logit = strict = true;
+          return (int)(b * 4 + j);
+        }
+        if ((uint32_t)old == q) {
+          old = atom_min_s(ba + 8 * j, key);
+          logit = key <= old;
+          strict = key < old;
+          return (int)(b * 4 + j);
+        }
+      }
+    b = (b + 1 == nb) ? 0 : b + 1;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ int insert_g(u64* tab, uint32_t nb, uint32_t q, u64 key, bool& claimed, bool& logit,
+                                        bool& strict) {
+  uint32_t b = bucket_of(q, nb);
+  claimed = logit = strict = false;
+#pragma unroll 1
+  for (int p = 0; p < kMaxProbeG; ++p) {
+    u64* bk = tab + (size_t)b * 4;
+    u64 x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = ldg_volatile64(bk + j);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((uint32_t)x[j] == q && x[j] != kEmpty) {
+        u64 old = atomicMin(bk + j, key);
+        logit = key <= old;
+        strict = key < old;
+        return (int)(b * 4 + j);
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (x[j] == kEmpty) {
+        u64 old = atomicCAS(bk + j, kEmpty, key);
+        if (old == kEmpty) {
+          claimed = logit = strict = true;
+          return (int)(b * 4 + j);
+        }
+        if ((uint32_t)old == q) {
+          old = atomicMin(bk + j, key);
+          logit = key <= old;
+          strict = key < old;
+          return (int)(b * 4 + j);
+        }
+      }
+    b = (b + 1 == nb) ? 0 : b + 1;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ int warp_incl_scan(int x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// warp-aggregated append to a shared counter: returns this lane's index (or -1 if !need)
+__device__ __forceinline__ int warp_append(bool need, uint32_t counter_sa) {
+  const int lane = threadIdx.x & 31;
+  unsigned m = __ballot_sync(0xffffffffu, need);
+  if (m == 0) return -1;
+  int leader = __ffs(m) - 1, base = 0;
+  if (lane == leader) base = atom_add_s(counter_sa, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return need ? base + __popc(m & ((1u << lane) - 1u)) : -1;
+}
+
+template <int BS>
+__device__ __forceinline__ long long block_sum64(long long v, long long* s_tmp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) s_tmp[w] = v;
+  __syncthreads();
+  long long t = 0;
+#pragma unroll
+  for (int i = 0; i < BS / 32; i++) t += s_tmp[i];
+  __syncthreads();
+  return t;
+}
+
+// ---------------- one lane's frames ----------------
+template <int BS, int R>
+struct Frame {
+  static constexpr int NW = BS / 32;
+  const KParams& p;
+  SmemCtl& S;
+  uint32_t tab_sa;   // shared address of the token table
+  uint32_t hist_sa;  // shared address of the cost histogram (kNB ints)
+  int* hist;         // same, generic (reads)
+  int* wbuf;         // this warp's owner buffer (32 ints, -1 when idle)
+  // lane buffers
+  int4* F0;   // frontier buffer 0; buffer 1 follows at +FCAP
+  uint32_t* claim;
+  u64* win;
+  int4* lg;
+  int32_t* slotrec;
+  int4* tmpA;
+  int4* tmpB;
+  u64* ovf;
+  uint32_t* wl0;  // epsilon worklist 0; worklist 1 follows at +FCAP
+  int32_t* epsfix;
+  int2* rec;
+  float* rec_cost;
+
+  __device__ Frame(const KParams& p_, SmemCtl& S_, uint32_t tab_sa_, int* hist_, int* wbuf_)
+      : p(p_), S(S_), tab_sa(tab_sa_), hist_sa(saddr(hist_)), hist(hist_), wbuf(wbuf_) {}
+
+  __device__ void bind(int lane) {
+    size_t L = (size_t)lane, FC = (size_t)p.FCAP;
+    F0 = p.front + L * 2 * FC;
+    claim = p.claim + L * FC;
+    win = p.win + L * FC;
+    lg = p.log + L * (size_t)p.LOGCAP;
+    slotrec = p.slotrec + L * FC;
+    tmpA = p.tmpA + L * FC;
+    tmpB = p.tmpB + L * FC;
+    ovf = p.ovf + L * (size_t)p.C_ovf;
+    wl0 = p.wl + L * 2 * FC;
+    epsfix = p.epsfix + L * FC;
+    rec = p.rec + L * (size_t)p.R_cap;
+    rec_cost = p.rec_cost ? p.rec_cost + L * (size_t)p.R_cap : nullptr;
+  }
+
+  __device__ __forceinline__ u64 read_slot(int slot) const {
+    return slot < p.C ? lds64(tab_sa + 8u * (uint32_t)slot) : ldg_volatile64(ovf + (slot - p.C));
+  }
+  __device__ __forceinline__ void clear_slot(int slot) const {
+    if (slot < p.C) sts64(tab_sa + 8u * (uint32_t)slot, kEmpty);
+    else ovf[slot - p.C] = kEmpty;
+  }
+  __device__ __forceinline__ bool keep(float c) const {
+    return c < S.beam_cut && (!S.use_alpha || c <= S.kalpha);
+  }
+
+  __device__ __forceinline__ int insert(uint32_t q, u64 key, bool& claimed, bool& logit, bool& strict) {
+    int s = insert_s(tab_sa, (uint32_t)p.NBK, q, key, claimed, logit, strict);
+    if (s >= 0) return s;
+    s = insert_g(ovf, (uint32_t)(p.C_ovf / 4), q, key, claimed, logit, strict);
+    if (s < 0) {
+      S.status = WFST_ERR_CAPACITY;
+      return -1;
+    }
+    if (claimed) atomicAdd(&S.n_ovf, 1);
+    return s + p.C;
+  }
+
+  // Record a claim and/or an improvement (warp-collective: every lane of the warp calls it).
+  __device__ __forceinline__ void record(int slot, bool claimed, bool logit, uint32_t eps_flag, uint32_t ord,
+                                         uint32_t arc, int32_t prev, int bin) {
+    int ci = warp_append(claimed, saddr(&S.n_claim));
+    if (claimed) {
+      if (ci < p.FCAP) {
+        claim[ci] = (uint32_t)slot | (eps_flag << 31);
+        win[slot] = kEmpty;
+      } else {
+        S.status = WFST_ERR_CAPACITY;
+      }
+      if (bin >= 0) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
+    }
+    int li = warp_append(logit, saddr(&S.n_log));
+    if (logit) {
+      if (li < p.LOGCAP) lg[li] = make_int4(slot, (int)ord, (int)arc, prev);
+      else S.status = WFST_ERR_CAPACITY;
+    }
+  }
+
+  // theta = smallest b such that >= alpha distinct states have first-insert bin < b (warp-collective)
+  __device__ void update_theta() {
+    const int lane = threadIdx.x & 31;
+    const int base = lane * (kNB / 32);
+    int s = 0;
+#pragma unroll 8
+    for (int i = 0; i < kNB / 32; i++) s += lds32(hist_sa + 4u * (base + i));
+    int incl = warp_incl_scan(s);
+    unsigned m = __ballot_sync(0xffffffffu, incl >= p.alpha);
+    if (m == 0) return;
+    const int L = __ffs(m) - 1;
+    if (lane == L) {
+      int c = incl - s;
+      for (int i = 0; i < kNB / 32; i++) {
+        c += lds32(hist_sa + 4u * (base + i));
+        if (c >= p.alpha) {
+          atomicMin(&S.theta, base + i + 1);
+          break;
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  // candidate filter + insert for one emitting arc (all lanes call; v = lane has an arc)
+  __device__ __forceinline__ void emit_one(bool v, float c, const int4& arc, int32_t prev, float ref, float inv_w,
+                                           uint32_t best_sa, uint32_t theta_sa) {
+    bool claimed = false, logit = false, strict = false;
+    int slot = -1, bin = -1;
+    uint32_t o = 0;
+    if (v) {
+      const uint32_t bo = (uint32_t)lds32(best_sa);
+      bool ok = !(bo != 0xFFFFFFFFu && !(c < __fadd_rn(float_of_ord(bo), p.beam)));
+      if (ok) {
+        bin = bin_of(c, ref, inv_w);
+        ok = bin < lds32(theta_sa);
+      }
+      if (ok) {
+        o = ord_of(c);
+        if (o < bo) atom_min_s32(best_sa, o);
+        const uint32_t q = (uint32_t)arc.x;
+        slot = insert(q, ((u64)o << 32) | q, claimed, logit, strict);
+        if (slot < 0) claimed = logit = false;
+      }
+    }
+    record(slot, claimed, logit, (uint32_t)arc.w >> 31, o, 0u, prev, bin);
+  }
+
+  // ---- rows a1 + a2: load-balanced emitting expansion ----
+  // Each warp takes 32 frontier tokens, scans their emitting degrees, and walks the flattened
+  // arcs 32*R at a time; the owner of arc j is found from head flags + a max-scan (no search).
+  __device__ void expand(const float* __restrict__ row) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_f = S.L.n_front;
+    const int4* Fin = F0 + (size_t)S.L.cur * p.FCAP;
+    const int32_t layer_base = S.L.layer_base;
+    const float ref = S.ref, inv_w = S.inv_w;
+    const uint32_t best_sa = saddr(&S.best_ord), theta_sa = saddr(&S.theta), nclaim_sa = saddr(&S.n_claim);
+    long long arcs_total = 0;
+    int last_theta = 0;
+    for (int tb = warp * 32; tb < n_f; tb += NW * 32) {
+      const int i = tb + lane;
+      int deg = 0, eb = 0;
+      float cost = 0.f;
+      if (i < n_f) {
+        int4 f = __ldcg(Fin + i);
+        eb = f.z;
+        deg = f.w;
+        cost = __int_as_float(f.y);
+      }
+      arcs_total += deg;
+      if (deg > kBig) {
+        int k = atomicAdd(&S.n_big, 1);
+        if (k < kBigCap) {
+          S.big[k] = i;
+          deg = 0;
+        }
+      }
+      const int incl = warp_incl_scan(deg);
+      const int excl = incl - deg;
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      for (int r0 = 0; r0 < total; r0 += 32 * R) {
+        int a[R], own[R];
+        bool v[R];
+#pragma unroll
+        for (int u = 0; u < R; u++) {
+          const int w0 = r0 + u * 32;
+          if (deg > 0 && excl >= w0 && excl < w0 + 32) wbuf[excl - w0] = lane;
+          const unsigned cm = __ballot_sync(0xffffffffu, deg > 0 && excl <= w0 && w0 < incl);
+          __syncwarp();
+          int o = wbuf[lane];
+          __syncwarp();
+          wbuf[lane] = -1;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, o, d);
+            if (lane >= d) o = max(o, y);
+          }
+          if (cm) o = max(o, __ffs(cm) - 1);
+          own[u] = o & 31;
+          const int j = w0 + lane;
+          v[u] = j < total;
+          const int eb_o = __shfl_sync(0xffffffffu, eb, own[u]);
+          const int ex_o = __shfl_sync(0xffffffffu, excl, own[u]);
+          a[u] = eb_o + (j - ex_o);
+          __syncwarp();
+        }
+        int4 arc[R];
+#pragma unroll
+        for (int u = 0; u < R; u++) arc[u] = v[u] ? __ldg(p.arcs + a[u]) : make_int4(0, 0, 0, 0);
+        float L[R];
+#pragma unroll
+        for (int u = 0; u < R; u++) L[u] = v[u] ? __ldg(row + arc[u].z) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < R; u++) {
+          const float co = __shfl_sync(0xffffffffu, cost, own[u]);
+          float c = __fadd_rn(__fsub_rn(__fadd_rn(co, __int_as_float(arc[u].y)), L[u]), 0.0f);
+          emit_one(v[u], c, arc[u], layer_base + tb + own[u], ref, inv_w, best_sa, theta_sa);
+        }
+        if (p.alpha > 0) {
+          const int nc = __shfl_sync(0xffffffffu, lds32(nclaim_sa), 0);
+          if (nc >= p.alpha && nc - last_theta >= 512) {
+            update_theta();
+            last_theta = nc;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // tokens with large out-degree (hub states): all threads share their arcs
+    const int nbig = min(S.n_big, kBigCap);
+    for (int k = 0; k < nbig; k++) {
+      const int i = S.big[k];
+      const int4 f = __ldcg(Fin + i);
+      const float cost = __int_as_float(f.y);
+      const int deg = f.w;
+      for (int j0 = 0; j0 < deg; j0 += BS * R) {
+        int4 arc[R];
+        bool v[R];
+#pragma unroll
+        for (int u = 0; u < R; u++) {
+          const int j = j0 + u * BS + tid;
+          v[u] = j < deg;
+          arc[u] = v[u] ? __ldg(p.arcs + f.z + j) : make_int4(0, 0, 0, 0);
+        }
+        float L[R];
+#pragma unroll
+        for (int u = 0; u < R; u++) L[u] = v[u] ? __ldg(row + arc[u].z) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < R; u++) {
+          float c = __fadd_rn(__fsub_rn(__fadd_rn(cost, __int_as_float(arc[u].y)), L[u]), 0.0f);
+          emit_one(v[u], c, arc[u], layer_base + i, ref, inv_w, best_sa, theta_sa);
+        }
+        if (p.alpha > 0 && warp == 0) {
+          const int nc = __shfl_sync(0xffffffffu, lds32(nclaim_sa), 0);
+          if (nc >= p.alpha) update_theta();
+        }
+        __syncwarp();
+      }
+    }
+    arcs_total = block_sum64<BS>(arcs_total, S.warp_tmp64);
+    if (tid == 0) S.emit_arcs = arcs_total;
+    __syncthreads();
+  }
+
+  // ---- row a3: beam + exact max-active (readings R5, R6) ----
+  __device__ void select_cutoff() {
+    const int tid = threadIdx.x;
+    const float beam_cut = S.beam_cut;
+    const int n_claim = min(S.n_claim, p.FCAP);
+    if (p.alpha <= 0 || n_claim <= p.alpha) {   // max-active cannot bind (n_in <= n_claim)
+      if (tid == 0) {
+        S.n_in = -1;
+        S.use_alpha = 0;
+        S.kalpha = INFINITY;
+      }
+      __syncthreads();
+      return;
+    }
+    long long cnt = 0;
+    for (int i = tid; i < n_claim; i += BS) {
+      const int slot = (int)(claim[i] & 0x7FFFFFFFu);
+      if (key_cost(read_slot(slot)) < beam_cut) cnt++;
+    }
+    const long long n_in = block_sum64<BS>(cnt, S.warp_tmp64);
+    if (tid == 0) {
+      S.n_in = (int)n_in;
+      S.use_alpha = 0;
+      S.kalpha = INFINITY;
+      S.radix_prefix = 0;
+      S.radix_k = p.alpha;
+    }
+    __syncthreads();
+    if (n_in <= p.alpha) return;
+    // exact alpha-th smallest in-beam cost: 4 radix passes of 8 bits on ord(cost)
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = tid; i < 256; i += BS) hist[i] = 0;
+      __syncthreads();
+      const uint32_t prefix = (uint32_t)S.radix_prefix;
+      const uint32_t hmask = (shift == 24) ? 0u : (0xFFFFFFFFu << (shift + 8));
+      for (int i = tid; i < n_claim; i += BS) {
+        const int slot = (int)(claim[i] & 0x7FFFFFFFu);
+        const u64 v = read_slot(slot);
+        if (!(key_cost(v) < beam_cut)) continue;
+        const uint32_t o = (uint32_t)(v >> 32);
+        if ((o & hmask) == (prefix & hmask)) red_add_s(hist_sa + 4u * ((o >> shift) & 255u), 1);
+      }
+      __syncthreads();
+      if (tid < 32) {   // warp 0: locate the digit holding rank k
+        const int lane = tid;
+        int k = S.radix_k;
+        int s = 0;
+        for (int i = 0; i < 8; i++) s += hist[lane * 8 + i];
+        const int incl = warp_incl_scan(s);
+        const unsigned m = __ballot_sync(0xffffffffu, incl >= k);
+        const int L = __ffs(m) - 1;
+        if (lane == L) {
+          int c = incl - s;
+          int d = lane * 8;
+          for (; d < lane * 8 + 8; d++) {
+            if (c + hist[d] >= k) break;
+            c += hist[d];
+          }
+          S.radix_k = k - c;
+          S.radix_prefix = (int)(prefix | ((uint32_t)d << shift));
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      S.kalpha = float_of_ord((uint32_t)S.radix_prefix);
+      S.use_alpha = 1;
+    }
+    for (int i = tid; i < kNB; i += BS) hist[i] = 0;
+    __syncthreads();
+  }
+
+  // ---- row a5: epsilon closure under the fixed cutoff (reading R7) ----
+  __device__ void eps_closure() {
+    const int tid = threadIdx.x;
+    const int n_claim = min(S.n_claim, p.FCAP);
+    const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
+    for (int i0 = 0; i0 < n_claim; i0 += BS) {   // warp-uniform trip count (warp_append)
+      const int i = i0 + tid;
+      const uint32_t cl = i < n_claim ? claim[i] : 0u;
+      bool need = false;
+      if (cl & 0x80000000u) {
+        const float c = key_cost(read_slot((int)(cl & 0x7FFFFFFFu)));
+        need = c < cut_b && c <= cut_a;
+      }
+      const int idx = warp_append(need, saddr(&S.n_wl));
+      if (need) wl0[idx] = cl & 0x7FFFFFFFu;
+    }
+    __syncthreads();
+    int cur = 0;
+    long long relax = 0;
+    while (true) {
+      const int n_wl = S.n_wl;
+      if (n_wl == 0) break;
+      __syncthreads();
+      if (tid == 0) S.n_wl_next = 0;
+      __syncthreads();
+      const uint32_t* W = wl0 + (size_t)cur * p.FCAP;
+      uint32_t* Wn = wl0 + (size_t)(cur ^ 1) * p.FCAP;
+      for (int i0 = 0; i0 < n_wl; i0 += BS) {
+        const int i = i0 + tid;
+        int e0 = 0, e1 = 0, src_slot = 0;
+        float cp = 0.f;
+        if (i < n_wl) {
+          src_slot = (int)W[i];
+          const u64 v = read_slot(src_slot);
+          cp = key_cost(v);
+          const int4 si = __ldg(p.state_info + (uint32_t)v);
+          e0 = si.y;
+          e1 = si.z;
+        }
+        // each thread relaxes its token's epsilon arcs (epsilon out-degrees are small)
+        int n_more = e1 - e0;
+        int maxd = n_more;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) maxd = max(maxd, __shfl_xor_sync(0xffffffffu, maxd, o));
+        for (int k = 0; k < maxd; k++) {
+          const bool v = k < n_more;
+          int4 arc = make_int4(0, 0, 0, 0);
+          bool claimed = false, logit = false, strict = false;
+          int slot = -1;
+          uint32_t o = 0;
+          if (v) {
+            arc = __ldg(p.arcs + e0 + k);
+            const float c = __fadd_rn(__fadd_rn(cp, __int_as_float(arc.y)), 0.0f);
+            relax++;
+            if (keep(c)) {
+              o = ord_of(c);
+              const uint32_t q = (uint32_t)arc.x;
+              slot = insert(q, ((u64)o << 32) | q, claimed, logit, strict);
+              if (slot < 0) claimed = logit = strict = false;
+            }
+          }
+          const uint32_t has_eps = (uint32_t)arc.w >> 31;
+          record(slot, claimed, logit, has_eps, o, (uint32_t)(e0 + k), kEpsFlag | src_slot, -1);
+          const bool push = strict && has_eps;
+          const int wi = warp_append(push, saddr(&S.n_wl_next));
+          if (push) {
+            if (wi < p.FCAP) Wn[wi] = (uint32_t)slot;
+            else S.status = WFST_ERR_CAPACITY;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) S.n_wl = min(S.n_wl_next, p.FCAP);
+      cur ^= 1;
+      __syncthreads();
+    }
+    const long long tot = block_sum64<BS>(relax, S.warp_tmp64);
+    if (tid == 0) S.eps_relax = tot;
+  }
+
+  // winner of each slot = min (arc, back-pointer) among logged entries whose cost equals the
+  // slot's final cost (R9: ties broken by arc id)
+  __device__ void resolve_winners() {
+    const int tid = threadIdx.x;
+    const int n_log = min(S.n_log, p.LOGCAP);
+    constexpr int U = 4;
+    for (int i0 = 0; i0 < n_log; i0 += BS * U) {
+      int4 e[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int i = i0 + u * BS + tid;
+        e[u] = i < n_log ? __ldcg(lg + i) : make_int4(-1, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        if (e[u].x < 0) continue;
+        const u64 v = read_slot(e[u].x);
+        if ((uint32_t)(v >> 32) == (uint32_t)e[u].y)
+          atomicMin(win + e[u].x, ((u64)(uint32_t)e[u].z << 32) | (uint32_t)e[u].w);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- rows a4 + a6: contraction into the next frontier (cost-bucketed) + records ----
+  __device__ void contract() {
+    const int tid = threadIdx.x;
+    const int n_claim = min(S.n_claim, p.FCAP);
+    if (tid < kNBuck) S.bucket_base[tid] = 0;
+    if (tid == 0) {
+      S.n_surv = 0;
+      S.n_fix = 0;
+      // bucket range: [best, cutoff)
+      const float best = float_of_ord(S.best_ord);
+      float cut = S.use_alpha ? fminf(S.beam_cut, S.kalpha) : S.beam_cut;
+      float span = __fsub_rn(cut, best);
+      if (!(span > 0.0f) || isinf(span)) span = 32.0f;
+      S.bk_ref = best;
+      S.bk_inv = (float)kNBuck / span;
+    }
+    __syncthreads();
+    long long epsd = 0;
+    float mn = INFINITY;
+    const float bk_ref = S.bk_ref, bk_inv = S.bk_inv;
+    const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
+    constexpr int U = 4;
+    // pass 1: keep() over the claims, gather state records, stage survivors
+    for (int i0 = 0; i0 < n_claim; i0 += BS * U) {
+      int slot[U];
+      u64 v[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int i = i0 + u * BS + tid;
+        slot[u] = i < n_claim ? (int)(__ldcg(claim + i) & 0x7FFFFFFFu) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        v[u] = slot[u] >= 0 ? read_slot(slot[u]) : kEmpty;
+        if (slot[u] >= 0) clear_slot(slot[u]);
+      }
+      int4 si[U];
+      u64 w[U];
+      bool k[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const float cu = key_cost(v[u]);
+        k[u] = slot[u] >= 0 && cu < cut_b && cu <= cut_a;
+        si[u] = k[u] ? __ldg(p.state_info + (uint32_t)v[u]) : make_int4(0, 0, 0, 0);
+        w[u] = k[u] ? __ldcg(win + slot[u]) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int r = warp_append(k[u], saddr(&S.n_surv));
+        if (!k[u]) continue;
+        if (r >= p.FCAP) {
+          S.status = WFST_ERR_CAPACITY;
+          continue;
+        }
+        const float c = key_cost(v[u]);
+        int bk = (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1));
+        red_add_s(saddr(&S.bucket_base[bk]), 1);
+        tmpA[r] = make_int4((int)(uint32_t)v[u], __float_as_int(c), si[u].x, si[u].y - si[u].x);
+        tmpB[r] = make_int4(slot[u], (int)(uint32_t)(w[u] >> 32), (int)(uint32_t)w[u], bk);
+        epsd += si[u].z - si[u].y;
+        mn = fminf(mn, c);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if ((tid & 31) == 0) S.warp_tmp[tid >> 5] = __float_as_int(mn);
+    const long long eps_deg = block_sum64<BS>(epsd, S.warp_tmp64);
+    if (tid == 0) {
+      float m = INFINITY;
+      for (int w = 0; w < NW; w++) m = fminf(m, __int_as_float(S.warp_tmp[w]));
+      S.min_surv = m;
+      S.eps_deg = eps_deg;
+      int acc = 0;
+      for (int b = 0; b < kNBuck; b++) {
+        const int n = S.bucket_base[b];
+        S.bucket_base[b] = acc;
+        acc += n;
+      }
+    }
+    __syncthreads();
+    const int n_surv = min(S.n_surv, p.FCAP);
+    const int32_t rb = S.L.rec_used;
+    if ((long long)rb + n_surv > p.R_cap) {
+      if (tid == 0) S.status = WFST_ERR_CAPACITY;
+      __syncthreads();
+      return;
+    }
+    int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
+    // pass 2: place survivors in cost-bucket order; records {arc, prev}
+    for (int r = tid; r < n_surv; r += BS) {
+      const int4 A = tmpA[r];
+      const int4 Bv = tmpB[r];
+      const int pos = atom_add_s(saddr(&S.bucket_base[Bv.w]), 1);
+      Fout[pos] = A;
+      slotrec[Bv.x] = pos;
+      const int32_t arc = (uint32_t)Bv.y == 0xFFFFFFFFu ? -1 : Bv.y;
+      int32_t pv = Bv.z;
+      if (pv < -1) {   // epsilon back-pointer: a slot of this layer, resolved in pass 3
+        const int fi = atomicAdd(&S.n_fix, 1);
+        epsfix[fi] = pos;
+      }
+      rec[rb + pos] = make_int2(arc, pv);
+      if (rec_cost) rec_cost[rb + pos] = __int_as_float(A.y);
+    }
+    __syncthreads();
+    // pass 3: epsilon back-pointers -> record index of the source survivor
+    const int n_fix = S.n_fix;
+    for (int k = tid; k < n_fix; k += BS) {
+      const int pos = epsfix[k];
+      int2 e = rec[rb + pos];
+      e.y = rb + slotrec[e.y & 0x7FFFFFFF];
+      rec[rb + pos] = e;
+    }
+    __syncthreads();
+  }
+
+  __device__ void begin_frame(float beam_cut_fixed) {
+    const int tid = threadIdx.x;
+    for (int i = tid; i < kNB; i += BS) hist[i] = 0;
+    if (tid == 0) {
+      S.best_ord = 0xFFFFFFFFu;
+      S.theta = kNB;
+      S.n_claim = 0;
+      S.n_ovf = 0;
+      S.n_log = 0;
+      S.n_big = 0;
+      S.n_wl = 0;
+      S.use_alpha = 0;
+      S.kalpha = INFINITY;
+      S.beam_cut = beam_cut_fixed;
+      S.emit_arcs = 0;
+      S.eps_relax = 0;
+      S.n_in = -1;
+      const float half = isinf(p.beam) ? 32.0f : 0.5f * p.beam;
+      S.ref = S.L.front_best - half;
+      S.inv_w = (float)kNB / (4.0f * half);
+    }
+    __syncthreads();
+  }
+
+  __device__ void clear_all() {
+    for (int i = threadIdx.x; i < p.C; i += BS) sts64(tab_sa + 8u * i, kEmpty);
+    for (int i = threadIdx.x; i < p.C_ovf; i += BS) ovf[i] = kEmpty;
+    __syncthreads();
+  }
+
+  __device__ void finish_frame(int t, bool emitting) {
+    const int tid = threadIdx.x;
+    if (S.status != WFST_OK) clear_all();
+    if (tid == 0) {
+      LaneState& L = S.L;
+      const int n_surv = min(S.n_surv, p.FCAP);
+      if (S.status != WFST_OK) L.status = S.status;
+      if (L.status == WFST_OK) {
+        L.layer_base = L.rec_used;
+        L.rec_used += n_surv;
+        L.n_front = n_surv;
+        L.cur ^= 1;
+        L.front_best = S.min_surv;
+        const int layer = emitting ? L.frames + 1 : 0;
+        if (emitting) L.frames++;
+        L.eps_arcs += S.eps_deg;
+        L.eps_relax += S.eps_relax;
+        L.cand += S.n_claim;
+        L.surv += n_surv;
+        L.ovf += S.n_ovf;
+        if (emitting) {
+          L.emit_arcs += S.emit_arcs;
+          L.alpha_frames += S.use_alpha;
+          L.frames_total++;
+        }
+        const size_t lane = (size_t)S.lane;
+        if (layer <= p.TMAX) p.layer_info[lane * (p.TMAX + 1) + layer] = make_int2(L.layer_base, n_surv);
+        if (emitting && t >= 0 && L.frames - 1 < p.TMAX) {
+          const size_t fi = lane * p.TMAX + (L.frames - 1);
+          p.fstats[fi * 3 + 0] = float_of_ord(S.best_ord);
+          p.fstats[fi * 3 + 1] = S.beam_cut;
+          p.fstats[fi * 3 + 2] = S.use_alpha ? S.kalpha : INFINITY;
+          p.fcounts[fi * 5 + 0] = S.n_claim_emit;
+          p.fcounts[fi * 5 + 1] = S.n_in;
+          p.fcounts[fi * 5 + 2] = n_surv;
+          p.fcounts[fi * 5 + 3] = S.emit_arcs;
+          p.fcounts[fi * 5 + 4] = S.eps_deg;
+        }
+      }
+      S.status = WFST_OK;
+    }
+    __syncthreads();
+  }
+
+  // R3: start token + epsilon closure with keep(c) = c < beam
+  __device__ void init_lane() {
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+      LaneState& L = S.L;   // a new utterance: keep the lifetime counters
+      L.n_front = 0;
+      L.cur = 0;
+      L.frames = 0;
+      L.layer_base = 0;
+      L.rec_used = 0;
+      L.status = WFST_OK;
+      L.initialized = 1;
+      L.front_best = 0.0f;
+    }
+    __syncthreads();
+    begin_frame(__fadd_rn(0.0f, p.beam));
+    if (tid < 32) {
+      bool claimed = false, logit = false, strict = false;
+      int slot = -1;
+      const uint32_t o = ord_of(0.0f);
+      uint32_t flag = 0;
+      if (tid == 0) {
+        slot = insert((uint32_t)p.start, ((u64)o << 32) | (uint32_t)p.start, claimed, logit, strict);
+        const int4 si = __ldg(p.state_info + p.start);
+        flag = si.z > si.y ? 1u : 0u;
+        if (slot < 0) claimed = logit = false;
+      }
+      record(slot, claimed, logit, flag, o, 0xFFFFFFFFu, -1, -1);
+      if (tid == 0) {
+        S.best_ord = o;
+        S.n_claim_emit = 1;
+      }
+    }
+    __syncthreads();
+    eps_closure();
+    resolve_winners();
+    contract();
+    finish_frame(-1, false);
+  }
+
+  __device__ void run_frame(int t) {
+    const int tid = threadIdx.x;
+    const float* row = p.ll + ((size_t)t * p.B + S.b) * (size_t)p.P;
+    begin_frame(INFINITY);
+    expand(row);
+    if (tid == 0) {
+      S.n_claim_emit = S.n_claim;
+      if (S.best_ord == 0xFFFFFFFFu) S.status = WFST_ERR_NO_SURVIVOR;
+      else S.beam_cut = __fadd_rn(float_of_ord(S.best_ord), p.beam);
+    }
+    __syncthreads();
+    if (S.status != WFST_OK) {
+      if (tid == 0) S.n_surv = 0;
+      __syncthreads();
+      finish_frame(t, true);   // wipes the tables
+      return;
+    }
+    select_cutoff();
+    eps_closure();
+    resolve_winners();
+    contract();
+    finish_frame(t, true);
+  }
+};
+
+template <int BS, int R>
+__global__ void __launch_bounds__(BS, 1) frame_kernel(KParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ SmemCtl S;
+  __shared__ int s_wbuf[BS];
+  u64* tab = (u64*)smem_raw;
+  int* hist = (int*)(tab + p.C);
+  const int tid = threadIdx.x;
+  const uint32_t tab_sa = saddr(tab);
+  for (int i = tid; i < p.C; i += BS) sts64(tab_sa + 8u * i, kEmpty);
+  s_wbuf[tid] = -1;
+  if (tid == 0) S.status = WFST_OK;
+  __syncthreads();
+  Frame<BS, R> fr(p, S, tab_sa, hist, s_wbuf + (tid & ~31));
+  while (true) {
+    if (tid == 0) S.item = atomicAdd(p.q_head, 1);
+    __syncthreads();
+    const int item = S.item;
+    if (item >= p.n_items) break;
+    const int b = item % p.B, r = item / p.B;
+    const int lane = p.lanes[b];
+    if (tid == 0) {
+      volatile int32_t* lr = p.lane_round + b;
+      while (*lr != r) __nanosleep(64);
+      __threadfence();
+      S.lane = lane;
+      S.b = b;
+      const int* src = (const int*)&p.lanes_st[lane];
+      int* dst = (int*)&S.L;
+      for (int k = 0; k < (int)(sizeof(LaneState) / 4); k++) dst[k] = __ldcg(src + k);
+    }
+    __syncthreads();
+    fr.bind(lane);
+    if (p.mode == kModeInit) {
+      fr.init_lane();
+    } else {
+      const int t_end = min(p.T, (r + 1) * p.K);
+      for (int t = r * p.K; t < t_end; t++) {
+        if (S.L.status != WFST_OK) break;
+        fr.run_frame(t);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      p.lanes_st[lane] = S.L;
+      __threadfence();
+      *(volatile int32_t*)(p.lane_round + b) = r + 1;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace wfst_dev
