@@ -123,6 +123,11 @@ __device__ __forceinline__ u64 atom_min_s(uint32_t a, u64 v) {
   asm volatile("atom.shared.min.u64 %0, [%1], %2;" : "=l"(old) : "r"(a), "l"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ uint32_t atom_min_s_u32(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.min.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ int atom_add_s(uint32_t a, int v) {
   int old;
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
@@ -155,6 +160,7 @@ __device__ __forceinline__ int bin_of(float c, float ref, float inv_w) {
 __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q, u64 key, bool& claimed,
                                         bool& logit, bool& strict) {
   uint32_t b = bucket_of(q, nb);
+  const uint32_t hi = (uint32_t)(key >> 32);
   claimed = logit = strict = false;
 #pragma unroll 1
   for (int p = 0; p < kMaxProbeS; ++p) {
@@ -165,23 +171,25 @@ __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if ((uint32_t)x[j] == q && x[j] != kEmpty) {
-        u64 old = atom_min_s(ba + 8 * j, key);
-        logit = key <= old;
-        strict = key < old;
+        // the state half of the slot never changes: a 32-bit min on the cost half (+4 bytes,
+        // little-endian) is the 64-bit min, and is a native shared atomic
+        const uint32_t old = atom_min_s_u32(ba + 8 * j + 4, hi);
+        logit = hi <= old;
+        strict = hi < old;
         return (int)(b * 4 + j);
       }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if (x[j] == kEmpty) {
-        u64 old = atom_cas_s(ba + 8 * j, kEmpty, key);
+        const u64 old = atom_cas_s(ba + 8 * j, kEmpty, key);
         if (old == kEmpty) {
           claimed = logit = strict = true;
           return (int)(b * 4 + j);
         }
         if ((uint32_t)old == q) {
-          old = atom_min_s(ba + 8 * j, key);
-          logit = key <= old;
-          strict = key < old;
+          const uint32_t o2 = atom_min_s_u32(ba + 8 * j + 4, hi);
+          logit = hi <= o2;
+          strict = hi < o2;
           return (int)(b * 4 + j);
         }
       }
@@ -374,8 +382,8 @@ struct Frame {
   }
 
   // candidate filter + insert for one emitting arc (all lanes call; v = lane has an arc)
-  __device__ __forceinline__ void emit_one(bool v, float c, const int4& arc, int32_t prev, float ref, float inv_w,
-                                           uint32_t best_sa, uint32_t theta_sa) {
+  __device__ __forceinline__ void emit_one(bool v, float c, const int4& arc, uint32_t arc_id, int32_t prev, float ref,
+                                           float inv_w, uint32_t best_sa, uint32_t theta_sa) {
     bool claimed = false, logit = false, strict = false;
     int slot = -1, bin = -1;
     uint32_t o = 0;
@@ -394,7 +402,7 @@ struct Frame {
         if (slot < 0) claimed = logit = false;
       }
     }
-    record(slot, claimed, logit, (uint32_t)arc.w >> 31, o, 0u, prev, bin);
+    record(slot, claimed, logit, (uint32_t)arc.w >> 31, o, arc_id, prev, bin);
   }
 
   // ---- rows a1 + a2: load-balanced emitting expansion ----
@@ -466,7 +474,7 @@ struct Frame {
         for (int u = 0; u < R; u++) {
           const float co = __shfl_sync(0xffffffffu, cost, own[u]);
           float c = __fadd_rn(__fsub_rn(__fadd_rn(co, __int_as_float(arc[u].y)), L[u]), 0.0f);
-          emit_one(v[u], c, arc[u], layer_base + tb + own[u], ref, inv_w, best_sa, theta_sa);
+          emit_one(v[u], c, arc[u], (uint32_t)a[u], layer_base + tb + own[u], ref, inv_w, best_sa, theta_sa);
         }
         if (p.alpha > 0) {
           const int nc = __shfl_sync(0xffffffffu, lds32(nclaim_sa), 0);
@@ -500,7 +508,7 @@ struct Frame {
 #pragma unroll
         for (int u = 0; u < R; u++) {
           float c = __fadd_rn(__fsub_rn(__fadd_rn(cost, __int_as_float(arc[u].y)), L[u]), 0.0f);
-          emit_one(v[u], c, arc[u], layer_base + i, ref, inv_w, best_sa, theta_sa);
+          emit_one(v[u], c, arc[u], (uint32_t)(f.z + j0 + u * BS + tid), layer_base + i, ref, inv_w, best_sa, theta_sa);
         }
         if (p.alpha > 0 && warp == 0) {
           const int nc = __shfl_sync(0xffffffffu, lds32(nclaim_sa), 0);
