@@ -285,12 +285,14 @@ def gpu_arm(args):
         "frames_per_s": round(args.steps * frames_per_step * world / (ms_max / 1e3), 1),
         "e2e": e2e,
         "gpu_launches": 3 * args.steps,
-        "roofline": {"bound": "hbm", "kernel": "frame_kernel<512,2>", "achieved": round(achieved, 1),
+        "roofline": {"bound": "hbm", "kernel": "frame_kernel<512,4>", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": args.traffic, "algorithmic_bytes_per_launch": int(abytes),
                      "kernel_ms": round(kmean, 3), "kernel_share_of_step": round(kmean / (ms_max / args.steps), 3),
                      "peak_source": peak_src},
-        "counters_per_step": {k: v / args.steps for k, v in st.items() if k not in ("device_bytes", "records_used_max")},
+        "counters_per_step": {k: v / args.steps for k, v in st.items()
+                              if k not in ("device_bytes", "records_used_max", "phase_cycles")},
+        "phase_share": {k: round(v / max(1, sum(st["phase_cycles"].values())), 4) for k, v in st["phase_cycles"].items()},
         "memory": {"graph_device_bytes": ginfo.device_bytes, "graph_eq1_bytes": ginfo.eq1_bytes,
                    "decoder_device_bytes": st["device_bytes"],
                    "eq2_bytes_nc=nl=B": W.eq2_bytes(wl["alpha"], B, B)},

@@ -38,6 +38,7 @@ struct LaneState {
   int32_t rec_used;
   float front_best;     // min cost of the current survivors
   u64 emit_arcs, eps_arcs, eps_relax, cand, surv, ovf, alpha_frames, frames_total;
+  u64 phase[6];         // clock64 cycles: expand, select, eps, resolve, contract, rest
 };
 
 struct KParams {
@@ -928,11 +929,22 @@ struct Frame {
     finish_frame(-1, false);
   }
 
+  __device__ __forceinline__ void tick(long long& t0, int ph) {
+    if (threadIdx.x == 0) {
+      const long long t1 = clock64();
+      S.L.phase[ph] += (u64)(t1 - t0);
+      t0 = t1;
+    }
+  }
+
   __device__ void run_frame(int t) {
     const int tid = threadIdx.x;
     const float* row = p.ll + ((size_t)t * p.B + S.b) * (size_t)p.P;
+    long long t0 = clock64();
     begin_frame(INFINITY);
+    tick(t0, 5);
     expand(row);
+    tick(t0, 0);
     if (tid == 0) {
       S.n_claim_emit = S.n_claim;
       if (S.best_ord == 0xFFFFFFFFu) S.status = WFST_ERR_NO_SURVIVOR;
@@ -946,10 +958,15 @@ struct Frame {
       return;
     }
     select_cutoff();
+    tick(t0, 1);
     eps_closure();
+    tick(t0, 2);
     resolve_winners();
+    tick(t0, 3);
     contract();
+    tick(t0, 4);
     finish_frame(t, true);
+    tick(t0, 5);
   }
 };
 
