@@ -164,6 +164,15 @@ def run_gpu_once(cfg="c3", preset="clean", with_paths=True):
     return res, wl
 
 
+def decoder_opts(args) -> dict:
+    o = {}
+    for k in ("threads", "ctas_per_sm", "table_slots", "frames_per_item"):
+        v = getattr(args, k, 0)
+        if v:
+            o[k] = v
+    return o
+
+
 # ------------------------------------------------------------------------- GPU arm
 def gpu_arm(args):
     import torch
@@ -186,7 +195,7 @@ def gpu_arm(args):
     T, B, P = wl["T"], wl["B"], wl["P"]
     G = W.Graph.from_arrays(wl["graph"], device=local)
     ginfo = G.info()
-    D = W.Decoder(G, B, wl["beam"], wl["alpha"])
+    D = W.Decoder(G, B, wl["beam"], wl["alpha"], **decoder_opts(args))
     ll = device_loglikes(W, torch, wl, dev)
     cap = 4 * T + 64
 
@@ -285,7 +294,8 @@ def gpu_arm(args):
         "frames_per_s": round(args.steps * frames_per_step * world / (ms_max / 1e3), 1),
         "e2e": e2e,
         "gpu_launches": 3 * args.steps,
-        "roofline": {"bound": "hbm", "kernel": "frame_kernel<512,4>", "achieved": round(achieved, 1),
+        "decoder_opts": decoder_opts(args),
+        "roofline": {"bound": "hbm", "kernel": "frame_kernel", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": args.traffic, "algorithmic_bytes_per_launch": int(abytes),
                      "kernel_ms": round(kmean, 3), "kernel_share_of_step": round(kmean / (ms_max / args.steps), 3),
@@ -375,6 +385,10 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--chunk", type=int, default=25, help="frames per H2D chunk in the e2e leg")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch (from profiles/)")
+    ap.add_argument("--threads", type=int, default=0, help="frame-kernel CTA size (default by variant)")
+    ap.add_argument("--ctas-per-sm", dest="ctas_per_sm", type=int, default=0)
+    ap.add_argument("--table-slots", dest="table_slots", type=int, default=0)
+    ap.add_argument("--frames-per-item", dest="frames_per_item", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)

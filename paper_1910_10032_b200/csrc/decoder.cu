@@ -132,6 +132,13 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ lanes, i
 }  // namespace
 
 // ---------------- host side ----------------
+// kernel variants: (threads per CTA, arcs in flight per lane, resident CTAs per SM)
+struct WfstVariant {
+  int bs, ctas;
+  void* fn;
+  void (*launch)(int grid, size_t smem, cudaStream_t st, const KParams& kp);
+};
+
 struct wfst_decoder_s {
   wfst_graph_t g = nullptr;
   int device = 0;
@@ -141,7 +148,8 @@ struct wfst_decoder_s {
   wfst_decoder_opts_t o{};
   int32_t C = 0, C_ovf = 0, FCAP = 0, TMAX = 0, LOGCAP = 0;
   int64_t R_cap = 0;
-  int n_sm = 0, threads = 512;
+  int n_sm = 0, threads = 512, ctas_per_sm = 1;
+  const WfstVariant* variant = nullptr;
   size_t smem_bytes = 0;
   KParams kp{};
   // device allocations
@@ -173,23 +181,29 @@ struct DeviceGuard {
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
-template <int BS>
-void* kernel_ptr() {
-  return (void*)frame_kernel<BS, (BS == 1024 ? 2 : 4)>;
+template <int BS, int R, int MINB>
+void launch_v(int grid, size_t smem, cudaStream_t st, const KParams& kp) {
+  frame_kernel<BS, R, MINB><<<grid, BS, smem, st>>>(kp);
+}
+#define WFST_VARIANT(BS, R, MINB) {BS, MINB, (void*)frame_kernel<BS, R, MINB>, launch_v<BS, R, MINB>}
+const WfstVariant kVariants[] = {
+    WFST_VARIANT(512, 4, 1), WFST_VARIANT(256, 4, 1), WFST_VARIANT(1024, 2, 1), WFST_VARIANT(256, 4, 2),
+    WFST_VARIANT(512, 2, 2), WFST_VARIANT(256, 2, 3), WFST_VARIANT(256, 2, 4),
+};
+const WfstVariant* find_variant(int bs, int ctas) {
+  for (const WfstVariant& v : kVariants)
+    if (v.bs == bs && v.ctas == ctas) return &v;
+  return nullptr;
 }
 
 cudaError_t launch_frames(wfst_decoder_t d, KParams kp, cudaStream_t st) {
-  int grid = std::min(kp.n_items, d->o.max_ctas > 0 ? d->o.max_ctas : d->n_sm);
+  int grid = std::min(kp.n_items, d->o.max_ctas > 0 ? d->o.max_ctas : d->n_sm * d->ctas_per_sm);
   if (grid <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(kp.q_head, 0, sizeof(int32_t), st);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(kp.lane_round, 0, sizeof(int32_t) * kp.B, st);
   if (e != cudaSuccess) return e;
-  switch (d->threads) {
-    case 256: frame_kernel<256, 4><<<grid, 256, d->smem_bytes, st>>>(kp); break;
-    case 1024: frame_kernel<1024, 2><<<grid, 1024, d->smem_bytes, st>>>(kp); break;
-    default: frame_kernel<512, 4><<<grid, 512, d->smem_bytes, st>>>(kp); break;
-  }
+  d->variant->launch(grid, d->smem_bytes, st, kp);
   return cudaGetLastError();
 }
 
@@ -228,11 +242,20 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     return cuda_fail(e, "cudaGetDeviceProperties");
   }
   d->n_sm = prop.multiProcessorCount;
-  d->threads = d->o.threads == 256 || d->o.threads == 1024 ? d->o.threads : 512;
-  int C = d->o.table_slots > 0 ? d->o.table_slots : 24576;
-  C = std::max(64, (C + 3) / 4 * 4);
-  size_t max_smem = prop.sharedMemPerBlockOptin;
-  while (C > 64 && smem_for(C, d->threads) + sizeof(SmemCtl) + 4 * d->threads + 1024 > max_smem) C -= 1024;
+  d->ctas_per_sm = d->o.ctas_per_sm > 0 ? d->o.ctas_per_sm : 1;
+  d->threads = d->o.threads > 0 ? d->o.threads : (d->ctas_per_sm == 1 ? 512 : 256);
+  d->variant = find_variant(d->threads, d->ctas_per_sm);
+  if (!d->variant) {
+    delete d;
+    return fail(WFST_ERR_INVALID_ARG, "unsupported (threads, ctas_per_sm) combination");
+  }
+  // on-chip table: what is left of the SM's shared memory per resident CTA
+  const size_t static_smem = sizeof(SmemCtl) + 4 * (size_t)d->threads + 1024;
+  const size_t per_cta = std::min((size_t)prop.sharedMemPerBlockOptin,
+                                  (size_t)prop.sharedMemPerMultiprocessor / d->ctas_per_sm);
+  int C = d->o.table_slots > 0 ? d->o.table_slots : (int)((per_cta - static_smem - (size_t)kNB * 4) / 8);
+  C = std::max(64, C / 256 * 256);
+  while (C > 256 && smem_for(C, d->threads) + static_smem > per_cta) C -= 256;
   d->C = C;
   int Co = d->o.overflow_slots > 0 ? d->o.overflow_slots : C;
   d->C_ovf = std::max(64, (Co + 3) / 4 * 4);
@@ -257,8 +280,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   if (d->R_cap > INT32_MAX - 1) d->R_cap = INT32_MAX - 1;
   if (d->o.frames_per_item <= 0) d->o.frames_per_item = 16;
   d->smem_bytes = smem_for(d->C, d->threads);
-  void* kfn = d->threads == 256 ? kernel_ptr<256>() : d->threads == 1024 ? kernel_ptr<1024>() : kernel_ptr<512>();
-  e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d->smem_bytes);
+  e = cudaFuncSetAttribute(d->variant->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d->smem_bytes);
   if (e != cudaSuccess) {
     delete d;
     return cuda_fail(e, "cudaFuncSetAttribute");

@@ -970,8 +970,8 @@ struct Frame {
   }
 };
 
-template <int BS, int R>
-__global__ void __launch_bounds__(BS, 1) frame_kernel(KParams p) {
+template <int BS, int R, int MINB>
+__global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SmemCtl S;
   __shared__ int s_wbuf[BS];

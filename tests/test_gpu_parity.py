@@ -256,3 +256,15 @@ def test_c3_full_size_sampled(W, torch, oracle_mod):
         assert res["reached_final"][b] == r.reached_final
         assert list(res["arcs"][b, :n]) == list(r.arcs)
         assert res["cost"][b] == r.cost32
+
+
+@pytest.mark.parametrize("threads,ctas", [(256, 1), (256, 2), (512, 2), (256, 3), (256, 4), (1024, 1)])
+def test_kernel_variants_parity(W, torch, oracle_mod, threads, ctas):
+    """Every (CTA size, CTAs per SM) variant of the frame kernel gives the oracle's answer,
+    including when its smaller on-chip table spills to the overflow table."""
+    g, ll = _hclg_case(20_000, 3.0, 500, 12, 60, seed=16, preset="other")
+    og = oracle_mod.OracleGraph(g)
+    D, res = _gpu_run(W, torch, g, ll, 15.0, 3000, threads=threads, ctas_per_sm=ctas)
+    assert res["rc"] == 0
+    for b in range(12):
+        _compare(og, ll, 15.0, 3000, res, b)
