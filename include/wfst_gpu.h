@@ -77,7 +77,7 @@ typedef struct {
 /* Decoder tuning; zero fields mean "default".  See DESIGN.md §5. */
 typedef struct {
   int32_t table_slots;       /* per-stream on-chip token table slots (default: all free smem)     */
-  int32_t overflow_slots;    /* per-stream global overflow table slots (default 2*table_slots)     */
+  int32_t overflow_slots;    /* per-stream global overflow table slots (default max(32768, 4*alpha)) */
   int64_t records_per_stream;/* traceback records per stream (default sized from max_frames)      */
   int32_t max_frames;        /* frames per utterance kept in per-frame stats (default 2048)       */
   int32_t threads;           /* CTA size of the frame kernel (256/512/1024; default 512 or 256)   */

@@ -257,7 +257,8 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   C = std::max(64, C / 256 * 256);
   while (C > 256 && smem_for(C, d->threads) + static_smem > per_cta) C -= 256;
   d->C = C;
-  int Co = d->o.overflow_slots > 0 ? d->o.overflow_slots : C;
+  // overflow table: room for every distinct candidate a frame can hold beyond the on-chip table
+  int Co = d->o.overflow_slots > 0 ? d->o.overflow_slots : std::max(std::max(C, 32768), 4 * d->alpha);
   d->C_ovf = std::max(64, (Co + 3) / 4 * 4);
   d->FCAP = d->C + d->C_ovf;
   d->LOGCAP = 4 * d->FCAP;

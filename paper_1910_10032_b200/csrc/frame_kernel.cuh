@@ -537,47 +537,66 @@ struct Frame {
       __syncthreads();
       return;
     }
-    long long cnt = 0;
-    for (int i = tid; i < n_claim; i += BS) {
-      const int slot = (int)(claim[i] & 0x7FFFFFFFu);
-      if (key_cost(read_slot(slot)) < beam_cut) cnt++;
-    }
-    const long long n_in = block_sum64<BS>(cnt, S.warp_tmp64);
+    // exact alpha-th smallest in-beam cost by radix select on rk = ord(c) - ord(best) (every
+    // entry is >= best), 10-bit digits from the top set bit of ord(beam_cut) - ord(best); the
+    // first pass also counts the in-beam entries.
+    const uint32_t ob = S.best_ord;
+    const uint32_t span = ord_of(beam_cut) - ob;   // beam_cut = +inf gives a large span: fine
+    const int nbits = span ? 32 - __clz(span) : 1;
+    int shift = ((nbits + 9) / 10) * 10 - 10;
     if (tid == 0) {
-      S.n_in = (int)n_in;
-      S.use_alpha = 0;
-      S.kalpha = INFINITY;
       S.radix_prefix = 0;
       S.radix_k = p.alpha;
     }
-    __syncthreads();
-    if (n_in <= p.alpha) return;
-    // exact alpha-th smallest in-beam cost: 4 radix passes of 8 bits on ord(cost)
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = tid; i < 256; i += BS) hist[i] = 0;
+    long long cnt = 0;
+    bool first = true;
+    while (true) {
+      for (int i = tid; i < kNB; i += BS) hist[i] = 0;
       __syncthreads();
       const uint32_t prefix = (uint32_t)S.radix_prefix;
-      const uint32_t hmask = (shift == 24) ? 0u : (0xFFFFFFFFu << (shift + 8));
-      for (int i = tid; i < n_claim; i += BS) {
-        const int slot = (int)(claim[i] & 0x7FFFFFFFu);
-        const u64 v = read_slot(slot);
-        if (!(key_cost(v) < beam_cut)) continue;
-        const uint32_t o = (uint32_t)(v >> 32);
-        if ((o & hmask) == (prefix & hmask)) red_add_s(hist_sa + 4u * ((o >> shift) & 255u), 1);
+      const uint32_t hmask = (shift + 10 >= 32) ? 0u : (0xFFFFFFFFu << (shift + 10));
+      constexpr int U = 4;
+      for (int i0 = 0; i0 < n_claim; i0 += BS * U) {
+        u64 v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int i = i0 + u * BS + tid;
+          v[u] = i < n_claim ? read_slot((int)(__ldcg(claim + i) & 0x7FFFFFFFu)) : kEmpty;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          if (v[u] == kEmpty || !(key_cost(v[u]) < beam_cut)) continue;
+          if (first) cnt++;
+          const uint32_t rk = (uint32_t)(v[u] >> 32) - ob;
+          if ((rk & hmask) == (prefix & hmask)) red_add_s(hist_sa + 4u * ((rk >> shift) & 1023u), 1);
+        }
       }
-      __syncthreads();
+      if (first) {
+        const long long n_in = block_sum64<BS>(cnt, S.warp_tmp64);   // includes a barrier
+        if (tid == 0) S.n_in = (int)n_in;
+        first = false;
+        if (n_in <= p.alpha) {
+          if (tid == 0) {
+            S.use_alpha = 0;
+            S.kalpha = INFINITY;
+          }
+          break;
+        }
+      } else {
+        __syncthreads();
+      }
       if (tid < 32) {   // warp 0: locate the digit holding rank k
         const int lane = tid;
-        int k = S.radix_k;
-        int s = 0;
-        for (int i = 0; i < 8; i++) s += hist[lane * 8 + i];
-        const int incl = warp_incl_scan(s);
+        const int k = S.radix_k;
+        int sum = 0;
+        for (int i = 0; i < 32; i++) sum += hist[lane * 32 + i];
+        const int incl = warp_incl_scan(sum);
         const unsigned m = __ballot_sync(0xffffffffu, incl >= k);
         const int L = __ffs(m) - 1;
         if (lane == L) {
-          int c = incl - s;
-          int d = lane * 8;
-          for (; d < lane * 8 + 8; d++) {
+          int c = incl - sum;
+          int d = lane * 32;
+          for (; d < lane * 32 + 31; d++) {
             if (c + hist[d] >= k) break;
             c += hist[d];
           }
@@ -586,10 +605,14 @@ struct Frame {
         }
       }
       __syncthreads();
-    }
-    if (tid == 0) {
-      S.kalpha = float_of_ord((uint32_t)S.radix_prefix);
-      S.use_alpha = 1;
+      if (shift == 0) {
+        if (tid == 0) {
+          S.kalpha = float_of_ord(ob + (uint32_t)S.radix_prefix);
+          S.use_alpha = 1;
+        }
+        break;
+      }
+      shift = max(shift - 10, 0);
     }
     for (int i = tid; i < kNB; i += BS) hist[i] = 0;
     __syncthreads();
