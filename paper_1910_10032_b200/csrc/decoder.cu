@@ -243,7 +243,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   }
   d->n_sm = prop.multiProcessorCount;
   d->ctas_per_sm = d->o.ctas_per_sm > 0 ? d->o.ctas_per_sm : 1;
-  d->threads = d->o.threads > 0 ? d->o.threads : (d->ctas_per_sm == 1 ? 512 : 256);
+  d->threads = d->o.threads > 0 ? d->o.threads : (d->ctas_per_sm == 1 ? 1024 : 256);
   d->variant = find_variant(d->threads, d->ctas_per_sm);
   if (!d->variant) {
     delete d;
