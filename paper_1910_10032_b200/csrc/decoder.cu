@@ -26,7 +26,8 @@ namespace {
 // ---------------- best path (row a7; readings R10, R11) ----------------
 // One CTA per lane: argmin over the last layer's survivors of (c + F, arc) among final states,
 // else of (c, arc); then the traceback walk over {arc, prev} records.
-__global__ void best_path_kernel(KParams p, const int32_t* __restrict__ lanes, int32_t n, int32_t cap,
+__global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, const int32_t* __restrict__ lanes,
+                                 int32_t n, int32_t cap,
                                  float* cost_out, int32_t* reached_out, int32_t* n_arcs_out, int32_t* arcs_out,
                                  int32_t* olab_out, int32_t* n_olab_out, int32_t* status_out) {
   __shared__ u64 s_fin[32], s_any[32];
@@ -119,7 +120,7 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ lanes, i
   }
   int nol = 0;
   for (int k = 0; k < len && k < cap; k++) {
-    int32_t ol = __ldg(&p.arcs[arcs_out[(size_t)li * cap + k]].w) & 0x7FFFFFFF;
+    int32_t ol = __ldg(olabel + arcs_out[(size_t)li * cap + k]);
     if (ol != 0) {
       if (nol < cap) olab_out[(size_t)li * cap + nol] = ol;
       nol++;
@@ -146,7 +147,7 @@ struct wfst_decoder_s {
   float beam = 15.f;
   int32_t alpha = 0;
   wfst_decoder_opts_t o{};
-  int32_t C = 0, C_ovf = 0, FCAP = 0, TMAX = 0, LOGCAP = 0;
+  int32_t C = 0, C_ovf = 0, FCAP = 0, TMAX = 0;
   int64_t R_cap = 0;
   int n_sm = 0, threads = 512, ctas_per_sm = 1;
   const WfstVariant* variant = nullptr;
@@ -250,7 +251,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     return fail(WFST_ERR_INVALID_ARG, "unsupported (threads, ctas_per_sm) combination");
   }
   // on-chip table: what is left of the SM's shared memory per resident CTA
-  const size_t static_smem = sizeof(SmemCtl) + 4 * (size_t)d->threads + 1024;
+  const size_t static_smem = sizeof(SmemCtl) + 4 * (size_t)d->threads + (size_t)(d->threads / 32) * kStage * 16 + 1024;
   const size_t per_cta = std::min((size_t)prop.sharedMemPerBlockOptin,
                                   (size_t)prop.sharedMemPerMultiprocessor / d->ctas_per_sm);
   int C = d->o.table_slots > 0 ? d->o.table_slots : (int)((per_cta - static_smem - (size_t)kNB * 4) / 8);
@@ -261,7 +262,6 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   int Co = d->o.overflow_slots > 0 ? d->o.overflow_slots : std::max(std::max(C, 32768), 4 * d->alpha);
   d->C_ovf = std::max(64, (Co + 3) / 4 * 4);
   d->FCAP = d->C + d->C_ovf;
-  d->LOGCAP = 4 * d->FCAP;
   d->TMAX = d->o.max_frames > 0 ? d->o.max_frames : 2048;
   int64_t per_frame = d->alpha > 0 ? std::min<int64_t>((int64_t)d->alpha * 5 / 4 + 1024, d->FCAP) : d->FCAP;
   if (d->o.records_per_stream > 0) {
@@ -271,8 +271,8 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     d->R_cap = (int64_t)(d->TMAX / 4 + 1) * per_frame;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-      int64_t per_lane_other = (int64_t)d->FCAP * (32 + 4 + 8 + 4 + 32 + 8 + 4) + (int64_t)d->LOGCAP * 16 +
-                               (int64_t)d->C_ovf * 8 + (int64_t)d->TMAX * 60;
+      int64_t per_lane_other = (int64_t)d->FCAP * (32 + 4 + 8 + 8 + 16 + 8 + 8) + (int64_t)d->C_ovf * 8 +
+                               (int64_t)d->TMAX * 60;
       int64_t budget = (int64_t)(free_b / 2) / n_streams - per_lane_other;
       int64_t cap = budget / (int64_t)(sizeof(int2) + (d->o.debug_costs ? 4 : 0));
       if (cap < d->R_cap) d->R_cap = std::max<int64_t>(cap, per_frame);
@@ -297,17 +297,14 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     total += bytes;
     return parts.size() - 1;
   };
-  const size_t LG = (size_t)d->LOGCAP;
   size_t i_front = add(L * 2 * FC * sizeof(int4));
   size_t i_claim = add(L * FC * 4);
-  size_t i_win = add(L * FC * 8);
-  size_t i_log = add(L * LG * sizeof(int4));
-  size_t i_slotrec = add(L * FC * 4);
-  size_t i_tmpA = add(L * FC * sizeof(int4));
-  size_t i_tmpB = add(L * FC * sizeof(int4));
+  size_t i_win_e = add(L * FC * 8);
+  size_t i_win_eps = add(L * FC * 8);
+  size_t i_tmp = add(L * FC * sizeof(int4));
+  size_t i_sort2 = add(L * FC * sizeof(int2));
   size_t i_ovf = add(L * (size_t)d->C_ovf * 8);
   size_t i_wl = add(L * 2 * FC * 4);
-  size_t i_fix = add(L * FC * 4);
   size_t i_rec = add(L * (size_t)d->R_cap * sizeof(int2));
   size_t i_rcost = d->o.debug_costs ? add(L * (size_t)d->R_cap * 4) : (size_t)-1;
   size_t i_fst = add(L * (size_t)d->TMAX * 3 * 4);
@@ -333,6 +330,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.state_info = g->d_state;
   kp.arcs = g->d_arcs;
   kp.start = g->start;
+  kp.n_states = g->Q;
   kp.beam = beam;
   kp.alpha = d->alpha;
   kp.C = d->C;
@@ -344,15 +342,12 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.lanes_st = d->d_lanes;
   kp.front = (int4*)(base + parts[i_front].off);
   kp.claim = (uint32_t*)(base + parts[i_claim].off);
-  kp.win = (u64*)(base + parts[i_win].off);
-  kp.log = (int4*)(base + parts[i_log].off);
-  kp.LOGCAP = d->LOGCAP;
-  kp.slotrec = (int32_t*)(base + parts[i_slotrec].off);
-  kp.tmpA = (int4*)(base + parts[i_tmpA].off);
-  kp.tmpB = (int4*)(base + parts[i_tmpB].off);
+  kp.win_e = (u64*)(base + parts[i_win_e].off);
+  kp.win_eps = (u64*)(base + parts[i_win_eps].off);
+  kp.tmp = (int4*)(base + parts[i_tmp].off);
+  kp.sort2 = (int2*)(base + parts[i_sort2].off);
   kp.ovf = (u64*)(base + parts[i_ovf].off);
   kp.wl = (uint32_t*)(base + parts[i_wl].off);
-  kp.epsfix = (int32_t*)(base + parts[i_fix].off);
   kp.rec = (int2*)(base + parts[i_rec].off);
   kp.rec_cost = i_rcost != (size_t)-1 ? (float*)(base + parts[i_rcost].off) : nullptr;
   kp.fstats = (float*)(base + parts[i_fst].off);
@@ -361,6 +356,8 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.q_head = d->d_qhead;
   kp.lane_round = d->d_round;
   e = cudaMemset(base + parts[i_ovf].off, 0xFF, parts[i_ovf].bytes);
+  if (e == cudaSuccess) e = cudaMemset(base + parts[i_win_e].off, 0xFF, parts[i_win_e].bytes);
+  if (e == cudaSuccess) e = cudaMemset(base + parts[i_win_eps].off, 0xFF, parts[i_win_eps].bytes);
   if (e == cudaSuccess) e = cudaMemset(d->d_lanes, 0, sizeof(LaneState) * L);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -588,7 +585,8 @@ wfst_status wfst_get_best_paths(wfst_decoder_t d, const int32_t* streams, int32_
   for (int i = 0; i < n; i++) ids[i] = streams ? streams[i] : i;
   e = cudaMemcpy(d_ids, ids.data(), 4 * (size_t)n, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "ids");
-  best_path_kernel<<<n, 256>>>(d->kp, d_ids, n, cap, d_cost, d_reached, d_nar, d_arcs, d_ol, d_nol, d_st);
+  best_path_kernel<<<n, 256>>>(d->kp, d->g->d_olabel, d_ids, n, cap, d_cost, d_reached, d_nar, d_arcs, d_ol, d_nol,
+                               d_st);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cuda_fail(e, "best path kernel");

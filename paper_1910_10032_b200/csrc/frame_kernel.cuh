@@ -3,9 +3,8 @@
 // One persistent CTA per SM owns one lane (stream) at a time and runs whole frames with CTA
 // barriers only between phases: warp-centric load-balanced emitting expansion, running
 // best + beam and exact max-active, epsilon closure to a fixed point under the
-// fixed cutoff, contraction into a cost-ordered frontier of one representative per
-// state with traceback records.  Lanes are re-queued every K frames.
-// DESIGN.md §5 explains the layout.
+// fixed cutoff, contraction into a frontier of one representative per state,
+// sorted by state id, with traceback records.  DESIGN.md §5 explains the layout.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -19,32 +18,32 @@ using wfst::kArcMask;
 using wfst::kArcNone;
 
 constexpr u64 kEmpty = 0xFFFFFFFFFFFFFFFFull;
-constexpr int kNB = 1024;          // cost bins of the max-active bound (DESIGN.md §5.2)
+constexpr int kNB = 1024;          // cost bins of the max-active bound (DESIGN.md §5.4)
 constexpr int kMaxProbeS = 32;     // buckets probed in the on-chip table before overflowing
 constexpr int kMaxProbeG = 512;    // buckets probed in the global overflow table
-constexpr int32_t kEpsFlag = (int32_t)0x80000000;
 constexpr int kModeFrames = 0, kModeInit = 1;
 constexpr int kBig = 64;           // tokens with more emitting arcs are expanded CTA-wide
 constexpr int kBigCap = 256;
-constexpr int kNBuck = 16;         // cost buckets ordering the next frontier
+constexpr int kStage = 32;         // per-warp staging buffer (candidates awaiting insertion)
+constexpr int kSortBuckets = 4096; // contraction: bucket sort of survivors by state id
 
 struct LaneState {
   int32_t status;       // wfst_status, sticky
   int32_t initialized;
-  int32_t n_front;      // survivors in the current frontier
+  int32_t n_front;      // survivors in the current frontier (sorted by state id)
   int32_t cur;          // frontier buffer holding them
   int32_t frames;       // frames decoded in this utterance
   int32_t layer_base;   // record index of the current layer's first survivor
   int32_t rec_used;
   float front_best;     // min cost of the current survivors
   u64 emit_arcs, eps_arcs, eps_relax, cand, surv, ovf, alpha_frames, frames_total;
-  u64 phase[6];         // clock64 cycles: expand, select, eps, resolve, contract, rest
+  u64 phase[6];         // clock64 cycles: expand, cutoff, epsilon, (unused), contract, rest
 };
 
 struct KParams {
   const int4* __restrict__ state_info;   // {e_begin, e_end, eps_end, final bits}
-  const int4* __restrict__ arcs;         // {dst, weight bits, pdf, olabel | dst_has_eps << 31}
-  int32_t start;
+  const int4* __restrict__ arcs;         // {dst, weight bits, pdf, src | dst_has_eps << 31}
+  int32_t start, n_states;
   const float* ll;
   int32_t T, B, P;
   const int32_t* lanes;   // batch index -> lane id
@@ -53,20 +52,18 @@ struct KParams {
   int32_t* lane_round;
   float beam;
   int32_t alpha;
-  int32_t C, NBK, C_ovf, FCAP, LOGCAP;
+  int32_t C, NBK, C_ovf, FCAP;
   int64_t R_cap;
   int32_t TMAX;
   LaneState* lanes_st;
-  int4* front;        // [lane][2][FCAP]  {state, cost bits, e_begin, n_emit}, cost-ordered
+  int4* front;        // [lane][2][FCAP]  {state, cost bits, e_begin, n_emit}, sorted by state
   uint32_t* claim;    // [lane][FCAP]     slot | has_eps << 31, one per distinct state
-  u64* win;           // [lane][FCAP]     per slot: (arc << 32) | back-pointer of the winner
-  int4* log;          // [lane][LOGCAP]   improvements {slot, ord(cost), arc, back-pointer}
-  int32_t* slotrec;   // [lane][FCAP]     slot -> survivor index
-  int4* tmpA;         // [lane][FCAP]     contraction scratch {state, cost, e_begin, n_emit}
-  int4* tmpB;         // [lane][FCAP]     contraction scratch {slot, arc, prev, bucket}
+  u64* win_e;         // [lane][FCAP]     per slot: min (ord(cost) << 32 | token << k | offset)
+  u64* win_eps;       // [lane][FCAP]     per slot: min (ord(cost) << 32 | epsilon arc id)
+  int4* tmp;          // [lane][FCAP]     contraction scratch {state, cost, arc | eps flag, prev/src}
+  int2* sort2;        // [lane][FCAP]     contraction sort scratch when it does not fit on chip
   u64* ovf;           // [lane][C_ovf]    global overflow token table
   uint32_t* wl;       // [lane][2][FCAP]  epsilon worklists (slots)
-  int32_t* epsfix;    // [lane][FCAP]     survivor positions whose back-pointer is an eps slot
   int2* rec;          // [lane][R_cap]    traceback records {arc, prev}
   float* rec_cost;    // [lane][R_cap]    (debug) survivor cost
   float* fstats;      // [lane][TMAX][3]
@@ -78,12 +75,12 @@ struct SmemCtl {
   int32_t item, lane, b, status;
   uint32_t best_ord;
   int32_t theta;
-  int32_t n_claim, n_claim_emit, n_ovf, n_surv, n_in, n_wl, n_wl_next, n_log, n_big, n_fix;
-  float beam_cut, kalpha, ref, inv_w, min_surv, bk_ref, bk_inv;
+  int32_t n_claim, n_claim_emit, n_ovf, n_surv, n_in, n_wl, n_wl_next, n_big;
+  int32_t off_bits;   // split of the emitting winner key: token << off_bits | offset
+  float beam_cut, kalpha, ref, inv_w, min_surv;
   int32_t use_alpha;
   int32_t radix_prefix, radix_k;
   long long emit_arcs, eps_deg, eps_relax;
-  int32_t bucket_base[kNBuck];
   int32_t warp_tmp[32];
   long long warp_tmp64[32];
   int32_t big[kBigCap];
@@ -114,14 +111,21 @@ __device__ __forceinline__ void lds64x2(uint32_t a, u64& x, u64& y) {
 __device__ __forceinline__ void sts64(uint32_t a, u64 v) {
   asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
+__device__ __forceinline__ int4 lds128(uint32_t a) {
+  int4 v;
+  asm volatile("ld.volatile.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, int4 v) {
+  asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ u64 atom_cas_s(uint32_t a, u64 cmp, u64 v) {
   u64 old;
   asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "r"(a), "l"(cmp), "l"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ u64 atom_min_s(uint32_t a, u64 v) {
-  u64 old;
-  asm volatile("atom.shared.min.u64 %0, [%1], %2;" : "=l"(old) : "r"(a), "l"(v) : "memory");
   return old;
 }
 __device__ __forceinline__ uint32_t atom_min_s_u32(uint32_t a, uint32_t v) {
@@ -134,7 +138,7 @@ __device__ __forceinline__ int atom_add_s(uint32_t a, int v) {
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
   return old;
 }
-__device__ __forceinline__ void atom_min_s32(uint32_t a, uint32_t v) {
+__device__ __forceinline__ void red_min_s32(uint32_t a, uint32_t v) {
   asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ void red_add_s(uint32_t a, int v) {
@@ -145,9 +149,15 @@ __device__ __forceinline__ int lds32(uint32_t a) {
   asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
   return v;
 }
+__device__ __forceinline__ void sts32(uint32_t a, int v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ u64 ldg_volatile64(const u64* p) { return *(const volatile u64*)p; }
+__device__ __forceinline__ void red_min_g64(u64* p, u64 v) {
+  asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
-// monotone cost -> bin map, used both to count and to reject (DESIGN.md §5.2)
+// monotone cost -> bin map, used both to count and to reject (DESIGN.md §5.4)
 __device__ __forceinline__ int bin_of(float c, float ref, float inv_w) {
   float x = __fmul_rn(__fsub_rn(c, ref), inv_w);
   x = fminf(fmaxf(x, 0.0f), (float)(kNB - 1));
@@ -155,9 +165,8 @@ __device__ __forceinline__ int bin_of(float c, float ref, float inv_w) {
 }
 
 // Insert (state q, key = ord(cost) << 32 | q) into a table of nb buckets of 4 slots.
-// Returns the slot, or -1 when the probe limit is reached.  claimed: the slot was empty.
-// logit: the key is <= the slot value it met (an improvement or a tie -- both are logged so
-// the winner's (arc, back-pointer) can be chosen after the frame, R9).  strict: key < old.
+// Returns the slot, or -1 when the probe limit is reached.  claimed: the slot was empty;
+// logit: the cost is <= the slot's (an improvement or a tie); strict: <.
 __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q, u64 key, bool& claimed,
                                         bool& logit, bool& strict) {
   uint32_t b = bucket_of(q, nb);
@@ -172,8 +181,8 @@ __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if ((uint32_t)x[j] == q && x[j] != kEmpty) {
-        // the state half of the slot never changes: a 32-bit min on the cost half (+4 bytes,
-        // little-endian) is the 64-bit min, and is a native shared atomic
+        // the state half of a slot never changes: a 32-bit min on the cost half (+4 bytes,
+        // little-endian) is the 64-bit min and a native shared atomic
         const uint32_t old = atom_min_s_u32(ba + 8 * j + 4, hi);
         logit = hi <= old;
         strict = hi < old;
@@ -250,9 +259,10 @@ __device__ __forceinline__ int warp_incl_scan(int x) {
 // warp-aggregated append to a shared counter: returns this lane's index (or -1 if !need)
 __device__ __forceinline__ int warp_append(bool need, uint32_t counter_sa) {
   const int lane = threadIdx.x & 31;
-  unsigned m = __ballot_sync(0xffffffffu, need);
+  const unsigned m = __ballot_sync(0xffffffffu, need);
   if (m == 0) return -1;
-  int leader = __ffs(m) - 1, base = 0;
+  const int leader = __ffs(m) - 1;
+  int base = 0;
   if (lane == leader) base = atom_add_s(counter_sa, __popc(m));
   base = __shfl_sync(0xffffffffu, base, leader);
   return need ? base + __popc(m & ((1u << lane) - 1u)) : -1;
@@ -278,39 +288,36 @@ struct Frame {
   static constexpr int NW = BS / 32;
   const KParams& p;
   SmemCtl& S;
-  uint32_t tab_sa;   // shared address of the token table
-  uint32_t hist_sa;  // shared address of the cost histogram (kNB ints)
-  int* hist;         // same, generic (reads)
-  int* wbuf;         // this warp's owner buffer (32 ints, -1 when idle)
+  uint32_t tab_sa;    // shared address of the token table (C slots of 8 B)
+  uint32_t hist_sa;   // shared address of the cost histogram (kNB ints)
+  uint32_t stage_sa;  // shared address of this warp's staging buffer (kStage x 16 B)
+  int* hist;
+  int* wbuf;          // this warp's owner buffer (32 ints, -1 when idle)
   // lane buffers
-  int4* F0;   // frontier buffer 0; buffer 1 follows at +FCAP
+  int4* F0;           // frontier buffer 0; buffer 1 follows at +FCAP
   uint32_t* claim;
-  u64* win;
-  int4* lg;
-  int32_t* slotrec;
-  int4* tmpA;
-  int4* tmpB;
+  u64* win_e;
+  u64* win_eps;
+  int4* tmp;
+  int2* sort2;
   u64* ovf;
-  uint32_t* wl0;  // epsilon worklist 0; worklist 1 follows at +FCAP
-  int32_t* epsfix;
+  uint32_t* wl0;      // epsilon worklist 0; worklist 1 follows at +FCAP
   int2* rec;
   float* rec_cost;
 
-  __device__ Frame(const KParams& p_, SmemCtl& S_, uint32_t tab_sa_, int* hist_, int* wbuf_)
-      : p(p_), S(S_), tab_sa(tab_sa_), hist_sa(saddr(hist_)), hist(hist_), wbuf(wbuf_) {}
+  __device__ Frame(const KParams& p_, SmemCtl& S_, uint32_t tab_sa_, int* hist_, int* wbuf_, uint32_t stage_sa_)
+      : p(p_), S(S_), tab_sa(tab_sa_), hist_sa(saddr(hist_)), stage_sa(stage_sa_), hist(hist_), wbuf(wbuf_) {}
 
   __device__ void bind(int lane) {
-    size_t L = (size_t)lane, FC = (size_t)p.FCAP;
+    const size_t L = (size_t)lane, FC = (size_t)p.FCAP;
     F0 = p.front + L * 2 * FC;
     claim = p.claim + L * FC;
-    win = p.win + L * FC;
-    lg = p.log + L * (size_t)p.LOGCAP;
-    slotrec = p.slotrec + L * FC;
-    tmpA = p.tmpA + L * FC;
-    tmpB = p.tmpB + L * FC;
+    win_e = p.win_e + L * FC;
+    win_eps = p.win_eps + L * FC;
+    tmp = p.tmp + L * FC;
+    sort2 = p.sort2 + L * FC;
     ovf = p.ovf + L * (size_t)p.C_ovf;
     wl0 = p.wl + L * 2 * FC;
-    epsfix = p.epsfix + L * FC;
     rec = p.rec + L * (size_t)p.R_cap;
     rec_cost = p.rec_cost ? p.rec_cost + L * (size_t)p.R_cap : nullptr;
   }
@@ -321,9 +328,6 @@ struct Frame {
   __device__ __forceinline__ void clear_slot(int slot) const {
     if (slot < p.C) sts64(tab_sa + 8u * (uint32_t)slot, kEmpty);
     else ovf[slot - p.C] = kEmpty;
-  }
-  __device__ __forceinline__ bool keep(float c) const {
-    return c < S.beam_cut && (!S.use_alpha || c <= S.kalpha);
   }
 
   __device__ __forceinline__ int insert(uint32_t q, u64 key, bool& claimed, bool& logit, bool& strict) {
@@ -338,23 +342,13 @@ struct Frame {
     return s + p.C;
   }
 
-  // Record a claim and/or an improvement (warp-collective: every lane of the warp calls it).
-  __device__ __forceinline__ void record(int slot, bool claimed, bool logit, uint32_t eps_flag, uint32_t ord,
-                                         uint32_t arc, int32_t prev, int bin) {
-    int ci = warp_append(claimed, saddr(&S.n_claim));
+  // claim bookkeeping (warp-collective: every lane of the warp calls it)
+  __device__ __forceinline__ void add_claim(int slot, bool claimed, uint32_t eps_flag, int bin) {
+    const int ci = warp_append(claimed, saddr(&S.n_claim));
     if (claimed) {
-      if (ci < p.FCAP) {
-        claim[ci] = (uint32_t)slot | (eps_flag << 31);
-        win[slot] = kEmpty;
-      } else {
-        S.status = WFST_ERR_CAPACITY;
-      }
-      if (bin >= 0) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
-    }
-    int li = warp_append(logit, saddr(&S.n_log));
-    if (logit) {
-      if (li < p.LOGCAP) lg[li] = make_int4(slot, (int)ord, (int)arc, prev);
+      if (ci < p.FCAP) claim[ci] = (uint32_t)slot | (eps_flag << 31);
       else S.status = WFST_ERR_CAPACITY;
+      if (bin >= 0) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
     }
   }
 
@@ -365,72 +359,100 @@ struct Frame {
     int s = 0;
 #pragma unroll 8
     for (int i = 0; i < kNB / 32; i++) s += lds32(hist_sa + 4u * (base + i));
-    int incl = warp_incl_scan(s);
-    unsigned m = __ballot_sync(0xffffffffu, incl >= p.alpha);
-    if (m == 0) return;
-    const int L = __ffs(m) - 1;
-    if (lane == L) {
-      int c = incl - s;
-      for (int i = 0; i < kNB / 32; i++) {
-        c += lds32(hist_sa + 4u * (base + i));
-        if (c >= p.alpha) {
-          atomicMin(&S.theta, base + i + 1);
-          break;
+    const int incl = warp_incl_scan(s);
+    const unsigned m = __ballot_sync(0xffffffffu, incl >= p.alpha);
+    if (m != 0) {
+      const int L = __ffs(m) - 1;
+      if (lane == L) {
+        int c = incl - s;
+        for (int i = 0; i < kNB / 32; i++) {
+          c += lds32(hist_sa + 4u * (base + i));
+          if (c >= p.alpha) {
+            atomicMin(&S.theta, base + i + 1);
+            break;
+          }
         }
       }
     }
     __syncwarp();
   }
 
-  // candidate filter + insert for one emitting arc (all lanes call; v = lane has an arc)
-  __device__ __forceinline__ void emit_one(bool v, float c, const int4& arc, uint32_t arc_id, int32_t prev, float ref,
-                                           float inv_w, uint32_t best_sa, uint32_t theta_sa) {
+  // insert the first n staged candidates of this warp (warp-collective)
+  __device__ __forceinline__ void flush(int n, float beam, uint32_t best_sa, uint32_t theta_sa) {
+    const int lane = threadIdx.x & 31;
     bool claimed = false, logit = false, strict = false;
     int slot = -1, bin = -1;
-    uint32_t o = 0;
-    if (v) {
+    uint32_t flag = 0;
+    if (lane < n) {
+      const int4 e = lds128(stage_sa + 16u * lane);   // {q, ord, low key, bin | eps flag << 31}
+      const uint32_t o = (uint32_t)e.y;
+      bin = e.w & 0x7FFFFFFF;
+      flag = (uint32_t)e.w >> 31;
+      // re-check against the bounds as they are now (both only tighten)
       const uint32_t bo = (uint32_t)lds32(best_sa);
-      bool ok = !(bo != 0xFFFFFFFFu && !(c < __fadd_rn(float_of_ord(bo), p.beam)));
+      const bool ok = (bo == 0xFFFFFFFFu || float_of_ord(o) < __fadd_rn(float_of_ord(bo), beam)) &&
+                      bin < lds32(theta_sa);
       if (ok) {
-        bin = bin_of(c, ref, inv_w);
-        ok = bin < lds32(theta_sa);
-      }
-      if (ok) {
-        o = ord_of(c);
-        if (o < bo) atom_min_s32(best_sa, o);
-        const uint32_t q = (uint32_t)arc.x;
-        slot = insert(q, ((u64)o << 32) | q, claimed, logit, strict);
-        if (slot < 0) claimed = logit = false;
+        if (o < bo) red_min_s32(best_sa, o);
+        slot = insert((uint32_t)e.x, ((u64)o << 32) | (uint32_t)e.x, claimed, logit, strict);
+        if (slot >= 0 && logit) red_min_g64(win_e + slot, ((u64)o << 32) | (uint32_t)e.z);
+        if (slot < 0) claimed = false;
       }
     }
-    record(slot, claimed, logit, (uint32_t)arc.w >> 31, o, arc_id, prev, bin);
+    add_claim(slot, claimed, flag, bin);
+  }
+
+  // stage one round of candidates (warp-collective); flushes when the buffer fills
+  __device__ __forceinline__ void stage(bool pass, const int4& entry, int& staged, float beam, uint32_t best_sa,
+                                        uint32_t theta_sa) {
+    const int lane = threadIdx.x & 31;
+    const unsigned m = __ballot_sync(0xffffffffu, pass);
+    const int n = __popc(m);
+    const int rank = __popc(m & ((1u << lane) - 1u));
+    if (staged + n < kStage) {
+      if (pass) sts128(stage_sa + 16u * (staged + rank), entry);
+      staged += n;
+    } else {
+      const int room = kStage - staged;
+      if (pass && rank < room) sts128(stage_sa + 16u * (staged + rank), entry);
+      __syncwarp();
+      flush(kStage, beam, best_sa, theta_sa);
+      __syncwarp();
+      if (pass && rank >= room) sts128(stage_sa + 16u * (rank - room), entry);
+      staged = n - room;
+    }
   }
 
   // ---- rows a1 + a2: load-balanced emitting expansion ----
-  // Each warp takes 32 frontier tokens, scans their emitting degrees, and walks the flattened
-  // arcs 32*R at a time; the owner of arc j is found from head flags + a max-scan (no search).
+  // Each warp takes 32 frontier tokens, scans their emitting degrees, walks the flattened arcs
+  // 32*R at a time (owner of arc j from head flags + a max-scan), filters the candidates against
+  // the running beam and the max-active bound, and stages the survivors so that the table
+  // inserts run with full warps.  The winner key's low word is (token << off_bits | offset):
+  // with the frontier sorted by state it orders exactly like the canonical arc id (R9).
   __device__ void expand(const float* __restrict__ row) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_f = S.L.n_front;
     const int4* Fin = F0 + (size_t)S.L.cur * p.FCAP;
-    const int32_t layer_base = S.L.layer_base;
-    const float ref = S.ref, inv_w = S.inv_w;
+    const float ref = S.ref, inv_w = S.inv_w, beam = p.beam;
+    const int off_bits = S.off_bits;
     const uint32_t best_sa = saddr(&S.best_ord), theta_sa = saddr(&S.theta), nclaim_sa = saddr(&S.n_claim);
     long long arcs_total = 0;
     int last_theta = 0;
+    int staged = 0;   // warp-uniform
     for (int tb = warp * 32; tb < n_f; tb += NW * 32) {
       const int i = tb + lane;
       int deg = 0, eb = 0;
       float cost = 0.f;
       if (i < n_f) {
-        int4 f = __ldcg(Fin + i);
+        const int4 f = __ldcg(Fin + i);
         eb = f.z;
         deg = f.w;
         cost = __int_as_float(f.y);
       }
       arcs_total += deg;
+      if (off_bits < 31 && deg > (1 << off_bits)) S.status = WFST_ERR_CAPACITY;   // key split overflow
       if (deg > kBig) {
-        int k = atomicAdd(&S.n_big, 1);
+        const int k = atomicAdd(&S.n_big, 1);
         if (k < kBigCap) {
           S.big[k] = i;
           deg = 0;
@@ -440,7 +462,7 @@ struct Frame {
       const int excl = incl - deg;
       const int total = __shfl_sync(0xffffffffu, incl, 31);
       for (int r0 = 0; r0 < total; r0 += 32 * R) {
-        int a[R], own[R];
+        int a[R], own[R], offv[R];
         bool v[R];
 #pragma unroll
         for (int u = 0; u < R; u++) {
@@ -453,7 +475,7 @@ struct Frame {
           wbuf[lane] = -1;
 #pragma unroll
           for (int d = 1; d < 32; d <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, o, d);
+            const int y = __shfl_up_sync(0xffffffffu, o, d);
             if (lane >= d) o = max(o, y);
           }
           if (cm) o = max(o, __ffs(cm) - 1);
@@ -462,7 +484,8 @@ struct Frame {
           v[u] = j < total;
           const int eb_o = __shfl_sync(0xffffffffu, eb, own[u]);
           const int ex_o = __shfl_sync(0xffffffffu, excl, own[u]);
-          a[u] = eb_o + (j - ex_o);
+          offv[u] = j - ex_o;
+          a[u] = eb_o + offv[u];
           __syncwarp();
         }
         int4 arc[R];
@@ -471,11 +494,18 @@ struct Frame {
         float L[R];
 #pragma unroll
         for (int u = 0; u < R; u++) L[u] = v[u] ? __ldg(row + arc[u].z) : 0.0f;
+        const uint32_t bo = (uint32_t)lds32(best_sa);
+        const int th = lds32(theta_sa);
+        const float bound = bo == 0xFFFFFFFFu ? INFINITY : __fadd_rn(float_of_ord(bo), beam);
 #pragma unroll
         for (int u = 0; u < R; u++) {
           const float co = __shfl_sync(0xffffffffu, cost, own[u]);
-          float c = __fadd_rn(__fsub_rn(__fadd_rn(co, __int_as_float(arc[u].y)), L[u]), 0.0f);
-          emit_one(v[u], c, arc[u], (uint32_t)a[u], layer_base + tb + own[u], ref, inv_w, best_sa, theta_sa);
+          const float c = __fadd_rn(__fsub_rn(__fadd_rn(co, __int_as_float(arc[u].y)), L[u]), 0.0f);
+          const int bin = bin_of(c, ref, inv_w);
+          const bool pass = v[u] && c < bound && bin < th;
+          const uint32_t low = ((uint32_t)(tb + own[u]) << off_bits) | (uint32_t)offv[u];
+          const int4 entry = make_int4(arc[u].x, (int)ord_of(c), (int)low, bin | (int)(arc[u].w & 0x80000000));
+          stage(pass, entry, staged, beam, best_sa, theta_sa);
         }
         if (p.alpha > 0) {
           const int nc = __shfl_sync(0xffffffffu, lds32(nclaim_sa), 0);
@@ -486,6 +516,9 @@ struct Frame {
         }
       }
     }
+    __syncwarp();
+    if (staged > 0) flush(staged, beam, best_sa, theta_sa);
+    staged = 0;
     __syncthreads();
     // tokens with large out-degree (hub states): all threads share their arcs
     const int nbig = min(S.n_big, kBigCap);
@@ -506,18 +539,30 @@ struct Frame {
         float L[R];
 #pragma unroll
         for (int u = 0; u < R; u++) L[u] = v[u] ? __ldg(row + arc[u].z) : 0.0f;
+        const uint32_t bo = (uint32_t)lds32(best_sa);
+        const int th = lds32(theta_sa);
+        const float bound = bo == 0xFFFFFFFFu ? INFINITY : __fadd_rn(float_of_ord(bo), beam);
 #pragma unroll
         for (int u = 0; u < R; u++) {
-          float c = __fadd_rn(__fsub_rn(__fadd_rn(cost, __int_as_float(arc[u].y)), L[u]), 0.0f);
-          emit_one(v[u], c, arc[u], (uint32_t)(f.z + j0 + u * BS + tid), layer_base + i, ref, inv_w, best_sa, theta_sa);
+          const float c = __fadd_rn(__fsub_rn(__fadd_rn(cost, __int_as_float(arc[u].y)), L[u]), 0.0f);
+          const int bin = bin_of(c, ref, inv_w);
+          const bool pass = v[u] && c < bound && bin < th;
+          const int j = j0 + u * BS + tid;
+          const uint32_t low = ((uint32_t)i << off_bits) | (uint32_t)j;
+          const int4 entry = make_int4(arc[u].x, (int)ord_of(c), (int)low, bin | (int)(arc[u].w & 0x80000000));
+          stage(pass, entry, staged, beam, best_sa, theta_sa);
         }
-        if (p.alpha > 0 && warp == 0) {
+        if (p.alpha > 0) {
           const int nc = __shfl_sync(0xffffffffu, lds32(nclaim_sa), 0);
-          if (nc >= p.alpha) update_theta();
+          if (nc >= p.alpha && nc - last_theta >= 512) {
+            update_theta();
+            last_theta = nc;
+          }
         }
-        __syncwarp();
       }
     }
+    __syncwarp();
+    if (staged > 0) flush(staged, beam, best_sa, theta_sa);
     arcs_total = block_sum64<BS>(arcs_total, S.warp_tmp64);
     if (tid == 0) S.emit_arcs = arcs_total;
     __syncthreads();
@@ -541,7 +586,7 @@ struct Frame {
     // entry is >= best), 10-bit digits from the top set bit of ord(beam_cut) - ord(best); the
     // first pass also counts the in-beam entries.
     const uint32_t ob = S.best_ord;
-    const uint32_t span = ord_of(beam_cut) - ob;   // beam_cut = +inf gives a large span: fine
+    const uint32_t span = ord_of(beam_cut) - ob;
     const int nbits = span ? 32 - __clz(span) : 1;
     int shift = ((nbits + 9) / 10) * 10 - 10;
     if (tid == 0) {
@@ -625,7 +670,7 @@ struct Frame {
     const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
     for (int i0 = 0; i0 < n_claim; i0 += BS) {   // warp-uniform trip count (warp_append)
       const int i = i0 + tid;
-      const uint32_t cl = i < n_claim ? claim[i] : 0u;
+      const uint32_t cl = i < n_claim ? __ldcg(claim + i) : 0u;
       bool need = false;
       if (cl & 0x80000000u) {
         const float c = key_cost(read_slot((int)(cl & 0x7FFFFFFFu)));
@@ -647,18 +692,17 @@ struct Frame {
       uint32_t* Wn = wl0 + (size_t)(cur ^ 1) * p.FCAP;
       for (int i0 = 0; i0 < n_wl; i0 += BS) {
         const int i = i0 + tid;
-        int e0 = 0, e1 = 0, src_slot = 0;
+        int e0 = 0, e1 = 0;
         float cp = 0.f;
         if (i < n_wl) {
-          src_slot = (int)W[i];
-          const u64 v = read_slot(src_slot);
+          const u64 v = read_slot((int)__ldcg(W + i));
           cp = key_cost(v);
           const int4 si = __ldg(p.state_info + (uint32_t)v);
           e0 = si.y;
           e1 = si.z;
         }
         // each thread relaxes its token's epsilon arcs (epsilon out-degrees are small)
-        int n_more = e1 - e0;
+        const int n_more = e1 - e0;
         int maxd = n_more;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) maxd = max(maxd, __shfl_xor_sync(0xffffffffu, maxd, o));
@@ -667,20 +711,20 @@ struct Frame {
           int4 arc = make_int4(0, 0, 0, 0);
           bool claimed = false, logit = false, strict = false;
           int slot = -1;
-          uint32_t o = 0;
           if (v) {
             arc = __ldg(p.arcs + e0 + k);
             const float c = __fadd_rn(__fadd_rn(cp, __int_as_float(arc.y)), 0.0f);
             relax++;
-            if (keep(c)) {
-              o = ord_of(c);
+            if (c < cut_b && c <= cut_a) {
+              const uint32_t o = ord_of(c);
               const uint32_t q = (uint32_t)arc.x;
               slot = insert(q, ((u64)o << 32) | q, claimed, logit, strict);
-              if (slot < 0) claimed = logit = strict = false;
+              if (slot >= 0 && logit) red_min_g64(win_eps + slot, ((u64)o << 32) | (uint32_t)(e0 + k));
+              if (slot < 0) claimed = strict = false;
             }
           }
           const uint32_t has_eps = (uint32_t)arc.w >> 31;
-          record(slot, claimed, logit, has_eps, o, (uint32_t)(e0 + k), kEpsFlag | src_slot, -1);
+          add_claim(slot, claimed, has_eps, -1);
           const bool push = strict && has_eps;
           const int wi = warp_append(push, saddr(&S.n_wl_next));
           if (push) {
@@ -698,56 +742,26 @@ struct Frame {
     if (tid == 0) S.eps_relax = tot;
   }
 
-  // winner of each slot = min (arc, back-pointer) among logged entries whose cost equals the
-  // slot's final cost (R9: ties broken by arc id)
-  __device__ void resolve_winners() {
-    const int tid = threadIdx.x;
-    const int n_log = min(S.n_log, p.LOGCAP);
-    constexpr int U = 4;
-    for (int i0 = 0; i0 < n_log; i0 += BS * U) {
-      int4 e[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int i = i0 + u * BS + tid;
-        e[u] = i < n_log ? __ldcg(lg + i) : make_int4(-1, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        if (e[u].x < 0) continue;
-        const u64 v = read_slot(e[u].x);
-        if ((uint32_t)(v >> 32) == (uint32_t)e[u].y)
-          atomicMin(win + e[u].x, ((u64)(uint32_t)e[u].z << 32) | (uint32_t)e[u].w);
-      }
-    }
-    __syncthreads();
-  }
-
-  // ---- rows a4 + a6: contraction into the next frontier (cost-bucketed) + records ----
+  // ---- rows a4 + a6: contraction into the next frontier (sorted by state) + records ----
   __device__ void contract() {
     const int tid = threadIdx.x;
     const int n_claim = min(S.n_claim, p.FCAP);
-    if (tid < kNBuck) S.bucket_base[tid] = 0;
+    const int4* Fin = F0 + (size_t)S.L.cur * p.FCAP;
+    const int32_t prev_base = S.L.layer_base;
+    const int off_bits = S.off_bits;
+    const uint32_t off_mask = off_bits >= 32 ? 0xFFFFFFFFu : ((1u << off_bits) - 1u);
+    const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
     if (tid == 0) {
       S.n_surv = 0;
-      S.n_fix = 0;
-      // bucket range: [best, cutoff)
-      const float best = float_of_ord(S.best_ord);
-      float cut = S.use_alpha ? fminf(S.beam_cut, S.kalpha) : S.beam_cut;
-      float span = __fsub_rn(cut, best);
-      if (!(span > 0.0f) || isinf(span)) span = 32.0f;
-      S.bk_ref = best;
-      S.bk_inv = (float)kNBuck / span;
+      S.min_surv = INFINITY;
     }
     __syncthreads();
-    long long epsd = 0;
     float mn = INFINITY;
-    const float bk_ref = S.bk_ref, bk_inv = S.bk_inv;
-    const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
     constexpr int U = 4;
-    // pass 1: keep() over the claims, gather state records, stage survivors
+    // pass 1: drain the tables; survivors -> tmp {state, cost, arc | eps flag, prev | eps source}
     for (int i0 = 0; i0 < n_claim; i0 += BS * U) {
       int slot[U];
-      u64 v[U];
+      u64 v[U], we[U], wp[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int i = i0 + u * BS + tid;
@@ -756,18 +770,27 @@ struct Frame {
 #pragma unroll
       for (int u = 0; u < U; u++) {
         v[u] = slot[u] >= 0 ? read_slot(slot[u]) : kEmpty;
-        if (slot[u] >= 0) clear_slot(slot[u]);
+        we[u] = slot[u] >= 0 ? __ldcg(win_e + slot[u]) : kEmpty;
+        wp[u] = slot[u] >= 0 ? __ldcg(win_eps + slot[u]) : kEmpty;
       }
-      int4 si[U];
-      u64 w[U];
       bool k[U];
+      int tokf[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        const float cu = key_cost(v[u]);
-        k[u] = slot[u] >= 0 && cu < cut_b && cu <= cut_a;
-        si[u] = k[u] ? __ldg(p.state_info + (uint32_t)v[u]) : make_int4(0, 0, 0, 0);
-        w[u] = k[u] ? __ldcg(win + slot[u]) : 0ull;
+        if (slot[u] >= 0) {
+          clear_slot(slot[u]);
+          win_e[slot[u]] = kEmpty;
+          win_eps[slot[u]] = kEmpty;
+        }
+        const float c = key_cost(v[u]);
+        k[u] = slot[u] >= 0 && c < cut_b && c <= cut_a;
+        const uint32_t fo = (uint32_t)(v[u] >> 32);
+        const bool e_ok = we[u] != kEmpty && (uint32_t)(we[u] >> 32) == fo;
+        tokf[u] = (k[u] && e_ok) ? (int)(off_bits >= 32 ? 0u : ((uint32_t)we[u] >> off_bits)) : -1;
       }
+      int eb[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) eb[u] = tokf[u] >= 0 ? __ldcg(&Fin[tokf[u]].z) : 0;
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int r = warp_append(k[u], saddr(&S.n_surv));
@@ -776,32 +799,40 @@ struct Frame {
           S.status = WFST_ERR_CAPACITY;
           continue;
         }
+        const uint32_t fo = (uint32_t)(v[u] >> 32);
+        const bool p_ok = wp[u] != kEmpty && (uint32_t)(wp[u] >> 32) == fo;
+        const uint32_t ea = (uint32_t)wp[u];   // epsilon arc id; 0xFFFFFFFF = the start token
+        int32_t arc = -1, prev = -1;
+        uint32_t eps = 0;
+        if (tokf[u] >= 0) {
+          const int32_t a_e = eb[u] + (int32_t)((uint32_t)we[u] & off_mask);
+          if (p_ok && ea != 0xFFFFFFFFu && (uint32_t)a_e > ea) {   // R9: smaller arc id wins
+            arc = (int32_t)ea;
+            eps = 1;
+          } else {
+            arc = a_e;
+            prev = prev_base + tokf[u];
+          }
+        } else if (p_ok && ea != 0xFFFFFFFFu) {
+          arc = (int32_t)ea;
+          eps = 1;
+        }
+        if (eps) prev = __ldg(&p.arcs[arc].w) & 0x7FFFFFFF;   // source state, resolved below
         const float c = key_cost(v[u]);
-        int bk = (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1));
-        red_add_s(saddr(&S.bucket_base[bk]), 1);
-        tmpA[r] = make_int4((int)(uint32_t)v[u], __float_as_int(c), si[u].x, si[u].y - si[u].x);
-        tmpB[r] = make_int4(slot[u], (int)(uint32_t)(w[u] >> 32), (int)(uint32_t)w[u], bk);
-        epsd += si[u].z - si[u].y;
+        tmp[r] = make_int4((int)(uint32_t)v[u], __float_as_int(c), eps ? (int)((uint32_t)arc | 0x80000000u) : arc,
+                           prev);
         mn = fminf(mn, c);
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     if ((tid & 31) == 0) S.warp_tmp[tid >> 5] = __float_as_int(mn);
-    const long long eps_deg = block_sum64<BS>(epsd, S.warp_tmp64);
+    __syncthreads();
     if (tid == 0) {
       float m = INFINITY;
       for (int w = 0; w < NW; w++) m = fminf(m, __int_as_float(S.warp_tmp[w]));
       S.min_surv = m;
-      S.eps_deg = eps_deg;
-      int acc = 0;
-      for (int b = 0; b < kNBuck; b++) {
-        const int n = S.bucket_base[b];
-        S.bucket_base[b] = acc;
-        acc += n;
-      }
     }
-    __syncthreads();
     const int n_surv = min(S.n_surv, p.FCAP);
     const int32_t rb = S.L.rec_used;
     if ((long long)rb + n_surv > p.R_cap) {
@@ -809,32 +840,100 @@ struct Frame {
       __syncthreads();
       return;
     }
-    int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
-    // pass 2: place survivors in cost-bucket order; records {arc, prev}
+    // bucket sort of the survivors by state id, in the drained table memory:
+    // [kSortBuckets counters][n_surv x {state, tmp index}] (global scratch if that does not fit)
+    const bool on_chip = (size_t)kSortBuckets * 4 + (size_t)n_surv * 8 <= (size_t)p.C * 8;
+    const uint32_t cnt_sa = tab_sa;
+    const uint32_t pairs_sa = tab_sa + kSortBuckets * 4;
+    const unsigned long long nq = (unsigned long long)p.n_states;
+    for (int i = tid; i < kSortBuckets; i += BS) sts32(cnt_sa + 4u * i, 0);
+    __syncthreads();
     for (int r = tid; r < n_surv; r += BS) {
-      const int4 A = tmpA[r];
-      const int4 Bv = tmpB[r];
-      const int pos = atom_add_s(saddr(&S.bucket_base[Bv.w]), 1);
-      Fout[pos] = A;
-      slotrec[Bv.x] = pos;
-      const int32_t arc = (uint32_t)Bv.y == 0xFFFFFFFFu ? -1 : Bv.y;
-      int32_t pv = Bv.z;
-      if (pv < -1) {   // epsilon back-pointer: a slot of this layer, resolved in pass 3
-        const int fi = atomicAdd(&S.n_fix, 1);
-        epsfix[fi] = pos;
-      }
-      rec[rb + pos] = make_int2(arc, pv);
-      if (rec_cost) rec_cost[rb + pos] = __int_as_float(A.y);
+      const uint32_t q = (uint32_t)__ldcg(&tmp[r].x);
+      red_add_s(cnt_sa + 4u * (uint32_t)(((unsigned long long)q * kSortBuckets) / nq), 1);
     }
     __syncthreads();
-    // pass 3: epsilon back-pointers -> record index of the source survivor
-    const int n_fix = S.n_fix;
-    for (int k = tid; k < n_fix; k += BS) {
-      const int pos = epsfix[k];
-      int2 e = rec[rb + pos];
-      e.y = rb + slotrec[e.y & 0x7FFFFFFF];
-      rec[rb + pos] = e;
+    if (tid < 32) {   // exclusive scan of the bucket counters (warp 0)
+      constexpr int PER = kSortBuckets / 32;
+      int s = 0;
+      for (int i = 0; i < PER; i++) s += lds32(cnt_sa + 4u * (tid * PER + i));
+      const int incl = warp_incl_scan(s);
+      int run = incl - s;
+      for (int i = 0; i < PER; i++) {
+        const uint32_t a = cnt_sa + 4u * (tid * PER + i);
+        const int c = lds32(a);
+        sts32(a, run);
+        run += c;
+      }
     }
+    __syncthreads();
+    for (int r = tid; r < n_surv; r += BS) {
+      const uint32_t q = (uint32_t)__ldcg(&tmp[r].x);
+      const int pos = atom_add_s(cnt_sa + 4u * (uint32_t)(((unsigned long long)q * kSortBuckets) / nq), 1);
+      if (on_chip) {
+        sts32(pairs_sa + 8u * pos, (int)q);
+        sts32(pairs_sa + 8u * pos + 4, r);
+      } else {
+        sort2[pos] = make_int2((int)q, r);
+      }
+    }
+    __syncthreads();
+    // insertion sort inside each bucket (the counters now hold bucket ends)
+    for (int bk = tid; bk < kSortBuckets; bk += BS) {
+      const int end = lds32(cnt_sa + 4u * bk);
+      const int beg = bk ? lds32(cnt_sa + 4u * (bk - 1)) : 0;
+      for (int x = beg + 1; x < end; x++) {
+        const int2 e = on_chip ? make_int2(lds32(pairs_sa + 8u * x), lds32(pairs_sa + 8u * x + 4)) : sort2[x];
+        int y = x - 1;
+        while (y >= beg) {
+          const int2 f = on_chip ? make_int2(lds32(pairs_sa + 8u * y), lds32(pairs_sa + 8u * y + 4)) : sort2[y];
+          if ((uint32_t)f.x <= (uint32_t)e.x) break;
+          if (on_chip) {
+            sts32(pairs_sa + 8u * (y + 1), f.x);
+            sts32(pairs_sa + 8u * (y + 1) + 4, f.y);
+          } else {
+            sort2[y + 1] = f;
+          }
+          y--;
+        }
+        if (on_chip) {
+          sts32(pairs_sa + 8u * (y + 1), e.x);
+          sts32(pairs_sa + 8u * (y + 1) + 4, e.y);
+        } else {
+          sort2[y + 1] = e;
+        }
+      }
+    }
+    __syncthreads();
+    // write the sorted frontier and the records; an epsilon winner finds its source's position
+    // by binary search over the sorted states
+    int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
+    long long epsd = 0;
+    for (int pos = tid; pos < n_surv; pos += BS) {
+      const int r = on_chip ? lds32(pairs_sa + 8u * pos + 4) : sort2[pos].y;
+      const int4 t = __ldcg(tmp + r);
+      const int4 si = __ldg(p.state_info + t.x);
+      Fout[pos] = make_int4(t.x, t.y, si.x, si.y - si.x);
+      epsd += si.z - si.y;
+      int32_t arc = t.z, prev = t.w;
+      if (t.z != -1 && (t.z & 0x80000000)) {    // epsilon winner: prev = source's record
+        arc = t.z & 0x7FFFFFFF;
+        int lo = 0, hi = n_surv - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const int sm = on_chip ? lds32(pairs_sa + 8u * mid) : sort2[mid].x;
+          if ((uint32_t)sm < (uint32_t)prev) lo = mid + 1; else hi = mid;
+        }
+        prev = rb + lo;
+      }
+      rec[rb + pos] = make_int2(arc, prev);
+      if (rec_cost) rec_cost[rb + pos] = __int_as_float(t.y);
+    }
+    const long long eps_deg = block_sum64<BS>(epsd, S.warp_tmp64);
+    if (tid == 0) S.eps_deg = eps_deg;
+    // give the table memory back (empty slots)
+    const int used = (int)(((size_t)kSortBuckets * 4 + (on_chip ? (size_t)n_surv * 8 : 0) + 7) / 8);
+    for (int i = tid; i < used; i += BS) sts64(tab_sa + 8u * i, kEmpty);
     __syncthreads();
   }
 
@@ -846,7 +945,6 @@ struct Frame {
       S.theta = kNB;
       S.n_claim = 0;
       S.n_ovf = 0;
-      S.n_log = 0;
       S.n_big = 0;
       S.n_wl = 0;
       S.use_alpha = 0;
@@ -858,6 +956,9 @@ struct Frame {
       const float half = isinf(p.beam) ? 32.0f : 0.5f * p.beam;
       S.ref = S.L.front_best - half;
       S.inv_w = (float)kNB / (4.0f * half);
+      // token << off_bits | offset orders like the arc id when tokens are sorted by state
+      const int nf = max(S.L.n_front, 1);
+      S.off_bits = __clz(nf);   // 32 - bits(nf)
     }
     __syncthreads();
   }
@@ -865,6 +966,10 @@ struct Frame {
   __device__ void clear_all() {
     for (int i = threadIdx.x; i < p.C; i += BS) sts64(tab_sa + 8u * i, kEmpty);
     for (int i = threadIdx.x; i < p.C_ovf; i += BS) ovf[i] = kEmpty;
+    for (int i = threadIdx.x; i < p.FCAP; i += BS) {
+      win_e[i] = kEmpty;
+      win_eps[i] = kEmpty;
+    }
     __syncthreads();
   }
 
@@ -937,9 +1042,10 @@ struct Frame {
         slot = insert((uint32_t)p.start, ((u64)o << 32) | (uint32_t)p.start, claimed, logit, strict);
         const int4 si = __ldg(p.state_info + p.start);
         flag = si.z > si.y ? 1u : 0u;
-        if (slot < 0) claimed = logit = false;
+        if (slot >= 0) win_eps[slot] = ((u64)o << 32) | 0xFFFFFFFFull;   // the start token
+        else claimed = false;
       }
-      record(slot, claimed, logit, flag, o, 0xFFFFFFFFu, -1, -1);
+      add_claim(slot, claimed, flag, -1);
       if (tid == 0) {
         S.best_ord = o;
         S.n_claim_emit = 1;
@@ -947,7 +1053,6 @@ struct Frame {
     }
     __syncthreads();
     eps_closure();
-    resolve_winners();
     contract();
     finish_frame(-1, false);
   }
@@ -984,8 +1089,6 @@ struct Frame {
     tick(t0, 1);
     eps_closure();
     tick(t0, 2);
-    resolve_winners();
-    tick(t0, 3);
     contract();
     tick(t0, 4);
     finish_frame(t, true);
@@ -998,6 +1101,7 @@ __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SmemCtl S;
   __shared__ int s_wbuf[BS];
+  __shared__ __align__(16) int4 s_stage[(BS / 32) * kStage];
   u64* tab = (u64*)smem_raw;
   int* hist = (int*)(tab + p.C);
   const int tid = threadIdx.x;
@@ -1006,7 +1110,7 @@ __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
   s_wbuf[tid] = -1;
   if (tid == 0) S.status = WFST_OK;
   __syncthreads();
-  Frame<BS, R> fr(p, S, tab_sa, hist, s_wbuf + (tid & ~31));
+  Frame<BS, R> fr(p, S, tab_sa, hist, s_wbuf + (tid & ~31), saddr(s_stage + (tid >> 5) * kStage));
   while (true) {
     if (tid == 0) S.item = atomicAdd(p.q_head, 1);
     __syncthreads();

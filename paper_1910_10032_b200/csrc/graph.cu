@@ -159,10 +159,10 @@ wfst_status build_graph(int32_t Q, int32_t start, int64_t E, const int32_t* src,
     r.x = dst[i];
     memcpy(&r.y, &w, 4);
     r.z = ilabel[i] - 1;  // -1 for epsilon
-    r.w = olabel[i];
+    r.w = s;              // source state (| destination-has-epsilon flag, below)
     arcs[k] = r;
   }
-  // bit 31 of the olabel field: "the destination state has epsilon arcs" (lets the kernel
+  // bit 31 of the source field: "the destination state has epsilon arcs" (lets the kernel
   // build epsilon worklists without gathering state records)
   for (int64_t k = 0; k < E; k++) {
     int32_t d = arcs[k].x;
@@ -190,18 +190,22 @@ wfst_status build_graph(int32_t Q, int32_t start, int64_t E, const int32_t* src,
     return cuda_fail(e, "cudaSetDevice");
   }
   size_t bs = sizeof(int4) * (size_t)Q, ba = sizeof(int4) * (size_t)(E > 0 ? E : 1);
+  size_t bo = sizeof(int32_t) * (size_t)(E > 0 ? E : 1);
   e = cudaMalloc(&g->d_state, bs);
   if (e == cudaSuccess) e = cudaMalloc(&g->d_arcs, ba);
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_olabel, bo);
+  if (e == cudaSuccess && E > 0) e = cudaMemcpy(g->d_olabel, g->h_olabel.data(), bo, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(g->d_state, st.data(), bs, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && E > 0) e = cudaMemcpy(g->d_arcs, arcs.data(), sizeof(int4) * E, cudaMemcpyHostToDevice);
   cudaSetDevice(prev_dev);
   if (e != cudaSuccess) {
     cudaFree(g->d_state);
     cudaFree(g->d_arcs);
+    cudaFree(g->d_olabel);
     delete g;
     return cuda_fail(e, "graph upload");
   }
-  g->device_bytes = (int64_t)(bs + ba);
+  g->device_bytes = (int64_t)(bs + ba + bo);
   *out = g;
   return WFST_OK;
 }
@@ -319,6 +323,7 @@ void wfst_graph_free(wfst_graph_t g) {
   cudaSetDevice(g->device);
   cudaFree(g->d_state);
   cudaFree(g->d_arcs);
+  cudaFree(g->d_olabel);
   cudaSetDevice(prev);
   delete g;
 }

@@ -30,8 +30,9 @@ struct wfst_graph_s {
   int32_t max_pdf = -1;
   // state_info[q] = {e_begin, e_end (= eps begin), eps_end, final cost bits}     16 B/state
   int4* d_state = nullptr;
-  // arcs[a] = {dst, weight bits, pdf (-1 for epsilon), olabel}                   16 B/arc
+  // arcs[a] = {dst, weight bits, pdf (-1 for epsilon), src | dst_has_eps << 31}  16 B/arc
   int4* d_arcs = nullptr;
+  int32_t* d_olabel = nullptr;   // olabels (read only by the end-of-stream traceback)
   int64_t device_bytes = 0;
   std::vector<int64_t> perm;     // canonical arc -> input arc
   std::vector<int32_t> h_dst;    // canonical order (host copy for debug queries)
