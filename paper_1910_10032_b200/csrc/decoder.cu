@@ -271,7 +271,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     d->R_cap = (int64_t)(d->TMAX / 4 + 1) * per_frame;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-      int64_t per_lane_other = (int64_t)d->FCAP * (32 + 4 + 8 + 8 + 16 + 8 + 8) + (int64_t)d->C_ovf * 8 +
+      int64_t per_lane_other = (int64_t)d->FCAP * (32 + 4 + 8 + 16 + 16 + 4 + 8) + (int64_t)d->C_ovf * 8 +
                                (int64_t)d->TMAX * 60;
       int64_t budget = (int64_t)(free_b / 2) / n_streams - per_lane_other;
       int64_t cap = budget / (int64_t)(sizeof(int2) + (d->o.debug_costs ? 4 : 0));
@@ -299,10 +299,10 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   };
   size_t i_front = add(L * 2 * FC * sizeof(int4));
   size_t i_claim = add(L * FC * 4);
-  size_t i_win_e = add(L * FC * 8);
-  size_t i_win_eps = add(L * FC * 8);
+  size_t i_win = add(L * FC * 8);
   size_t i_tmp = add(L * FC * sizeof(int4));
-  size_t i_sort2 = add(L * FC * sizeof(int2));
+  size_t i_gmap = add(L * 2 * FC * 8);
+  size_t i_fix = add(L * FC * 4);
   size_t i_ovf = add(L * (size_t)d->C_ovf * 8);
   size_t i_wl = add(L * 2 * FC * 4);
   size_t i_rec = add(L * (size_t)d->R_cap * sizeof(int2));
@@ -342,10 +342,10 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.lanes_st = d->d_lanes;
   kp.front = (int4*)(base + parts[i_front].off);
   kp.claim = (uint32_t*)(base + parts[i_claim].off);
-  kp.win_e = (u64*)(base + parts[i_win_e].off);
-  kp.win_eps = (u64*)(base + parts[i_win_eps].off);
+  kp.win = (u64*)(base + parts[i_win].off);
   kp.tmp = (int4*)(base + parts[i_tmp].off);
-  kp.sort2 = (int2*)(base + parts[i_sort2].off);
+  kp.gmap = (u64*)(base + parts[i_gmap].off);
+  kp.epsfix = (int32_t*)(base + parts[i_fix].off);
   kp.ovf = (u64*)(base + parts[i_ovf].off);
   kp.wl = (uint32_t*)(base + parts[i_wl].off);
   kp.rec = (int2*)(base + parts[i_rec].off);
@@ -356,8 +356,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.q_head = d->d_qhead;
   kp.lane_round = d->d_round;
   e = cudaMemset(base + parts[i_ovf].off, 0xFF, parts[i_ovf].bytes);
-  if (e == cudaSuccess) e = cudaMemset(base + parts[i_win_e].off, 0xFF, parts[i_win_e].bytes);
-  if (e == cudaSuccess) e = cudaMemset(base + parts[i_win_eps].off, 0xFF, parts[i_win_eps].bytes);
+  if (e == cudaSuccess) e = cudaMemset(base + parts[i_win].off, 0xFF, parts[i_win].bytes);
   if (e == cudaSuccess) e = cudaMemset(d->d_lanes, 0, sizeof(LaneState) * L);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {

@@ -25,12 +25,12 @@ constexpr int kModeFrames = 0, kModeInit = 1;
 constexpr int kBig = 64;           // tokens with more emitting arcs are expanded CTA-wide
 constexpr int kBigCap = 256;
 constexpr int kStage = 32;         // per-warp staging buffer (candidates awaiting insertion)
-constexpr int kSortBuckets = 4096; // contraction: bucket sort of survivors by state id
+constexpr int kNBuck = 16;         // cost buckets ordering the next frontier
 
 struct LaneState {
   int32_t status;       // wfst_status, sticky
   int32_t initialized;
-  int32_t n_front;      // survivors in the current frontier (sorted by state id)
+  int32_t n_front;      // survivors in the current frontier (cost-bucketed order)
   int32_t cur;          // frontier buffer holding them
   int32_t frames;       // frames decoded in this utterance
   int32_t layer_base;   // record index of the current layer's first survivor
@@ -56,12 +56,12 @@ struct KParams {
   int64_t R_cap;
   int32_t TMAX;
   LaneState* lanes_st;
-  int4* front;        // [lane][2][FCAP]  {state, cost bits, e_begin, n_emit}, sorted by state
+  int4* front;        // [lane][2][FCAP]  {state, cost bits, e_begin, n_emit}, cost-bucketed
   uint32_t* claim;    // [lane][FCAP]     slot | has_eps << 31, one per distinct state
-  u64* win_e;         // [lane][FCAP]     per slot: min (ord(cost) << 32 | token << k | offset)
-  u64* win_eps;       // [lane][FCAP]     per slot: min (ord(cost) << 32 | epsilon arc id)
-  int4* tmp;          // [lane][FCAP]     contraction scratch {state, cost, arc | eps flag, prev/src}
-  int2* sort2;        // [lane][FCAP]     contraction sort scratch when it does not fit on chip
+  u64* win;           // [lane][FCAP]     per slot: min (ord(cost) << 32 | canonical arc id)
+  int4* tmp;          // [lane][FCAP]     contraction scratch {state, cost, arc, has_eps | bucket}
+  u64* gmap;          // [lane][2*FCAP]   state -> index maps when they do not fit on chip
+  int32_t* epsfix;    // [lane][FCAP]     positions of survivors won by an epsilon arc
   u64* ovf;           // [lane][C_ovf]    global overflow token table
   uint32_t* wl;       // [lane][2][FCAP]  epsilon worklists (slots)
   int2* rec;          // [lane][R_cap]    traceback records {arc, prev}
@@ -75,8 +75,8 @@ struct SmemCtl {
   int32_t item, lane, b, status;
   uint32_t best_ord;
   int32_t theta;
-  int32_t n_claim, n_claim_emit, n_ovf, n_surv, n_in, n_wl, n_wl_next, n_big;
-  int32_t off_bits;   // split of the emitting winner key: token << off_bits | offset
+  int32_t n_claim, n_claim_emit, n_ovf, n_surv, n_in, n_wl, n_wl_next, n_big, n_fix;
+  int32_t bucket_base[kNBuck];
   float beam_cut, kalpha, ref, inv_w, min_surv;
   int32_t use_alpha;
   int32_t radix_prefix, radix_k;
@@ -296,10 +296,10 @@ struct Frame {
   // lane buffers
   int4* F0;           // frontier buffer 0; buffer 1 follows at +FCAP
   uint32_t* claim;
-  u64* win_e;
-  u64* win_eps;
+  u64* win;
   int4* tmp;
-  int2* sort2;
+  u64* gmap;
+  int32_t* epsfix;
   u64* ovf;
   uint32_t* wl0;      // epsilon worklist 0; worklist 1 follows at +FCAP
   int2* rec;
@@ -312,10 +312,10 @@ struct Frame {
     const size_t L = (size_t)lane, FC = (size_t)p.FCAP;
     F0 = p.front + L * 2 * FC;
     claim = p.claim + L * FC;
-    win_e = p.win_e + L * FC;
-    win_eps = p.win_eps + L * FC;
+    win = p.win + L * FC;
     tmp = p.tmp + L * FC;
-    sort2 = p.sort2 + L * FC;
+    gmap = p.gmap + L * 2 * FC;
+    epsfix = p.epsfix + L * FC;
     ovf = p.ovf + L * (size_t)p.C_ovf;
     wl0 = p.wl + L * 2 * FC;
     rec = p.rec + L * (size_t)p.R_cap;
@@ -384,7 +384,7 @@ struct Frame {
     int slot = -1, bin = -1;
     uint32_t flag = 0;
     if (lane < n) {
-      const int4 e = lds128(stage_sa + 16u * lane);   // {q, ord, low key, bin | eps flag << 31}
+      const int4 e = lds128(stage_sa + 16u * lane);   // {q, ord, arc id, bin | eps flag << 31}
       const uint32_t o = (uint32_t)e.y;
       bin = e.w & 0x7FFFFFFF;
       flag = (uint32_t)e.w >> 31;
@@ -395,7 +395,7 @@ struct Frame {
       if (ok) {
         if (o < bo) red_min_s32(best_sa, o);
         slot = insert((uint32_t)e.x, ((u64)o << 32) | (uint32_t)e.x, claimed, logit, strict);
-        if (slot >= 0 && logit) red_min_g64(win_e + slot, ((u64)o << 32) | (uint32_t)e.z);
+        if (slot >= 0 && logit) red_min_g64(win + slot, ((u64)o << 32) | (uint32_t)e.z);
         if (slot < 0) claimed = false;
       }
     }
@@ -427,14 +427,14 @@ struct Frame {
   // Each warp takes 32 frontier tokens, scans their emitting degrees, walks the flattened arcs
   // 32*R at a time (owner of arc j from head flags + a max-scan), filters the candidates against
   // the running beam and the max-active bound, and stages the survivors so that the table
-  // inserts run with full warps.  The winner key's low word is (token << off_bits | offset):
-  // with the frontier sorted by state it orders exactly like the canonical arc id (R9).
+  // inserts run with full warps.  Each improving insert also does a fire-and-forget 64-bit
+  // RED.MIN of (cost, canonical arc id) into the slot's winner word: the min is exactly the
+  // (cost, arc) tie-break of R9.
   __device__ void expand(const float* __restrict__ row) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_f = S.L.n_front;
     const int4* Fin = F0 + (size_t)S.L.cur * p.FCAP;
     const float ref = S.ref, inv_w = S.inv_w, beam = p.beam;
-    const int off_bits = S.off_bits;
     const uint32_t best_sa = saddr(&S.best_ord), theta_sa = saddr(&S.theta), nclaim_sa = saddr(&S.n_claim);
     long long arcs_total = 0;
     int last_theta = 0;
@@ -450,7 +450,6 @@ struct Frame {
         cost = __int_as_float(f.y);
       }
       arcs_total += deg;
-      if (off_bits < 31 && deg > (1 << off_bits)) S.status = WFST_ERR_CAPACITY;   // key split overflow
       if (deg > kBig) {
         const int k = atomicAdd(&S.n_big, 1);
         if (k < kBigCap) {
@@ -462,7 +461,7 @@ struct Frame {
       const int excl = incl - deg;
       const int total = __shfl_sync(0xffffffffu, incl, 31);
       for (int r0 = 0; r0 < total; r0 += 32 * R) {
-        int a[R], own[R], offv[R];
+        int a[R], own[R];
         bool v[R];
 #pragma unroll
         for (int u = 0; u < R; u++) {
@@ -484,8 +483,7 @@ struct Frame {
           v[u] = j < total;
           const int eb_o = __shfl_sync(0xffffffffu, eb, own[u]);
           const int ex_o = __shfl_sync(0xffffffffu, excl, own[u]);
-          offv[u] = j - ex_o;
-          a[u] = eb_o + offv[u];
+          a[u] = eb_o + (j - ex_o);
           __syncwarp();
         }
         int4 arc[R];
@@ -503,8 +501,7 @@ struct Frame {
           const float c = __fadd_rn(__fsub_rn(__fadd_rn(co, __int_as_float(arc[u].y)), L[u]), 0.0f);
           const int bin = bin_of(c, ref, inv_w);
           const bool pass = v[u] && c < bound && bin < th;
-          const uint32_t low = ((uint32_t)(tb + own[u]) << off_bits) | (uint32_t)offv[u];
-          const int4 entry = make_int4(arc[u].x, (int)ord_of(c), (int)low, bin | (int)(arc[u].w & 0x80000000));
+          const int4 entry = make_int4(arc[u].x, (int)ord_of(c), a[u], bin | (int)(arc[u].w & 0x80000000));
           stage(pass, entry, staged, beam, best_sa, theta_sa);
         }
         if (p.alpha > 0) {
@@ -548,8 +545,7 @@ struct Frame {
           const int bin = bin_of(c, ref, inv_w);
           const bool pass = v[u] && c < bound && bin < th;
           const int j = j0 + u * BS + tid;
-          const uint32_t low = ((uint32_t)i << off_bits) | (uint32_t)j;
-          const int4 entry = make_int4(arc[u].x, (int)ord_of(c), (int)low, bin | (int)(arc[u].w & 0x80000000));
+          const int4 entry = make_int4(arc[u].x, (int)ord_of(c), f.z + j, bin | (int)(arc[u].w & 0x80000000));
           stage(pass, entry, staged, beam, best_sa, theta_sa);
         }
         if (p.alpha > 0) {
@@ -719,7 +715,7 @@ struct Frame {
               const uint32_t o = ord_of(c);
               const uint32_t q = (uint32_t)arc.x;
               slot = insert(q, ((u64)o << 32) | q, claimed, logit, strict);
-              if (slot >= 0 && logit) red_min_g64(win_eps + slot, ((u64)o << 32) | (uint32_t)(e0 + k));
+              if (slot >= 0 && logit) red_min_g64(win + slot, ((u64)o << 32) | (uint32_t)(e0 + k));
               if (slot < 0) claimed = strict = false;
             }
           }
@@ -742,55 +738,84 @@ struct Frame {
     if (tid == 0) S.eps_relax = tot;
   }
 
-  // ---- rows a4 + a6: contraction into the next frontier (sorted by state) + records ----
+  // state -> index open-addressing map (8 B entries {state, index}), on chip or global
+  __device__ __forceinline__ void map_put(bool sm, uint32_t base_sa, u64* gbase, uint32_t cap, uint32_t q,
+                                          int idx) const {
+    const u64 e = ((u64)(uint32_t)idx << 32) | q;
+    uint32_t h = __umulhi(q * 0x9E3779B1u, cap);
+    while (true) {
+      u64 old;
+      if (sm) old = atom_cas_s(base_sa + 8u * h, kEmpty, e);
+      else old = atomicCAS(gbase + h, kEmpty, e);
+      if (old == kEmpty) return;
+      h = (h + 1 == cap) ? 0 : h + 1;
+    }
+  }
+  __device__ __forceinline__ int map_get(bool sm, uint32_t base_sa, const u64* gbase, uint32_t cap,
+                                         uint32_t q) const {
+    uint32_t h = __umulhi(q * 0x9E3779B1u, cap);
+    for (uint32_t n = 0; n < cap; n++) {
+      const u64 v = sm ? lds64(base_sa + 8u * h) : __ldcg(gbase + h);
+      if (v == kEmpty) return -1;
+      if ((uint32_t)v == q) return (int)(v >> 32);
+      h = (h + 1 == cap) ? 0 : h + 1;
+    }
+    return -1;
+  }
+
+  // ---- rows a4 + a6: contraction into the next frontier (cost-bucketed) + records ----
+  // Back-pointers: an emitting winner's source is a token of the previous layer (map M1:
+  // state -> token, built here from that frontier); an epsilon winner's source is a survivor
+  // of this layer (map M2 over the survivors whose state has epsilon arcs).  Both maps live in
+  // the drained token table when they fit.
   __device__ void contract() {
     const int tid = threadIdx.x;
     const int n_claim = min(S.n_claim, p.FCAP);
+    const int n_front = S.L.n_front;
     const int4* Fin = F0 + (size_t)S.L.cur * p.FCAP;
     const int32_t prev_base = S.L.layer_base;
-    const int off_bits = S.off_bits;
-    const uint32_t off_mask = off_bits >= 32 ? 0xFFFFFFFFu : ((1u << off_bits) - 1u);
     const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
+    // bucket range [best, cutoff) for the cost order of the next frontier
+    const float bk_ref = float_of_ord(S.best_ord);
+    float span = __fsub_rn(S.use_alpha ? fminf(cut_b, cut_a) : cut_b, bk_ref);
+    if (!(span > 0.0f) || isinf(span)) span = 32.0f;
+    const float bk_inv = (float)kNBuck / span;
+    if (tid < kNBuck) S.bucket_base[tid] = 0;
     if (tid == 0) {
       S.n_surv = 0;
+      S.n_fix = 0;
       S.min_surv = INFINITY;
     }
     __syncthreads();
     float mn = INFINITY;
+    int n_eps_surv = 0;
     constexpr int U = 4;
-    // pass 1: drain the tables; survivors -> tmp {state, cost, arc | eps flag, prev | eps source}
+    // pass 1: drain the tables; survivors -> tmp {state, cost, arc, has_eps << 31 | bucket}
     for (int i0 = 0; i0 < n_claim; i0 += BS * U) {
-      int slot[U];
-      u64 v[U], we[U], wp[U];
+      uint32_t cl[U];
+      u64 v[U], w[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int i = i0 + u * BS + tid;
-        slot[u] = i < n_claim ? (int)(__ldcg(claim + i) & 0x7FFFFFFFu) : -1;
+        cl[u] = i < n_claim ? __ldcg(claim + i) : 0xFFFFFFFFu;
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        v[u] = slot[u] >= 0 ? read_slot(slot[u]) : kEmpty;
-        we[u] = slot[u] >= 0 ? __ldcg(win_e + slot[u]) : kEmpty;
-        wp[u] = slot[u] >= 0 ? __ldcg(win_eps + slot[u]) : kEmpty;
+        const int slot = (int)(cl[u] & 0x7FFFFFFFu);
+        v[u] = cl[u] != 0xFFFFFFFFu ? read_slot(slot) : kEmpty;
+        w[u] = cl[u] != 0xFFFFFFFFu ? __ldcg(win + slot) : kEmpty;
       }
       bool k[U];
-      int tokf[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        if (slot[u] >= 0) {
-          clear_slot(slot[u]);
-          win_e[slot[u]] = kEmpty;
-          win_eps[slot[u]] = kEmpty;
+        if (cl[u] != 0xFFFFFFFFu) {
+          const int slot = (int)(cl[u] & 0x7FFFFFFFu);
+          clear_slot(slot);
+          win[slot] = kEmpty;
         }
         const float c = key_cost(v[u]);
-        k[u] = slot[u] >= 0 && c < cut_b && c <= cut_a;
-        const uint32_t fo = (uint32_t)(v[u] >> 32);
-        const bool e_ok = we[u] != kEmpty && (uint32_t)(we[u] >> 32) == fo;
-        tokf[u] = (k[u] && e_ok) ? (int)(off_bits >= 32 ? 0u : ((uint32_t)we[u] >> off_bits)) : -1;
+        k[u] = cl[u] != 0xFFFFFFFFu && c < cut_b && c <= cut_a;
       }
-      int eb[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) eb[u] = tokf[u] >= 0 ? __ldcg(&Fin[tokf[u]].z) : 0;
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int r = warp_append(k[u], saddr(&S.n_surv));
@@ -799,39 +824,30 @@ struct Frame {
           S.status = WFST_ERR_CAPACITY;
           continue;
         }
-        const uint32_t fo = (uint32_t)(v[u] >> 32);
-        const bool p_ok = wp[u] != kEmpty && (uint32_t)(wp[u] >> 32) == fo;
-        const uint32_t ea = (uint32_t)wp[u];   // epsilon arc id; 0xFFFFFFFF = the start token
-        int32_t arc = -1, prev = -1;
-        uint32_t eps = 0;
-        if (tokf[u] >= 0) {
-          const int32_t a_e = eb[u] + (int32_t)((uint32_t)we[u] & off_mask);
-          if (p_ok && ea != 0xFFFFFFFFu && (uint32_t)a_e > ea) {   // R9: smaller arc id wins
-            arc = (int32_t)ea;
-            eps = 1;
-          } else {
-            arc = a_e;
-            prev = prev_base + tokf[u];
-          }
-        } else if (p_ok && ea != 0xFFFFFFFFu) {
-          arc = (int32_t)ea;
-          eps = 1;
-        }
-        if (eps) prev = __ldg(&p.arcs[arc].w) & 0x7FFFFFFF;   // source state, resolved below
         const float c = key_cost(v[u]);
-        tmp[r] = make_int4((int)(uint32_t)v[u], __float_as_int(c), eps ? (int)((uint32_t)arc | 0x80000000u) : arc,
-                           prev);
+        const int bk = (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1));
+        red_add_s(saddr(&S.bucket_base[bk]), 1);
+        // the winner word's cost must be the slot's final cost (every improving insert RED's)
+        const int32_t arc = (uint32_t)(w[u] >> 32) == (uint32_t)(v[u] >> 32) ? (int32_t)(uint32_t)w[u] : -2;
+        tmp[r] = make_int4((int)(uint32_t)v[u], __float_as_int(c), arc, (int)(cl[u] & 0x80000000u) | bk);
+        n_eps_surv += (cl[u] >> 31);
         mn = fminf(mn, c);
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     if ((tid & 31) == 0) S.warp_tmp[tid >> 5] = __float_as_int(mn);
-    __syncthreads();
+    const long long n_eps_tot = block_sum64<BS>(n_eps_surv, S.warp_tmp64);   // barriers
     if (tid == 0) {
       float m = INFINITY;
       for (int w = 0; w < NW; w++) m = fminf(m, __int_as_float(S.warp_tmp[w]));
       S.min_surv = m;
+      int acc = 0;
+      for (int b = 0; b < kNBuck; b++) {
+        const int n = S.bucket_base[b];
+        S.bucket_base[b] = acc;
+        acc += n;
+      }
     }
     const int n_surv = min(S.n_surv, p.FCAP);
     const int32_t rb = S.L.rec_used;
@@ -840,100 +856,68 @@ struct Frame {
       __syncthreads();
       return;
     }
-    // bucket sort of the survivors by state id, in the drained table memory:
-    // [kSortBuckets counters][n_surv x {state, tmp index}] (global scratch if that does not fit)
-    const bool on_chip = (size_t)kSortBuckets * 4 + (size_t)n_surv * 8 <= (size_t)p.C * 8;
-    const uint32_t cnt_sa = tab_sa;
-    const uint32_t pairs_sa = tab_sa + kSortBuckets * 4;
-    const unsigned long long nq = (unsigned long long)p.n_states;
-    for (int i = tid; i < kSortBuckets; i += BS) sts32(cnt_sa + 4u * i, 0);
-    __syncthreads();
-    for (int r = tid; r < n_surv; r += BS) {
-      const uint32_t q = (uint32_t)__ldcg(&tmp[r].x);
-      red_add_s(cnt_sa + 4u * (uint32_t)(((unsigned long long)q * kSortBuckets) / nq), 1);
+    // maps in the drained table: M1 (prev tokens) then M2 (this layer's epsilon-capable states)
+    const uint32_t cap1 = (uint32_t)max(n_front + (n_front >> 2) + 32, 64);
+    const uint32_t cap2 = (uint32_t)max((int)n_eps_tot * 2 + 32, 64);
+    const bool sm = (size_t)(cap1 + cap2) <= (size_t)p.C;
+    const uint32_t m1_sa = tab_sa, m2_sa = tab_sa + 8u * cap1;
+    u64* g1 = gmap;
+    u64* g2 = gmap + cap1;
+    if (!sm && cap1 + cap2 > 2u * (uint32_t)p.FCAP) {
+      if (tid == 0) S.status = WFST_ERR_CAPACITY;
+      __syncthreads();
+      return;
     }
+    if (!sm)
+      for (uint32_t i = tid; i < cap1 + cap2; i += BS) gmap[i] = kEmpty;
     __syncthreads();
-    if (tid < 32) {   // exclusive scan of the bucket counters (warp 0)
-      constexpr int PER = kSortBuckets / 32;
-      int s = 0;
-      for (int i = 0; i < PER; i++) s += lds32(cnt_sa + 4u * (tid * PER + i));
-      const int incl = warp_incl_scan(s);
-      int run = incl - s;
-      for (int i = 0; i < PER; i++) {
-        const uint32_t a = cnt_sa + 4u * (tid * PER + i);
-        const int c = lds32(a);
-        sts32(a, run);
-        run += c;
-      }
-    }
+    for (int i = tid; i < n_front; i += BS) map_put(sm, m1_sa, g1, cap1, (uint32_t)__ldcg(&Fin[i].x), i);
     __syncthreads();
-    for (int r = tid; r < n_surv; r += BS) {
-      const uint32_t q = (uint32_t)__ldcg(&tmp[r].x);
-      const int pos = atom_add_s(cnt_sa + 4u * (uint32_t)(((unsigned long long)q * kSortBuckets) / nq), 1);
-      if (on_chip) {
-        sts32(pairs_sa + 8u * pos, (int)q);
-        sts32(pairs_sa + 8u * pos + 4, r);
-      } else {
-        sort2[pos] = make_int2((int)q, r);
-      }
-    }
-    __syncthreads();
-    // insertion sort inside each bucket (the counters now hold bucket ends)
-    for (int bk = tid; bk < kSortBuckets; bk += BS) {
-      const int end = lds32(cnt_sa + 4u * bk);
-      const int beg = bk ? lds32(cnt_sa + 4u * (bk - 1)) : 0;
-      for (int x = beg + 1; x < end; x++) {
-        const int2 e = on_chip ? make_int2(lds32(pairs_sa + 8u * x), lds32(pairs_sa + 8u * x + 4)) : sort2[x];
-        int y = x - 1;
-        while (y >= beg) {
-          const int2 f = on_chip ? make_int2(lds32(pairs_sa + 8u * y), lds32(pairs_sa + 8u * y + 4)) : sort2[y];
-          if ((uint32_t)f.x <= (uint32_t)e.x) break;
-          if (on_chip) {
-            sts32(pairs_sa + 8u * (y + 1), f.x);
-            sts32(pairs_sa + 8u * (y + 1) + 4, f.y);
-          } else {
-            sort2[y + 1] = f;
-          }
-          y--;
-        }
-        if (on_chip) {
-          sts32(pairs_sa + 8u * (y + 1), e.x);
-          sts32(pairs_sa + 8u * (y + 1) + 4, e.y);
-        } else {
-          sort2[y + 1] = e;
-        }
-      }
-    }
-    __syncthreads();
-    // write the sorted frontier and the records; an epsilon winner finds its source's position
-    // by binary search over the sorted states
+    // pass 2: place survivors in cost-bucket order, state records, emitting back-pointers
     int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
     long long epsd = 0;
-    for (int pos = tid; pos < n_surv; pos += BS) {
-      const int r = on_chip ? lds32(pairs_sa + 8u * pos + 4) : sort2[pos].y;
+    for (int r = tid; r < n_surv; r += BS) {
       const int4 t = __ldcg(tmp + r);
+      const int pos = atom_add_s(saddr(&S.bucket_base[t.w & 0xFFFF]), 1);
       const int4 si = __ldg(p.state_info + t.x);
       Fout[pos] = make_int4(t.x, t.y, si.x, si.y - si.x);
       epsd += si.z - si.y;
-      int32_t arc = t.z, prev = t.w;
-      if (t.z != -1 && (t.z & 0x80000000)) {    // epsilon winner: prev = source's record
-        arc = t.z & 0x7FFFFFFF;
-        int lo = 0, hi = n_surv - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          const int sm = on_chip ? lds32(pairs_sa + 8u * mid) : sort2[mid].x;
-          if ((uint32_t)sm < (uint32_t)prev) lo = mid + 1; else hi = mid;
+      if (t.w & 0x80000000) map_put(sm, m2_sa, g2, cap2, (uint32_t)t.x, pos);
+      int32_t arc = t.z, prev = -1;
+      if (arc >= 0) {
+        const int4 a = __ldg(p.arcs + arc);
+        const uint32_t src = (uint32_t)a.w & 0x7FFFFFFFu;
+        if (a.z >= 0) {   // emitting winner: source token in the previous layer
+          const int ti = map_get(sm, m1_sa, g1, cap1, src);
+          prev = ti >= 0 ? prev_base + ti : -3;
+        } else {          // epsilon winner: resolved in pass 3
+          prev = (int32_t)(src | 0x80000000u);
+          const int fi = atomicAdd(&S.n_fix, 1);
+          epsfix[fi] = pos;
         }
-        prev = rb + lo;
+      } else if (arc == -2) {
+        prev = -3;        // inconsistent winner word (must not happen)
       }
+      if (prev == -3) S.status = WFST_ERR_STATE;
       rec[rb + pos] = make_int2(arc, prev);
       if (rec_cost) rec_cost[rb + pos] = __int_as_float(t.y);
     }
-    const long long eps_deg = block_sum64<BS>(epsd, S.warp_tmp64);
+    const long long eps_deg = block_sum64<BS>(epsd, S.warp_tmp64);   // barriers
     if (tid == 0) S.eps_deg = eps_deg;
+    // pass 3: epsilon back-pointers -> record of the source survivor in this layer
+    const int n_fix = S.n_fix;
+    for (int k = tid; k < n_fix; k += BS) {
+      const int pos = epsfix[k];
+      int2 e = rec[rb + pos];
+      const int si = map_get(sm, m2_sa, g2, cap2, (uint32_t)e.y & 0x7FFFFFFFu);
+      if (si < 0) S.status = WFST_ERR_STATE;
+      e.y = rb + si;
+      rec[rb + pos] = e;
+    }
+    __syncthreads();
     // give the table memory back (empty slots)
-    const int used = (int)(((size_t)kSortBuckets * 4 + (on_chip ? (size_t)n_surv * 8 : 0) + 7) / 8);
-    for (int i = tid; i < used; i += BS) sts64(tab_sa + 8u * i, kEmpty);
+    if (sm)
+      for (uint32_t i = tid; i < cap1 + cap2; i += BS) sts64(tab_sa + 8u * i, kEmpty);
     __syncthreads();
   }
 
@@ -956,9 +940,6 @@ struct Frame {
       const float half = isinf(p.beam) ? 32.0f : 0.5f * p.beam;
       S.ref = S.L.front_best - half;
       S.inv_w = (float)kNB / (4.0f * half);
-      // token << off_bits | offset orders like the arc id when tokens are sorted by state
-      const int nf = max(S.L.n_front, 1);
-      S.off_bits = __clz(nf);   // 32 - bits(nf)
     }
     __syncthreads();
   }
@@ -966,10 +947,7 @@ struct Frame {
   __device__ void clear_all() {
     for (int i = threadIdx.x; i < p.C; i += BS) sts64(tab_sa + 8u * i, kEmpty);
     for (int i = threadIdx.x; i < p.C_ovf; i += BS) ovf[i] = kEmpty;
-    for (int i = threadIdx.x; i < p.FCAP; i += BS) {
-      win_e[i] = kEmpty;
-      win_eps[i] = kEmpty;
-    }
+    for (int i = threadIdx.x; i < p.FCAP; i += BS) win[i] = kEmpty;
     __syncthreads();
   }
 
@@ -1042,7 +1020,7 @@ struct Frame {
         slot = insert((uint32_t)p.start, ((u64)o << 32) | (uint32_t)p.start, claimed, logit, strict);
         const int4 si = __ldg(p.state_info + p.start);
         flag = si.z > si.y ? 1u : 0u;
-        if (slot >= 0) win_eps[slot] = ((u64)o << 32) | 0xFFFFFFFFull;   // the start token
+        if (slot >= 0) win[slot] = ((u64)o << 32) | 0xFFFFFFFFull;   // the start token (arc -1)
         else claimed = false;
       }
       add_claim(slot, claimed, flag, -1);
