@@ -173,37 +173,37 @@ __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q
   const uint32_t hi = (uint32_t)(key >> 32);
   claimed = logit = strict = false;
 #pragma unroll 1
-  for (int p = 0; p < kMaxProbeS; ++p) {
+  for (int p = 0; p < kMaxProbeS;) {
     const uint32_t ba = tab_sa + b * 32u;
-    u64 x[4];
-    lds64x2(ba, x[0], x[1]);
-    lds64x2(ba + 16, x[2], x[3]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if ((uint32_t)x[j] == q && x[j] != kEmpty) {
-        // the state half of a slot never changes: a 32-bit min on the cost half (+4 bytes,
-        // little-endian) is the 64-bit min and a native shared atomic
-        const uint32_t old = atom_min_s_u32(ba + 8 * j + 4, hi);
-        logit = hi <= old;
-        strict = hi < old;
+    u64 x0, x1, x2, x3;
+    lds64x2(ba, x0, x1);
+    lds64x2(ba + 16, x2, x3);
+    // bit j: slot j holds q / slot j is empty
+    const uint32_t mq = ((uint32_t)x0 == q) | (((uint32_t)x1 == q) << 1) | (((uint32_t)x2 == q) << 2) |
+                        (((uint32_t)x3 == q) << 3);
+    const uint32_t me = (x0 == kEmpty) | ((x1 == kEmpty) << 1) | ((x2 == kEmpty) << 2) | ((x3 == kEmpty) << 3);
+    int j;
+    if (mq) {
+      j = __ffs(mq) - 1;
+    } else if (me) {
+      j = __ffs(me) - 1;
+      const u64 old = atom_cas_s(ba + 8 * j, kEmpty, key);
+      if (old == kEmpty) {
+        claimed = logit = strict = true;
         return (int)(b * 4 + j);
       }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (x[j] == kEmpty) {
-        const u64 old = atom_cas_s(ba + 8 * j, kEmpty, key);
-        if (old == kEmpty) {
-          claimed = logit = strict = true;
-          return (int)(b * 4 + j);
-        }
-        if ((uint32_t)old == q) {
-          const uint32_t o2 = atom_min_s_u32(ba + 8 * j + 4, hi);
-          logit = hi <= o2;
-          strict = hi < o2;
-          return (int)(b * 4 + j);
-        }
-      }
-    b = (b + 1 == nb) ? 0 : b + 1;
+      if ((uint32_t)old != q) continue;   // lost the slot to another state: re-read this bucket
+    } else {
+      b = (b + 1 == nb) ? 0 : b + 1;
+      p++;
+      continue;
+    }
+    // the state half of a slot never changes: a 32-bit min on the cost half (+4 bytes,
+    // little-endian) is the 64-bit min and a native shared atomic
+    const uint32_t old = atom_min_s_u32(ba + 8 * j + 4, hi);
+    logit = hi <= old;
+    strict = hi < old;
+    return (int)(b * 4 + j);
   }
   return -1;
 }
@@ -275,9 +275,14 @@ __device__ __forceinline__ long long block_sum64(long long v, long long* s_tmp) 
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if (lane == 0) s_tmp[w] = v;
   __syncthreads();
-  long long t = 0;
+  if (w == 0) {
+    long long t = lane < BS / 32 ? s_tmp[lane] : 0;
 #pragma unroll
-  for (int i = 0; i < BS / 32; i++) t += s_tmp[i];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) s_tmp[32 - 1] = t;
+  }
+  __syncthreads();
+  const long long t = s_tmp[32 - 1];
   __syncthreads();
   return t;
 }
@@ -342,14 +347,25 @@ struct Frame {
     return s + p.C;
   }
 
-  // claim bookkeeping (warp-collective: every lane of the warp calls it)
-  __device__ __forceinline__ void add_claim(int slot, bool claimed, uint32_t eps_flag, int bin) {
-    const int ci = warp_append(claimed, saddr(&S.n_claim));
+  // claim bookkeeping (warp-collective: every lane of the warp calls it).  Returns true on
+  // the warp whose append crossed a multiple of 1024 claims at or beyond alpha: that warp
+  // refreshes the max-active bound.
+  __device__ __forceinline__ bool add_claim(int slot, bool claimed, uint32_t eps_flag, int bin) {
+    const int lane = threadIdx.x & 31;
+    const unsigned m = __ballot_sync(0xffffffffu, claimed);
+    if (m == 0) return false;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atom_add_s(saddr(&S.n_claim), __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
     if (claimed) {
+      const int ci = base + __popc(m & ((1u << lane) - 1u));
       if (ci < p.FCAP) claim[ci] = (uint32_t)slot | (eps_flag << 31);
       else S.status = WFST_ERR_CAPACITY;
       if (bin >= 0) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
     }
+    const int end = base + __popc(m);
+    return p.alpha > 0 && end >= p.alpha && (end >> 10) != (base >> 10);
   }
 
   // theta = smallest b such that >= alpha distinct states have first-insert bin < b (warp-collective)
@@ -399,7 +415,7 @@ struct Frame {
         if (slot < 0) claimed = false;
       }
     }
-    add_claim(slot, claimed, flag, bin);
+    if (add_claim(slot, claimed, flag, bin)) update_theta();
   }
 
   // stage one round of candidates (warp-collective); flushes when the buffer fills
@@ -435,9 +451,8 @@ struct Frame {
     const int n_f = S.L.n_front;
     const int4* Fin = F0 + (size_t)S.L.cur * p.FCAP;
     const float ref = S.ref, inv_w = S.inv_w, beam = p.beam;
-    const uint32_t best_sa = saddr(&S.best_ord), theta_sa = saddr(&S.theta), nclaim_sa = saddr(&S.n_claim);
+    const uint32_t best_sa = saddr(&S.best_ord), theta_sa = saddr(&S.theta);
     long long arcs_total = 0;
-    int last_theta = 0;
     int staged = 0;   // warp-uniform
     for (int tb = warp * 32; tb < n_f; tb += NW * 32) {
       const int i = tb + lane;
@@ -504,13 +519,6 @@ struct Frame {
           const int4 entry = make_int4(arc[u].x, (int)ord_of(c), a[u], bin | (int)(arc[u].w & 0x80000000));
           stage(pass, entry, staged, beam, best_sa, theta_sa);
         }
-        if (p.alpha > 0) {
-          const int nc = __shfl_sync(0xffffffffu, lds32(nclaim_sa), 0);
-          if (nc >= p.alpha && nc - last_theta >= 512) {
-            update_theta();
-            last_theta = nc;
-          }
-        }
       }
     }
     __syncwarp();
@@ -547,13 +555,6 @@ struct Frame {
           const int j = j0 + u * BS + tid;
           const int4 entry = make_int4(arc[u].x, (int)ord_of(c), f.z + j, bin | (int)(arc[u].w & 0x80000000));
           stage(pass, entry, staged, beam, best_sa, theta_sa);
-        }
-        if (p.alpha > 0) {
-          const int nc = __shfl_sync(0xffffffffu, lds32(nclaim_sa), 0);
-          if (nc >= p.alpha && nc - last_theta >= 512) {
-            update_theta();
-            last_theta = nc;
-          }
         }
       }
     }
@@ -857,8 +858,10 @@ struct Frame {
       return;
     }
     // maps in the drained table: M1 (prev tokens) then M2 (this layer's epsilon-capable states)
-    const uint32_t cap1 = (uint32_t)max(n_front + (n_front >> 2) + 32, 64);
+    // load <= 1/2 on chip when there is room (linear probing); global maps otherwise
     const uint32_t cap2 = (uint32_t)max((int)n_eps_tot * 2 + 32, 64);
+    uint32_t cap1 = (uint32_t)max(2 * n_front + 32, 64);
+    if (cap1 + cap2 > (uint32_t)p.C) cap1 = max((uint32_t)p.C - cap2, (uint32_t)(n_front + (n_front >> 2) + 32));
     const bool sm = (size_t)(cap1 + cap2) <= (size_t)p.C;
     const uint32_t m1_sa = tab_sa, m2_sa = tab_sa + 8u * cap1;
     u64* g1 = gmap;
