@@ -879,31 +879,54 @@ struct Frame {
     // pass 2: place survivors in cost-bucket order, state records, emitting back-pointers
     int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
     long long epsd = 0;
-    for (int r = tid; r < n_surv; r += BS) {
-      const int4 t = __ldcg(tmp + r);
-      const int pos = atom_add_s(saddr(&S.bucket_base[t.w & 0xFFFF]), 1);
-      const int4 si = __ldg(p.state_info + t.x);
-      Fout[pos] = make_int4(t.x, t.y, si.x, si.y - si.x);
-      epsd += si.z - si.y;
-      if (t.w & 0x80000000) map_put(sm, m2_sa, g2, cap2, (uint32_t)t.x, pos);
-      int32_t arc = t.z, prev = -1;
-      if (arc >= 0) {
-        const int4 a = __ldg(p.arcs + arc);
-        const uint32_t src = (uint32_t)a.w & 0x7FFFFFFFu;
-        if (a.z >= 0) {   // emitting winner: source token in the previous layer
-          const int ti = map_get(sm, m1_sa, g1, cap1, src);
-          prev = ti >= 0 ? prev_base + ti : -3;
-        } else {          // epsilon winner: resolved in pass 3
-          prev = (int32_t)(src | 0x80000000u);
-          const int fi = atomicAdd(&S.n_fix, 1);
-          epsfix[fi] = pos;
-        }
-      } else if (arc == -2) {
-        prev = -3;        // inconsistent winner word (must not happen)
+    for (int r0 = 0; r0 < n_surv; r0 += BS * U) {   // warp-uniform trip count
+      int4 t[U];
+      int pos[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int r = r0 + u * BS + tid;
+        t[u] = r < n_surv ? __ldcg(tmp + r) : make_int4(-1, 0, -1, kNBuck);
       }
-      if (prev == -3) S.status = WFST_ERR_STATE;
-      rec[rb + pos] = make_int2(arc, prev);
-      if (rec_cost) rec_cost[rb + pos] = __int_as_float(t.y);
+#pragma unroll
+      for (int u = 0; u < U; u++) {   // warp-aggregated bucket cursors
+        const int bk = t[u].w & 0xFFFF;
+        const unsigned grp = __match_any_sync(0xffffffffu, bk);
+        const int leader = __ffs(grp) - 1;
+        int base = 0;
+        if (bk < kNBuck && (threadIdx.x & 31) == leader) base = atom_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        pos[u] = base + __popc(grp & ((1u << (threadIdx.x & 31)) - 1u));
+      }
+      int4 si[U], ar[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        si[u] = t[u].x >= 0 ? __ldg(p.state_info + t[u].x) : make_int4(0, 0, 0, 0);
+        ar[u] = t[u].z >= 0 ? __ldg(p.arcs + t[u].z) : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        if (t[u].x < 0) continue;
+        Fout[pos[u]] = make_int4(t[u].x, t[u].y, si[u].x, si[u].y - si[u].x);
+        epsd += si[u].z - si[u].y;
+        if (t[u].w & 0x80000000) map_put(sm, m2_sa, g2, cap2, (uint32_t)t[u].x, pos[u]);
+        int32_t arc = t[u].z, prev = -1;
+        if (arc >= 0) {
+          const uint32_t src = (uint32_t)ar[u].w & 0x7FFFFFFFu;
+          if (ar[u].z >= 0) {   // emitting winner: source token in the previous layer
+            const int ti = map_get(sm, m1_sa, g1, cap1, src);
+            prev = ti >= 0 ? prev_base + ti : -3;
+          } else {              // epsilon winner: resolved in pass 3
+            prev = (int32_t)(src | 0x80000000u);
+            const int fi = atomicAdd(&S.n_fix, 1);
+            epsfix[fi] = pos[u];
+          }
+        } else if (arc == -2) {
+          prev = -3;            // inconsistent winner word (must not happen)
+        }
+        if (prev == -3) S.status = WFST_ERR_STATE;
+        rec[rb + pos[u]] = make_int2(arc, prev);
+        if (rec_cost) rec_cost[rb + pos[u]] = __int_as_float(t[u].y);
+      }
     }
     const long long eps_deg = block_sum64<BS>(epsd, S.warp_tmp64);   // barriers
     if (tid == 0) S.eps_deg = eps_deg;
