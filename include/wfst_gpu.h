@@ -99,8 +99,8 @@ typedef struct {
   int64_t alpha_frames;      /* frames where max-active tightened the cutoff                      */
   int64_t device_bytes;      /* decoder device allocation                                         */
   int64_t records_used_max;  /* max traceback records used by any stream                          */
-  int64_t phase_cycles[6];   /* SM cycles summed over lanes: expand, cutoff, epsilon, (unused),
-                                contraction, frame overhead (instrumentation)                     */
+  int64_t phase_cycles[6];   /* SM cycles summed over lanes: expand, cutoff, epsilon, drain+maps,
+                                rest of contraction, frame overhead (instrumentation)            */
 } wfst_stats_t;
 
 /* ---- graph (row a0 of SURVEY §8) ------------------------------------------------ */

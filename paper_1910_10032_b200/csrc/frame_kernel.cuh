@@ -75,8 +75,9 @@ struct SmemCtl {
   int32_t item, lane, b, status;
   uint32_t best_ord;
   int32_t theta;
-  int32_t n_claim, n_claim_emit, n_ovf, n_surv, n_in, n_wl, n_wl_next, n_big, n_fix;
+  int32_t n_claim, n_claim_emit, n_ovf, n_surv, n_in, n_wl, n_wl_next, n_big, n_fix, next_group;
   int32_t bucket_base[kNBuck];
+  long long t_mark;
   float beam_cut, kalpha, ref, inv_w, min_surv;
   int32_t use_alpha;
   int32_t radix_prefix, radix_k;
@@ -447,14 +448,21 @@ struct Frame {
   // RED.MIN of (cost, canonical arc id) into the slot's winner word: the min is exactly the
   // (cost, arc) tie-break of R9.
   __device__ void expand(const float* __restrict__ row) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int n_f = S.L.n_front;
     const int4* Fin = F0 + (size_t)S.L.cur * p.FCAP;
     const float ref = S.ref, inv_w = S.inv_w, beam = p.beam;
     const uint32_t best_sa = saddr(&S.best_ord), theta_sa = saddr(&S.theta);
     long long arcs_total = 0;
     int staged = 0;   // warp-uniform
-    for (int tb = warp * 32; tb < n_f; tb += NW * 32) {
+    // token groups of 32 are handed out dynamically (warps whose groups hold long arc lists
+    // do not hold the CTA back at the barrier)
+    const uint32_t next_sa = saddr(&S.next_group);
+    while (true) {
+      int tb = 0;
+      if (lane == 0) tb = atom_add_s(next_sa, 32);
+      tb = __shfl_sync(0xffffffffu, tb, 0);
+      if (tb >= n_f) break;
       const int i = tb + lane;
       int deg = 0, eb = 0;
       float cost = 0.f;
@@ -786,6 +794,7 @@ struct Frame {
       S.n_surv = 0;
       S.n_fix = 0;
       S.min_surv = INFINITY;
+      S.t_mark = clock64();
     }
     __syncthreads();
     float mn = INFINITY;
@@ -820,14 +829,18 @@ struct Frame {
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int r = warp_append(k[u], saddr(&S.n_surv));
+        const float c = key_cost(v[u]);
+        const int bk = k[u] ? (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1))
+                            : kNBuck;
+        {   // warp-aggregated bucket count
+          const unsigned grp = __match_any_sync(0xffffffffu, bk);
+          if (bk < kNBuck && (tid & 31) == __ffs(grp) - 1) red_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
+        }
         if (!k[u]) continue;
         if (r >= p.FCAP) {
           S.status = WFST_ERR_CAPACITY;
           continue;
         }
-        const float c = key_cost(v[u]);
-        const int bk = (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1));
-        red_add_s(saddr(&S.bucket_base[bk]), 1);
         // the winner word's cost must be the slot's final cost (every improving insert RED's)
         const int32_t arc = (uint32_t)(w[u] >> 32) == (uint32_t)(v[u] >> 32) ? (int32_t)(uint32_t)w[u] : -2;
         tmp[r] = make_int4((int)(uint32_t)v[u], __float_as_int(c), arc, (int)(cl[u] & 0x80000000u) | bk);
@@ -874,8 +887,23 @@ struct Frame {
     if (!sm)
       for (uint32_t i = tid; i < cap1 + cap2; i += BS) gmap[i] = kEmpty;
     __syncthreads();
-    for (int i = tid; i < n_front; i += BS) map_put(sm, m1_sa, g1, cap1, (uint32_t)__ldcg(&Fin[i].x), i);
+    for (int i0 = 0; i0 < n_front; i0 += BS * U) {
+      uint32_t q[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int i = i0 + u * BS + tid;
+        q[u] = i < n_front ? (uint32_t)__ldcg(&Fin[i].x) : 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (q[u] != 0xFFFFFFFFu) map_put(sm, m1_sa, g1, cap1, q[u], i0 + u * BS + tid);
+    }
     __syncthreads();
+    if (tid == 0) {   // phase split: drain done, maps built
+      const long long t1 = clock64();
+      S.L.phase[3] += (u64)(t1 - S.t_mark);
+      S.t_mark = t1;
+    }
     // pass 2: place survivors in cost-bucket order, state records, emitting back-pointers
     int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
     long long epsd = 0;
@@ -956,6 +984,7 @@ struct Frame {
       S.n_claim = 0;
       S.n_ovf = 0;
       S.n_big = 0;
+      S.next_group = 0;
       S.n_wl = 0;
       S.use_alpha = 0;
       S.kalpha = INFINITY;
@@ -1068,6 +1097,14 @@ struct Frame {
       t0 = t1;
     }
   }
+  // contraction: phase[3] = drain + maps (measured inside), phase[4] = the rest
+  __device__ __forceinline__ void tick_contract(long long& t0) {
+    if (threadIdx.x == 0) {
+      const long long t1 = clock64();
+      S.L.phase[4] += (u64)(t1 - S.t_mark);
+      t0 = t1;
+    }
+  }
 
   __device__ void run_frame(int t) {
     const int tid = threadIdx.x;
@@ -1094,7 +1131,7 @@ struct Frame {
     eps_closure();
     tick(t0, 2);
     contract();
-    tick(t0, 4);
+    tick_contract(t0);
     finish_frame(t, true);
     tick(t0, 5);
   }
