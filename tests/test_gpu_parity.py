@@ -268,3 +268,21 @@ def test_kernel_variants_parity(W, torch, oracle_mod, threads, ctas):
     assert res["rc"] == 0
     for b in range(12):
         _compare(og, ll, 15.0, 3000, res, b)
+
+
+def test_tie_heavy_dyadic(W, torch, oracle_mod):
+    """Integer-valued weights and log-likelihoods make exact fp32 cost ties common: the GPU's
+    winner words must reproduce the oracle's (cost, canonical arc id) tie-break (R9) exactly,
+    including ties between candidates from different source tokens and between emitting and
+    epsilon arcs."""
+    g = I.hclg_graph(20_000, 3.0, 40, seed=17)
+    g.weight = np.round(g.weight).astype(np.float32)
+    g.final = np.where(np.isfinite(g.final), np.round(g.final), np.inf).astype(np.float32)
+    B, T, P = 8, 40, 40
+    rng = np.random.default_rng(5)
+    ll = rng.integers(-3, 1, (T, B, P)).astype(np.float32)
+    og = oracle_mod.OracleGraph(g)
+    for beam, alpha in ((6.0, 300), (4.0, 50), (INF, 2000)):
+        D, res = _gpu_run(W, torch, g, ll, beam, alpha)
+        for b in range(B):
+            _compare(og, ll, beam, alpha, res, b)
