@@ -262,10 +262,6 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   int Co = d->o.overflow_slots > 0 ? d->o.overflow_slots : std::max(std::max(C, 32768), 4 * d->alpha);
   d->C_ovf = std::max(64, (Co + 3) / 4 * 4);
   d->FCAP = d->C + d->C_ovf;
-  if (d->FCAP > (1 << 20)) {   // token indices ride in 20 bits of the staging entry
-    delete d;
-    return fail(WFST_ERR_INVALID_ARG, "table_slots + overflow_slots must be <= 2^20");
-  }
   d->TMAX = d->o.max_frames > 0 ? d->o.max_frames : 2048;
   int64_t per_frame = d->alpha > 0 ? std::min<int64_t>((int64_t)d->alpha * 5 / 4 + 1024, d->FCAP) : d->FCAP;
   if (d->o.records_per_stream > 0) {
@@ -304,7 +300,6 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   size_t i_front = add(L * 2 * FC * sizeof(int4));
   size_t i_claim = add(L * FC * 4);
   size_t i_win = add(L * FC * 8);
-  size_t i_win2 = add(L * FC * 8);
   size_t i_tmp = add(L * FC * sizeof(int4));
   size_t i_gmap = add(L * 2 * FC * 8);
   size_t i_fix = add(L * FC * 4);
@@ -348,7 +343,6 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.front = (int4*)(base + parts[i_front].off);
   kp.claim = (uint32_t*)(base + parts[i_claim].off);
   kp.win = (u64*)(base + parts[i_win].off);
-  kp.win2 = (u64*)(base + parts[i_win2].off);
   kp.tmp = (int4*)(base + parts[i_tmp].off);
   kp.gmap = (u64*)(base + parts[i_gmap].off);
   kp.epsfix = (int32_t*)(base + parts[i_fix].off);
@@ -363,7 +357,6 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.lane_round = d->d_round;
   e = cudaMemset(base + parts[i_ovf].off, 0xFF, parts[i_ovf].bytes);
   if (e == cudaSuccess) e = cudaMemset(base + parts[i_win].off, 0xFF, parts[i_win].bytes);
-  if (e == cudaSuccess) e = cudaMemset(base + parts[i_win2].off, 0xFF, parts[i_win2].bytes);
   if (e == cudaSuccess) e = cudaMemset(d->d_lanes, 0, sizeof(LaneState) * L);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {

@@ -59,7 +59,6 @@ struct KParams {
   int4* front;        // [lane][2][FCAP]  {state, cost bits, e_begin, n_emit}, cost-bucketed
   uint32_t* claim;    // [lane][FCAP]     slot | has_eps << 31, one per distinct state
   u64* win;           // [lane][FCAP]     per slot: min (ord(cost) << 32 | canonical arc id)
-  u64* win2;          // [lane][FCAP]     per slot: min (ord(cost) << 32 | source token) (emitting)
   int4* tmp;          // [lane][FCAP]     contraction scratch {state, cost, arc, has_eps | bucket}
   u64* gmap;          // [lane][2*FCAP]   state -> index maps when they do not fit on chip
   int32_t* epsfix;    // [lane][FCAP]     positions of survivors won by an epsilon arc
@@ -304,7 +303,6 @@ struct Frame {
   int4* F0;           // frontier buffer 0; buffer 1 follows at +FCAP
   uint32_t* claim;
   u64* win;
-  u64* win2;
   int4* tmp;
   u64* gmap;
   int32_t* epsfix;
@@ -321,7 +319,6 @@ struct Frame {
     F0 = p.front + L * 2 * FC;
     claim = p.claim + L * FC;
     win = p.win + L * FC;
-    win2 = p.win2 + L * FC;
     tmp = p.tmp + L * FC;
     gmap = p.gmap + L * 2 * FC;
     epsfix = p.epsfix + L * FC;
@@ -404,10 +401,10 @@ struct Frame {
     int slot = -1, bin = -1;
     uint32_t flag = 0;
     if (lane < n) {
-      const int4 e = lds128(stage_sa + 16u * lane);   // {q, ord, arc id, bin | eps << 10 | token << 11}
+      const int4 e = lds128(stage_sa + 16u * lane);   // {q, ord, arc id, bin | eps flag << 31}
       const uint32_t o = (uint32_t)e.y;
-      bin = e.w & 1023;
-      flag = ((uint32_t)e.w >> 10) & 1u;
+      bin = e.w & 0x7FFFFFFF;
+      flag = (uint32_t)e.w >> 31;
       // re-check against the bounds as they are now (both only tighten)
       const uint32_t bo = (uint32_t)lds32(best_sa);
       const bool ok = (bo == 0xFFFFFFFFu || float_of_ord(o) < __fadd_rn(float_of_ord(bo), beam)) &&
@@ -415,10 +412,7 @@ struct Frame {
       if (ok) {
         if (o < bo) red_min_s32(best_sa, o);
         slot = insert((uint32_t)e.x, ((u64)o << 32) | (uint32_t)e.x, claimed, logit, strict);
-        if (slot >= 0 && logit) {
-          red_min_g64(win + slot, ((u64)o << 32) | (uint32_t)e.z);
-          red_min_g64(win2 + slot, ((u64)o << 32) | ((uint32_t)e.w >> 11));
-        }
+        if (slot >= 0 && logit) red_min_g64(win + slot, ((u64)o << 32) | (uint32_t)e.z);
         if (slot < 0) claimed = false;
       }
     }
@@ -530,8 +524,7 @@ struct Frame {
           const float c = __fadd_rn(__fsub_rn(__fadd_rn(co, __int_as_float(arc[u].y)), L[u]), 0.0f);
           const int bin = bin_of(c, ref, inv_w);
           const bool pass = v[u] && c < bound && bin < th;
-          const int4 entry = make_int4(arc[u].x, (int)ord_of(c), a[u],
-                                       bin | (int)(((uint32_t)arc[u].w >> 31) << 10) | ((tb + own[u]) << 11));
+          const int4 entry = make_int4(arc[u].x, (int)ord_of(c), a[u], bin | (int)(arc[u].w & 0x80000000));
           stage(pass, entry, staged, beam, best_sa, theta_sa);
         }
       }
@@ -568,8 +561,7 @@ struct Frame {
           const int bin = bin_of(c, ref, inv_w);
           const bool pass = v[u] && c < bound && bin < th;
           const int j = j0 + u * BS + tid;
-          const int4 entry = make_int4(arc[u].x, (int)ord_of(c), f.z + j,
-                                       bin | (int)(((uint32_t)arc[u].w >> 31) << 10) | (i << 11));
+          const int4 entry = make_int4(arc[u].x, (int)ord_of(c), f.z + j, bin | (int)(arc[u].w & 0x80000000));
           stage(pass, entry, staged, beam, best_sa, theta_sa);
         }
       }
@@ -781,14 +773,12 @@ struct Frame {
   }
 
   // ---- rows a4 + a6: contraction into the next frontier (cost-bucketed) + records ----
-  // Back-pointers: the winner word gives the arc; for an emitting arc the second winner word
-  // gives the source token of the previous layer (checked: that token's state must be the
-  // arc's source; an exact cost tie between different tokens can make the two words name
-  // different candidates, and such a survivor finds its token by a warp-parallel search).
-  // An epsilon winner's source is a survivor of this layer (map M2, on chip, over the
-  // survivors whose state has epsilon arcs).
+  // Back-pointers: an emitting winner's source is a token of the previous layer (map M1:
+  // state -> token, built here from that frontier); an epsilon winner's source is a survivor
+  // of this layer (map M2 over the survivors whose state has epsilon arcs).  Both maps live in
+  // the drained token table when they fit.
   __device__ void contract() {
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     const int n_claim = min(S.n_claim, p.FCAP);
     const int n_front = S.L.n_front;
     const int4* Fin = F0 + (size_t)S.L.cur * p.FCAP;
@@ -810,10 +800,10 @@ struct Frame {
     float mn = INFINITY;
     int n_eps_surv = 0;
     constexpr int U = 4;
-    // pass 1: drain the tables; survivors -> tmp {state, cost, arc, has_eps << 31 | token << 5 | bucket}
+    // pass 1: drain the tables; survivors -> tmp {state, cost, arc, has_eps << 31 | bucket}
     for (int i0 = 0; i0 < n_claim; i0 += BS * U) {
       uint32_t cl[U];
-      u64 v[U], w[U], w2[U];
+      u64 v[U], w[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int i = i0 + u * BS + tid;
@@ -822,10 +812,8 @@ struct Frame {
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int slot = (int)(cl[u] & 0x7FFFFFFFu);
-        const bool has = cl[u] != 0xFFFFFFFFu;
-        v[u] = has ? read_slot(slot) : kEmpty;
-        w[u] = has ? __ldcg(win + slot) : kEmpty;
-        w2[u] = has ? __ldcg(win2 + slot) : kEmpty;
+        v[u] = cl[u] != 0xFFFFFFFFu ? read_slot(slot) : kEmpty;
+        w[u] = cl[u] != 0xFFFFFFFFu ? __ldcg(win + slot) : kEmpty;
       }
       bool k[U];
 #pragma unroll
@@ -834,7 +822,6 @@ struct Frame {
           const int slot = (int)(cl[u] & 0x7FFFFFFFu);
           clear_slot(slot);
           win[slot] = kEmpty;
-          win2[slot] = kEmpty;
         }
         const float c = key_cost(v[u]);
         k[u] = cl[u] != 0xFFFFFFFFu && c < cut_b && c <= cut_a;
@@ -847,7 +834,7 @@ struct Frame {
                             : kNBuck;
         {   // warp-aggregated bucket count
           const unsigned grp = __match_any_sync(0xffffffffu, bk);
-          if (bk < kNBuck && lane == __ffs(grp) - 1) red_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
+          if (bk < kNBuck && (tid & 31) == __ffs(grp) - 1) red_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
         }
         if (!k[u]) continue;
         if (r >= p.FCAP) {
@@ -855,11 +842,8 @@ struct Frame {
           continue;
         }
         // the winner word's cost must be the slot's final cost (every improving insert RED's)
-        const uint32_t fo = (uint32_t)(v[u] >> 32);
-        const int32_t arc = (uint32_t)(w[u] >> 32) == fo ? (int32_t)(uint32_t)w[u] : -2;
-        const int tok = (uint32_t)(w2[u] >> 32) == fo ? (int)(uint32_t)w2[u] : 0x3FFFFFF;
-        tmp[r] = make_int4((int)(uint32_t)v[u], __float_as_int(c), arc,
-                           (int)(cl[u] & 0x80000000u) | ((tok & 0x3FFFFFF) << 5) | bk);
+        const int32_t arc = (uint32_t)(w[u] >> 32) == (uint32_t)(v[u] >> 32) ? (int32_t)(uint32_t)w[u] : -2;
+        tmp[r] = make_int4((int)(uint32_t)v[u], __float_as_int(c), arc, (int)(cl[u] & 0x80000000u) | bk);
         n_eps_surv += (cl[u] >> 31);
         mn = fminf(mn, c);
       }
@@ -878,9 +862,6 @@ struct Frame {
         S.bucket_base[b] = acc;
         acc += n;
       }
-      const long long t1 = clock64();   // phase split: drain done
-      S.L.phase[3] += (u64)(t1 - S.t_mark);
-      S.t_mark = t1;
     }
     const int n_surv = min(S.n_surv, p.FCAP);
     const int32_t rb = S.L.rec_used;
@@ -889,20 +870,41 @@ struct Frame {
       __syncthreads();
       return;
     }
-    // M2 in the drained table (global scratch when it does not fit)
+    // maps in the drained table: M1 (prev tokens) then M2 (this layer's epsilon-capable states)
+    // load <= 1/2 on chip when there is room (linear probing); global maps otherwise
     const uint32_t cap2 = (uint32_t)max((int)n_eps_tot * 2 + 32, 64);
-    const bool sm = cap2 <= (uint32_t)p.C;
-    const uint32_t m2_sa = tab_sa;
-    u64* g2 = gmap;
-    if (!sm && cap2 > 2u * (uint32_t)p.FCAP) {
+    uint32_t cap1 = (uint32_t)max(2 * n_front + 32, 64);
+    if (cap1 + cap2 > (uint32_t)p.C) cap1 = max((uint32_t)p.C - cap2, (uint32_t)(n_front + (n_front >> 2) + 32));
+    const bool sm = (size_t)(cap1 + cap2) <= (size_t)p.C;
+    const uint32_t m1_sa = tab_sa, m2_sa = tab_sa + 8u * cap1;
+    u64* g1 = gmap;
+    u64* g2 = gmap + cap1;
+    if (!sm && cap1 + cap2 > 2u * (uint32_t)p.FCAP) {
       if (tid == 0) S.status = WFST_ERR_CAPACITY;
       __syncthreads();
       return;
     }
     if (!sm)
-      for (uint32_t i = tid; i < cap2; i += BS) gmap[i] = kEmpty;
+      for (uint32_t i = tid; i < cap1 + cap2; i += BS) gmap[i] = kEmpty;
     __syncthreads();
-    // pass 2: place survivors in cost-bucket order, state records, back-pointers
+    for (int i0 = 0; i0 < n_front; i0 += BS * U) {
+      uint32_t q[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int i = i0 + u * BS + tid;
+        q[u] = i < n_front ? (uint32_t)__ldcg(&Fin[i].x) : 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (q[u] != 0xFFFFFFFFu) map_put(sm, m1_sa, g1, cap1, q[u], i0 + u * BS + tid);
+    }
+    __syncthreads();
+    if (tid == 0) {   // phase split: drain done, maps built
+      const long long t1 = clock64();
+      S.L.phase[3] += (u64)(t1 - S.t_mark);
+      S.t_mark = t1;
+    }
+    // pass 2: place survivors in cost-bucket order, state records, emitting back-pointers
     int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
     long long epsd = 0;
     for (int r0 = 0; r0 < n_surv; r0 += BS * U) {   // warp-uniform trip count
@@ -915,22 +917,19 @@ struct Frame {
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {   // warp-aggregated bucket cursors
-        const int bk = t[u].w & 31;
+        const int bk = t[u].w & 0xFFFF;
         const unsigned grp = __match_any_sync(0xffffffffu, bk);
         const int leader = __ffs(grp) - 1;
         int base = 0;
-        if (bk < kNBuck && lane == leader) base = atom_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
+        if (bk < kNBuck && (threadIdx.x & 31) == leader) base = atom_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
         base = __shfl_sync(0xffffffffu, base, leader);
-        pos[u] = base + __popc(grp & ((1u << lane) - 1u));
+        pos[u] = base + __popc(grp & ((1u << (threadIdx.x & 31)) - 1u));
       }
       int4 si[U], ar[U];
-      int tstate[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        const int tok = (t[u].w >> 5) & 0x3FFFFFF;
         si[u] = t[u].x >= 0 ? __ldg(p.state_info + t[u].x) : make_int4(0, 0, 0, 0);
         ar[u] = t[u].z >= 0 ? __ldg(p.arcs + t[u].z) : make_int4(0, 0, 0, 0);
-        tstate[u] = (t[u].x >= 0 && tok < n_front) ? __ldcg(&Fin[tok].x) : -1;
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {
@@ -941,13 +940,9 @@ struct Frame {
         int32_t arc = t[u].z, prev = -1;
         if (arc >= 0) {
           const uint32_t src = (uint32_t)ar[u].w & 0x7FFFFFFFu;
-          const int tok = (t[u].w >> 5) & 0x3FFFFFF;
-          if (ar[u].z >= 0) {   // emitting winner: source token of the previous layer
-            prev = (tstate[u] == (int)src) ? prev_base + tok : (int32_t)(src | 0x80000000u);
-            if (tstate[u] != (int)src) {   // tie between tokens: search below
-              const int fi = atomicAdd(&S.n_fix, 1);
-              epsfix[fi] = pos[u] | (int)0x80000000;
-            }
+          if (ar[u].z >= 0) {   // emitting winner: source token in the previous layer
+            const int ti = map_get(sm, m1_sa, g1, cap1, src);
+            prev = ti >= 0 ? prev_base + ti : -3;
           } else {              // epsilon winner: resolved in pass 3
             prev = (int32_t)(src | 0x80000000u);
             const int fi = atomicAdd(&S.n_fix, 1);
@@ -955,46 +950,28 @@ struct Frame {
           }
         } else if (arc == -2) {
           prev = -3;            // inconsistent winner word (must not happen)
-          S.status = WFST_ERR_STATE;
         }
+        if (prev == -3) S.status = WFST_ERR_STATE;
         rec[rb + pos[u]] = make_int2(arc, prev);
         if (rec_cost) rec_cost[rb + pos[u]] = __int_as_float(t[u].y);
       }
     }
     const long long eps_deg = block_sum64<BS>(epsd, S.warp_tmp64);   // barriers
     if (tid == 0) S.eps_deg = eps_deg;
-    // pass 3: epsilon back-pointers (source survivor of this layer, via M2) and emitting
-    // back-pointers whose two winner words disagreed (source token found by a warp scan)
+    // pass 3: epsilon back-pointers -> record of the source survivor in this layer
     const int n_fix = S.n_fix;
-    const int warp = tid >> 5;
-    for (int k0 = warp; k0 < n_fix; k0 += NW) {
-      const int fx = epsfix[k0];
-      const int pos = fx & 0x7FFFFFFF;
+    for (int k = tid; k < n_fix; k += BS) {
+      const int pos = epsfix[k];
       int2 e = rec[rb + pos];
-      const uint32_t src = (uint32_t)e.y & 0x7FFFFFFFu;
-      int found = -1;
-      if (fx >= 0) {          // epsilon
-        if (lane == 0) found = map_get(sm, m2_sa, g2, cap2, src);
-        found = __shfl_sync(0xffffffffu, found, 0);
-        if (found >= 0) found += rb;
-      } else {                // emitting tie: scan the previous frontier for the source state
-        for (int i0 = 0; i0 < n_front && found < 0; i0 += 32) {
-          const int i = i0 + lane;
-          const bool hit = i < n_front && (uint32_t)__ldcg(&Fin[i].x) == src;
-          const unsigned m = __ballot_sync(0xffffffffu, hit);
-          if (m) found = prev_base + i0 + __ffs(m) - 1;
-        }
-      }
-      if (lane == 0) {
-        if (found < 0) S.status = WFST_ERR_STATE;
-        e.y = found;
-        rec[rb + pos] = e;
-      }
+      const int si = map_get(sm, m2_sa, g2, cap2, (uint32_t)e.y & 0x7FFFFFFFu);
+      if (si < 0) S.status = WFST_ERR_STATE;
+      e.y = rb + si;
+      rec[rb + pos] = e;
     }
     __syncthreads();
     // give the table memory back (empty slots)
     if (sm)
-      for (uint32_t i = tid; i < cap2; i += BS) sts64(tab_sa + 8u * i, kEmpty);
+      for (uint32_t i = tid; i < cap1 + cap2; i += BS) sts64(tab_sa + 8u * i, kEmpty);
     __syncthreads();
   }
 
@@ -1025,10 +1002,7 @@ struct Frame {
   __device__ void clear_all() {
     for (int i = threadIdx.x; i < p.C; i += BS) sts64(tab_sa + 8u * i, kEmpty);
     for (int i = threadIdx.x; i < p.C_ovf; i += BS) ovf[i] = kEmpty;
-    for (int i = threadIdx.x; i < p.FCAP; i += BS) {
-      win[i] = kEmpty;
-      win2[i] = kEmpty;
-    }
+    for (int i = threadIdx.x; i < p.FCAP; i += BS) win[i] = kEmpty;
     __syncthreads();
   }
 
