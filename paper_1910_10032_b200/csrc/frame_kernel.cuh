@@ -810,19 +810,15 @@ struct Frame {
         cl[u] = i < n_claim ? __ldcg(claim + i) : 0xFFFFFFFFu;
       }
 #pragma unroll
-      for (int u = 0; u < U; u++) {
+      for (int u = 0; u < U; u++) {   // winner word read and reset in one L2 transaction
         const int slot = (int)(cl[u] & 0x7FFFFFFFu);
         v[u] = cl[u] != 0xFFFFFFFFu ? read_slot(slot) : kEmpty;
-        w[u] = cl[u] != 0xFFFFFFFFu ? __ldcg(win + slot) : kEmpty;
+        w[u] = cl[u] != 0xFFFFFFFFu ? atomicExch(win + slot, kEmpty) : kEmpty;
       }
       bool k[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        if (cl[u] != 0xFFFFFFFFu) {
-          const int slot = (int)(cl[u] & 0x7FFFFFFFu);
-          clear_slot(slot);
-          win[slot] = kEmpty;
-        }
+        if (cl[u] != 0xFFFFFFFFu) clear_slot((int)(cl[u] & 0x7FFFFFFFu));
         const float c = key_cost(v[u]);
         k[u] = cl[u] != 0xFFFFFFFFu && c < cut_b && c <= cut_a;
       }
