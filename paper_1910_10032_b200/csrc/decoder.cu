@@ -147,7 +147,7 @@ struct wfst_decoder_s {
   float beam = 15.f;
   int32_t alpha = 0;
   wfst_decoder_opts_t o{};
-  int32_t C = 0, C_ovf = 0, FCAP = 0, TMAX = 0;
+  int32_t C = 0, C_ovf = 0, FCAP = 0, TMAX = 0, row_floats = 0, row_bytes = 0;
   int64_t R_cap = 0;
   int n_sm = 0, threads = 512, ctas_per_sm = 1;
   const WfstVariant* variant = nullptr;
@@ -208,10 +208,7 @@ cudaError_t launch_frames(wfst_decoder_t d, KParams kp, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-size_t smem_for(int C, int threads) {
-  (void)threads;
-  return (size_t)C * 8 + (size_t)kNB * 4;
-}
+size_t smem_for(int C, int row_bytes) { return (size_t)C * 8 + (size_t)kNB * 4 + (size_t)row_bytes; }
 
 }  // namespace
 
@@ -254,9 +251,19 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   const size_t static_smem = sizeof(SmemCtl) + 4 * (size_t)d->threads + (size_t)(d->threads / 32) * kStage * 16 + 1024;
   const size_t per_cta = std::min((size_t)prop.sharedMemPerBlockOptin,
                                   (size_t)prop.sharedMemPerMultiprocessor / d->ctas_per_sm);
-  int C = d->o.table_slots > 0 ? d->o.table_slots : (int)((per_cta - static_smem - (size_t)kNB * 4) / 8);
+  // the staged log-likelihood row: columns 0..max_pdf (+16 B alignment slack on each side)
+  const int row_floats = std::max(g->max_pdf + 1, 1);
+  const int row_bytes = (row_floats * 4 + 15) / 16 * 16 + 32;
+  int C = d->o.table_slots > 0 ? d->o.table_slots
+                               : (int)((per_cta - static_smem - (size_t)kNB * 4 - (size_t)row_bytes) / 8);
   C = std::max(64, C / 256 * 256);
-  while (C > 256 && smem_for(C, d->threads) + static_smem > per_cta) C -= 256;
+  while (C > 256 && smem_for(C, row_bytes) + static_smem > per_cta) C -= 256;
+  if (smem_for(C, row_bytes) + static_smem > per_cta) {
+    delete d;
+    return fail(WFST_ERR_INVALID_ARG, "log-likelihood row does not fit in shared memory (too many pdfs)");
+  }
+  d->row_floats = row_floats;
+  d->row_bytes = row_bytes;
   d->C = C;
   // overflow table: room for every distinct candidate a frame can hold beyond the on-chip table
   int Co = d->o.overflow_slots > 0 ? d->o.overflow_slots : std::max(std::max(C, 32768), 4 * d->alpha);
@@ -280,7 +287,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   }
   if (d->R_cap > INT32_MAX - 1) d->R_cap = INT32_MAX - 1;
   if (d->o.frames_per_item <= 0) d->o.frames_per_item = 16;
-  d->smem_bytes = smem_for(d->C, d->threads);
+  d->smem_bytes = smem_for(d->C, d->row_bytes);
   e = cudaFuncSetAttribute(d->variant->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d->smem_bytes);
   if (e != cudaSuccess) {
     delete d;
@@ -330,6 +337,8 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.state_info = g->d_state;
   kp.arcs = g->d_arcs;
   kp.start = g->start;
+  kp.row_floats = d->row_floats;
+  kp.row_bytes = d->row_bytes;
   kp.n_states = g->Q;
   kp.beam = beam;
   kp.alpha = d->alpha;

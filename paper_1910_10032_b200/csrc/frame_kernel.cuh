@@ -53,6 +53,8 @@ struct KParams {
   float beam;
   int32_t alpha;
   int32_t C, NBK, C_ovf, FCAP;
+  int32_t row_floats;     // log-likelihood columns staged on chip per frame (max pdf + 1)
+  int32_t row_bytes;      // shared bytes reserved for the staged row
   int64_t R_cap;
   int32_t TMAX;
   LaneState* lanes_st;
@@ -78,6 +80,8 @@ struct SmemCtl {
   int32_t n_claim, n_claim_emit, n_ovf, n_surv, n_in, n_wl, n_wl_next, n_big, n_fix, next_group;
   int32_t bucket_base[kNBuck];
   long long t_mark;
+  unsigned long long row_mbar;   // mbarrier of the row's bulk copy
+  int32_t row_parity, row_pending, row_off;
   float beam_cut, kalpha, ref, inv_w, min_surv;
   int32_t use_alpha;
   int32_t radix_prefix, radix_k;
@@ -156,6 +160,26 @@ __device__ __forceinline__ void sts32(uint32_t a, int v) {
 __device__ __forceinline__ u64 ldg_volatile64(const u64* p) { return *(const volatile u64*)p; }
 __device__ __forceinline__ void red_min_g64(u64* p, u64 v) {
   asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---- TMA bulk copy (global -> shared) completing on an mbarrier ----
+__device__ __forceinline__ void mbar_init(uint32_t a, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, int parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(a), "r"(parity) : "memory");
+  }
 }
 
 // monotone cost -> bin map, used both to count and to reject
@@ -297,6 +321,7 @@ struct Frame {
   uint32_t tab_sa;    // shared address of the token table (C slots of 8 B)
   uint32_t hist_sa;   // shared address of the cost histogram (kNB ints)
   uint32_t stage_sa;  // shared address of this warp's staging buffer (kStage x 16 B)
+  uint32_t row_sa;    // shared address of the staged log-likelihood row region
   int* hist;
   int* wbuf;          // this warp's owner buffer (32 ints, -1 when idle)
   // lane buffers
@@ -311,8 +336,36 @@ struct Frame {
   int2* rec;
   float* rec_cost;
 
-  __device__ Frame(const KParams& p_, SmemCtl& S_, uint32_t tab_sa_, int* hist_, int* wbuf_, uint32_t stage_sa_)
-      : p(p_), S(S_), tab_sa(tab_sa_), hist_sa(saddr(hist_)), stage_sa(stage_sa_), hist(hist_), wbuf(wbuf_) {}
+  __device__ Frame(const KParams& p_, SmemCtl& S_, uint32_t tab_sa_, int* hist_, int* wbuf_, uint32_t stage_sa_,
+                   uint32_t row_sa_)
+      : p(p_), S(S_), tab_sa(tab_sa_), hist_sa(saddr(hist_)), stage_sa(stage_sa_), row_sa(row_sa_), hist(hist_),
+        wbuf(wbuf_) {}
+
+  // ---- row a0: the frame's log-likelihood row is staged in shared memory by one TMA bulk
+  // copy (issued by thread 0; the next frame's row is prefetched during this frame's tail)
+  __device__ void row_issue(const float* row_g) {   // thread 0 only
+    if (S.row_pending) {
+      mbar_wait(saddr(&S.row_mbar), S.row_parity);
+      S.row_parity ^= 1;
+    }
+    const uintptr_t a = (uintptr_t)row_g;
+    const uintptr_t s = a & ~(uintptr_t)15;
+    const uintptr_t e = (a + (uintptr_t)p.row_floats * 4 + 15) & ~(uintptr_t)15;
+    const uint32_t bytes = (uint32_t)(e - s);
+    S.row_off = (int)(a - s);
+    mbar_expect_tx(saddr(&S.row_mbar), bytes);
+    bulk_g2s(row_sa, (const void*)s, bytes, saddr(&S.row_mbar));
+    S.row_pending = 1;
+  }
+  // all threads: wait for the pending row (caller guarantees one is pending)
+  __device__ void row_wait() {
+    mbar_wait(saddr(&S.row_mbar), S.row_parity);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      S.row_parity ^= 1;
+      S.row_pending = 0;
+    }
+  }
 
   __device__ void bind(int lane) {
     const size_t L = (size_t)lane, FC = (size_t)p.FCAP;
@@ -447,11 +500,12 @@ struct Frame {
   // inserts run with full warps.  Each improving insert also does a fire-and-forget 64-bit
   // RED.MIN of (cost, canonical arc id) into the slot's winner word: the min is exactly the
   // (cost, arc) tie-break of R9.
-  __device__ void expand(const float* __restrict__ row) {
+  __device__ void expand() {
     const int tid = threadIdx.x, lane = tid & 31;
     const int n_f = S.L.n_front;
     const int4* Fin = F0 + (size_t)S.L.cur * p.FCAP;
     const float ref = S.ref, inv_w = S.inv_w, beam = p.beam;
+    const uint32_t rowp = row_sa + (uint32_t)S.row_off;
     const uint32_t best_sa = saddr(&S.best_ord), theta_sa = saddr(&S.theta);
     long long arcs_total = 0;
     int staged = 0;   // warp-uniform
@@ -514,7 +568,7 @@ struct Frame {
         for (int u = 0; u < R; u++) arc[u] = v[u] ? __ldg(p.arcs + a[u]) : make_int4(0, 0, 0, 0);
         float L[R];
 #pragma unroll
-        for (int u = 0; u < R; u++) L[u] = v[u] ? __ldg(row + arc[u].z) : 0.0f;
+        for (int u = 0; u < R; u++) L[u] = v[u] ? __int_as_float(lds32(rowp + 4u * (uint32_t)arc[u].z)) : 0.0f;
         const uint32_t bo = (uint32_t)lds32(best_sa);
         const int th = lds32(theta_sa);
         const float bound = bo == 0xFFFFFFFFu ? INFINITY : __fadd_rn(float_of_ord(bo), beam);
@@ -551,7 +605,7 @@ struct Frame {
         }
         float L[R];
 #pragma unroll
-        for (int u = 0; u < R; u++) L[u] = v[u] ? __ldg(row + arc[u].z) : 0.0f;
+        for (int u = 0; u < R; u++) L[u] = v[u] ? __int_as_float(lds32(rowp + 4u * (uint32_t)arc[u].z)) : 0.0f;
         const uint32_t bo = (uint32_t)lds32(best_sa);
         const int th = lds32(theta_sa);
         const float bound = bo == 0xFFFFFFFFu ? INFINITY : __fadd_rn(float_of_ord(bo), beam);
@@ -1102,13 +1156,18 @@ struct Frame {
     }
   }
 
-  __device__ void run_frame(int t) {
+  __device__ const float* row_ptr(int t) const { return p.ll + ((size_t)t * p.B + S.b) * (size_t)p.P; }
+
+  // t_next < 0: no prefetch of the next frame's row
+  __device__ void run_frame(int t, int t_next) {
     const int tid = threadIdx.x;
-    const float* row = p.ll + ((size_t)t * p.B + S.b) * (size_t)p.P;
     long long t0 = clock64();
+    if (tid == 0 && !S.row_pending) row_issue(row_ptr(t));   // first frame of a work item
     begin_frame(INFINITY);
+    row_wait();
     tick(t0, 5);
-    expand(row);
+    expand();
+    if (tid == 0 && t_next >= 0) row_issue(row_ptr(t_next));   // overlaps the frame's tail
     tick(t0, 0);
     if (tid == 0) {
       S.n_claim_emit = S.n_claim;
@@ -1141,13 +1200,20 @@ __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
   __shared__ __align__(16) int4 s_stage[(BS / 32) * kStage];
   u64* tab = (u64*)smem_raw;
   int* hist = (int*)(tab + p.C);
+  unsigned char* rowmem = (unsigned char*)(hist + kNB);
   const int tid = threadIdx.x;
   const uint32_t tab_sa = saddr(tab);
   for (int i = tid; i < p.C; i += BS) sts64(tab_sa + 8u * i, kEmpty);
   s_wbuf[tid] = -1;
-  if (tid == 0) S.status = WFST_OK;
+  if (tid == 0) {
+    S.status = WFST_OK;
+    S.row_parity = 0;
+    S.row_pending = 0;
+    S.row_off = 0;
+    mbar_init(saddr(&S.row_mbar), 1);
+  }
   __syncthreads();
-  Frame<BS, R> fr(p, S, tab_sa, hist, s_wbuf + (tid & ~31), saddr(s_stage + (tid >> 5) * kStage));
+  Frame<BS, R> fr(p, S, tab_sa, hist, s_wbuf + (tid & ~31), saddr(s_stage + (tid >> 5) * kStage), saddr(rowmem));
   while (true) {
     if (tid == 0) S.item = atomicAdd(p.q_head, 1);
     __syncthreads();
@@ -1173,7 +1239,12 @@ __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
       const int t_end = min(p.T, (r + 1) * p.K);
       for (int t = r * p.K; t < t_end; t++) {
         if (S.L.status != WFST_OK) break;
-        fr.run_frame(t);
+        fr.run_frame(t, t + 1 < t_end ? t + 1 : -1);
+      }
+      if (tid == 0 && S.row_pending) {   // a prefetch left unused (lane stopped early)
+        mbar_wait(saddr(&S.row_mbar), S.row_parity);
+        S.row_parity ^= 1;
+        S.row_pending = 0;
       }
     }
     __syncthreads();
