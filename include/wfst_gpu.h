@@ -99,8 +99,10 @@ typedef struct {
   int64_t alpha_frames;      /* frames where max-active tightened the cutoff                      */
   int64_t device_bytes;      /* decoder device allocation                                         */
   int64_t records_used_max;  /* max traceback records used by any stream                          */
-  int64_t phase_cycles[6];   /* SM cycles summed over lanes: expand, cutoff, epsilon, drain+maps,
-                                rest of contraction, frame overhead (instrumentation)            */
+  int64_t phase_cycles[12];  /* SM cycles summed over lanes (instrumentation): 0 row prefetch issue,
+                                1 cutoff, 2 epsilon, 3 expansion (warp tokens), 4 expansion (hub
+                                tokens), 5 frame overhead, 6 drain, 7 map build, 8 placement,
+                                9 epsilon back-pointers, 10 table reset, 11 row wait            */
 } wfst_stats_t;
 
 /* ---- graph (row a0 of SURVEY §8) ------------------------------------------------ */

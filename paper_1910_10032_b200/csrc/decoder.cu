@@ -655,7 +655,7 @@ wfst_status wfst_decoder_stats(wfst_decoder_t d, wfst_stats_t* s) {
     s->overflow_inserts += x.ovf;
     s->alpha_frames += x.alpha_frames;
     s->records_used_max = std::max<int64_t>(s->records_used_max, x.rec_used);
-    for (int k = 0; k < 6; k++) s->phase_cycles[k] += (int64_t)x.phase[k];
+    for (int k = 0; k < 12; k++) s->phase_cycles[k] += (int64_t)x.phase[k];
   }
   s->device_bytes = d->device_bytes;
   return WFST_OK;
@@ -670,7 +670,7 @@ wfst_status wfst_decoder_reset_stats(wfst_decoder_t d) {
   if (e != cudaSuccess) return cuda_fail(e, "stats");
   for (auto& x : L) {
     x.emit_arcs = x.eps_arcs = x.eps_relax = x.cand = x.surv = x.ovf = x.alpha_frames = x.frames_total = 0;
-    for (int k = 0; k < 6; k++) x.phase[k] = 0;
+    for (int k = 0; k < 12; k++) x.phase[k] = 0;
   }
   e = cudaMemcpy(d->d_lanes, L.data(), sizeof(LaneState) * d->n_lanes, cudaMemcpyHostToDevice);
   return e == cudaSuccess ? WFST_OK : cuda_fail(e, "stats");

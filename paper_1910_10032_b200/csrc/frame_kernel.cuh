@@ -37,7 +37,7 @@ struct LaneState {
   int32_t rec_used;
   float front_best;     // min cost of the current survivors
   u64 emit_arcs, eps_arcs, eps_relax, cand, surv, ovf, alpha_frames, frames_total;
-  u64 phase[6];         // clock64 cycles: expand, cutoff, epsilon, (unused), contract, rest
+  u64 phase[12];        // clock64 cycles per phase (see wfst_stats_t.phase_cycles)
 };
 
 struct KParams {
@@ -587,6 +587,7 @@ struct Frame {
     if (staged > 0) flush(staged, beam, best_sa, theta_sa);
     staged = 0;
     __syncthreads();
+    mark(3);   // warp-expanded tokens done
     // tokens with large out-degree (hub states): all threads share their arcs
     const int nbig = min(S.n_big, kBigCap);
     for (int k = 0; k < nbig; k++) {
@@ -625,6 +626,7 @@ struct Frame {
     arcs_total = block_sum64<BS>(arcs_total, S.warp_tmp64);
     if (tid == 0) S.emit_arcs = arcs_total;
     __syncthreads();
+    mark(4);   // hub tokens done
   }
 
   // ---- row a3: beam + exact max-active (readings R5, R6) ----
@@ -848,7 +850,6 @@ struct Frame {
       S.n_surv = 0;
       S.n_fix = 0;
       S.min_surv = INFINITY;
-      S.t_mark = clock64();
     }
     __syncthreads();
     float mn = INFINITY;
@@ -902,6 +903,7 @@ struct Frame {
     for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     if ((tid & 31) == 0) S.warp_tmp[tid >> 5] = __float_as_int(mn);
     const long long n_eps_tot = block_sum64<BS>(n_eps_surv, S.warp_tmp64);   // barriers
+    mark(6);   // drain done
     if (tid == 0) {
       float m = INFINITY;
       for (int w = 0; w < NW; w++) m = fminf(m, __int_as_float(S.warp_tmp[w]));
@@ -949,11 +951,7 @@ struct Frame {
         if (q[u] != 0xFFFFFFFFu) map_put(sm, m1_sa, g1, cap1, q[u], i0 + u * BS + tid);
     }
     __syncthreads();
-    if (tid == 0) {   // phase split: drain done, maps built
-      const long long t1 = clock64();
-      S.L.phase[3] += (u64)(t1 - S.t_mark);
-      S.t_mark = t1;
-    }
+    mark(7);   // M1 built
     // pass 2: place survivors in cost-bucket order, state records, emitting back-pointers
     int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
     long long epsd = 0;
@@ -1008,6 +1006,7 @@ struct Frame {
     }
     const long long eps_deg = block_sum64<BS>(epsd, S.warp_tmp64);   // barriers
     if (tid == 0) S.eps_deg = eps_deg;
+    mark(8);   // pass 2 done
     // pass 3: epsilon back-pointers -> record of the source survivor in this layer
     const int n_fix = S.n_fix;
     for (int k = tid; k < n_fix; k += BS) {
@@ -1019,6 +1018,7 @@ struct Frame {
       rec[rb + pos] = e;
     }
     __syncthreads();
+    mark(9);   // pass 3 done
     // give the table memory back (empty slots)
     if (sm)
       for (uint32_t i = tid; i < cap1 + cap2; i += BS) sts64(tab_sa + 8u * i, kEmpty);
@@ -1140,6 +1140,13 @@ struct Frame {
     finish_frame(-1, false);
   }
 
+  __device__ __forceinline__ void mark(int ph) {   // thread 0, after a barrier
+    if (threadIdx.x == 0) {
+      const long long t1 = clock64();
+      S.L.phase[ph] += (u64)(t1 - S.t_mark);
+      S.t_mark = t1;
+    }
+  }
   __device__ __forceinline__ void tick(long long& t0, int ph) {
     if (threadIdx.x == 0) {
       const long long t1 = clock64();
@@ -1147,11 +1154,11 @@ struct Frame {
       t0 = t1;
     }
   }
-  // contraction: phase[3] = drain + maps (measured inside), phase[4] = the rest
+  // contraction sub-phases are marked inside contract(); this closes the last one
   __device__ __forceinline__ void tick_contract(long long& t0) {
     if (threadIdx.x == 0) {
       const long long t1 = clock64();
-      S.L.phase[4] += (u64)(t1 - S.t_mark);
+      S.L.phase[10] += (u64)(t1 - S.t_mark);
       t0 = t1;
     }
   }
@@ -1164,8 +1171,10 @@ struct Frame {
     long long t0 = clock64();
     if (tid == 0 && !S.row_pending) row_issue(row_ptr(t));   // first frame of a work item
     begin_frame(INFINITY);
-    row_wait();
     tick(t0, 5);
+    row_wait();
+    tick(t0, 11);
+    if (tid == 0) S.t_mark = clock64();
     expand();
     if (tid == 0 && t_next >= 0) row_issue(row_ptr(t_next));   // overlaps the frame's tail
     tick(t0, 0);
@@ -1185,6 +1194,7 @@ struct Frame {
     tick(t0, 1);
     eps_closure();
     tick(t0, 2);
+    if (tid == 0) S.t_mark = clock64();
     contract();
     tick_contract(t0);
     finish_frame(t, true);
