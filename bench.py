@@ -129,8 +129,12 @@ def reduce_over_ranks(dist, device, ms: float, arcs: float):
 
 
 # ------------------------------------------------------------------------- workload
-def make_workload(cfg: str, preset: str, rank: int = 0, world: int = 1):
-    c = I.CONFIGS[cfg]
+def make_workload(cfg: str, preset: str, rank: int = 0, world: int = 1, beam=None, max_active=None):
+    c = dict(I.CONFIGS[cfg])
+    if beam:
+        c["beam"] = beam
+    if max_active:
+        c["max_active"] = max_active
     g = I.config_graph(cfg)
     B, T, P = c["streams"], c["frames"], c["n_pdfs"]
     stream0 = rank_streams(rank, world, B).start
@@ -191,7 +195,7 @@ def gpu_arm(args):
     if world > 1:
         dist.barrier()
 
-    wl = make_workload(args.config, args.preset, rank, world)
+    wl = make_workload(args.config, args.preset, rank, world, args.beam, args.max_active)
     T, B, P = wl["T"], wl["B"], wl["P"]
     G = W.Graph.from_arrays(wl["graph"], device=local)
     ginfo = G.info()
@@ -389,6 +393,8 @@ def main(argv=None):
     ap.add_argument("--ctas-per-sm", dest="ctas_per_sm", type=int, default=0)
     ap.add_argument("--table-slots", dest="table_slots", type=int, default=0)
     ap.add_argument("--frames-per-item", dest="frames_per_item", type=int, default=0)
+    ap.add_argument("--beam", type=float, default=None, help="override the config's beam (experiments)")
+    ap.add_argument("--max-active", dest="max_active", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
