@@ -25,7 +25,10 @@ constexpr int kModeFrames = 0, kModeInit = 1;
 constexpr int kBig = 64;           // tokens with more emitting arcs are expanded CTA-wide
 constexpr int kBigCap = 256;
 constexpr int kStage = 32;         // per-warp staging buffer (candidates awaiting insertion)
-constexpr int kNBuck = 16;         // cost buckets ordering the next frontier
+#ifndef WFST_NBUCK
+#define WFST_NBUCK 16
+#endif
+constexpr int kNBuck = WFST_NBUCK; // cost buckets ordering the next frontier
 
 struct LaneState {
   int32_t status;       // wfst_status, sticky
