@@ -25,13 +25,14 @@ namespace {
 
 // ---------------- best path (row a7; readings R10, R11) ----------------
 // One CTA per lane: argmin over the last layer's survivors of (c + F, arc) among final states,
-// else of (c, arc); then the traceback walk over {arc, prev} records.
+// else of (c, arc); then the traceback: the predecessor of a record {arc, state} is the record
+// of src(arc) in the previous layer (emitting arc) or the same layer (epsilon arc), found by a
+// CTA-wide scan of that layer's records.  Arcs are written back to front into arcs_out.
 __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, const int32_t* __restrict__ lanes,
-                                 int32_t n, int32_t cap,
-                                 float* cost_out, int32_t* reached_out, int32_t* n_arcs_out, int32_t* arcs_out,
-                                 int32_t* olab_out, int32_t* n_olab_out, int32_t* status_out) {
+                                 int32_t n, int32_t cap, float* cost_out, int32_t* reached_out, int32_t* n_arcs_out,
+                                 int32_t* arcs_out, int32_t* olab_out, int32_t* n_olab_out, int32_t* status_out) {
   __shared__ u64 s_fin[32], s_any[32];
-  __shared__ int s_idx;
+  __shared__ int s_idx, s_arc, s_layer, s_len, s_status;
   const int li = blockIdx.x;
   const int lane = lanes[li];
   const int tid = threadIdx.x;
@@ -53,12 +54,13 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, 
   }
   const int4* Fc = p.front + (size_t)lane * 2 * p.FCAP + (size_t)L.cur * p.FCAP;
   const int2* rec = p.rec + (size_t)lane * p.R_cap;
+  const int2* linfo = p.layer_info + (size_t)lane * (p.TMAX + 1);
   u64 kf = kEmpty, ka = kEmpty;
   for (int i = tid; i < L.n_front; i += blockDim.x) {
-    int4 f = __ldcg(Fc + i);
-    float c = __int_as_float(f.y);
-    u64 arc = (uint32_t)__ldcg(&rec[L.layer_base + i].x);  // -1 -> 0xFFFFFFFF sorts last (R9)
-    float F = __int_as_float(__ldg(&p.state_info[f.x].w));
+    const int4 f = __ldcg(Fc + i);
+    const float c = __int_as_float(f.y);
+    const u64 arc = (uint32_t)__ldcg(&rec[L.layer_base + i].x);  // -1 -> 0xFFFFFFFF sorts last (R9)
+    const float F = __int_as_float(__ldg(&p.state_info[f.x].w));
     if (F < INFINITY) kf = min(kf, ((u64)ord_of(__fadd_rn(c, F)) << 32) | arc);
     ka = min(ka, ((u64)ord_of(c) << 32) | arc);
   }
@@ -70,7 +72,11 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, 
     s_fin[tid >> 5] = kf;
     s_any[tid >> 5] = ka;
   }
-  if (tid == 0) s_idx = -1;
+  if (tid == 0) {
+    s_idx = -1;
+    s_len = 0;
+    s_status = WFST_OK;
+  }
   __syncthreads();
   kf = kEmpty;
   ka = kEmpty;
@@ -84,50 +90,79 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, 
   for (int i = tid; i < L.n_front && kb != kEmpty; i += blockDim.x)
     if ((uint32_t)__ldcg(&rec[L.layer_base + i].x) == (uint32_t)kb) s_idx = i;
   __syncthreads();
+  if (kb == kEmpty || s_idx < 0) {
+    if (tid == 0) {
+      status_out[li] = WFST_ERR_NO_SURVIVOR;
+      n_arcs_out[li] = 0;
+      n_olab_out[li] = 0;
+      cost_out[li] = INFINITY;
+      reached_out[li] = 0;
+    }
+    return;
+  }
+  if (tid == 0) {
+    cost_out[li] = float_of_ord((uint32_t)(kb >> 32));
+    reached_out[li] = reached ? 1 : 0;
+    s_arc = __ldcg(&rec[L.layer_base + s_idx].x);
+    s_layer = L.frames;
+  }
+  __syncthreads();
+  // walk back: arcs are stored from the end of this lane's output row (reversed afterwards)
+  int32_t* out = arcs_out + (size_t)li * cap;
+  const long long max_steps = (long long)L.rec_used + 2;
+  for (long long step = 0; step < max_steps; step++) {
+    const int arc = s_arc;
+    if (arc < 0) break;
+    int src = 0, layer = 0;
+    if (tid == 0) {
+      const int4 a = __ldg(p.arcs + arc);
+      src = a.w & 0x7FFFFFFF;
+      layer = a.z >= 0 ? s_layer - 1 : s_layer;
+      if (s_len < cap) out[s_len] = arc;
+      s_len++;
+      s_idx = -1;
+      s_layer = layer;
+      s_arc = src;   // temporarily: the state to look for
+    }
+    __syncthreads();
+    const int want = s_arc;
+    layer = s_layer;
+    const int2 info = __ldcg(&linfo[layer]);
+    __syncthreads();
+    for (int i = tid; i < info.y; i += blockDim.x) {
+      const int2 r = __ldcg(rec + info.x + i);
+      if (r.y == want) {
+        s_idx = info.x + i;
+        s_arc = r.x;
+      }
+    }
+    __syncthreads();
+    if (s_idx < 0) {
+      if (tid == 0) s_status = WFST_ERR_STATE;   // broken chain (must not happen)
+      break;
+    }
+  }
+  __syncthreads();
   if (tid != 0) return;
-  const int best_i = s_idx;
-  if (kb == kEmpty || best_i < 0) {
-    status_out[li] = WFST_ERR_NO_SURVIVOR;
-    n_arcs_out[li] = 0;
-    n_olab_out[li] = 0;
-    cost_out[li] = INFINITY;
-    reached_out[li] = 0;
-    return;
-  }
-  cost_out[li] = float_of_ord((uint32_t)(kb >> 32));
-  reached_out[li] = reached ? 1 : 0;
-  int len = 0;
-  int32_t r = L.layer_base + best_i;
-  long long guard = (long long)L.rec_used + 2;
-  while (r >= 0 && --guard > 0) {
-    int2 e = __ldcg(rec + r);
-    if (e.x < 0) break;
-    len++;
-    r = e.y;
-  }
+  const int len = s_len;
   n_arcs_out[li] = len;
-  if (guard <= 0) {
-    n_olab_out[li] = 0;
-    status_out[li] = WFST_ERR_CAPACITY;
-    return;
-  }
-  // second walk writes arcs back to front; olabels are counted from the arc list
-  r = L.layer_base + best_i;
-  for (int pos = len - 1; pos >= 0; pos--) {
-    int2 e = __ldcg(rec + r);
-    if (pos < cap) arcs_out[(size_t)li * cap + pos] = e.x;
-    r = e.y;
+  // reverse in place to forward order, then olabels
+  const int m = min(len, cap);
+  for (int k = 0; k < m / 2; k++) {
+    const int32_t t = out[k];
+    out[k] = out[m - 1 - k];
+    out[m - 1 - k] = t;
   }
   int nol = 0;
-  for (int k = 0; k < len && k < cap; k++) {
-    int32_t ol = __ldg(olabel + arcs_out[(size_t)li * cap + k]);
+  for (int k = 0; k < m; k++) {
+    const int32_t ol = __ldg(olabel + out[k]);
     if (ol != 0) {
       if (nol < cap) olab_out[(size_t)li * cap + nol] = ol;
       nol++;
     }
   }
   n_olab_out[li] = nol;
-  status_out[li] = (len > cap) ? WFST_ERR_INVALID_ARG : WFST_OK;
+  status_out[li] = s_status != WFST_OK ? s_status : (len > cap ? WFST_ERR_INVALID_ARG : WFST_OK);
 }
 
 }  // namespace
@@ -269,7 +304,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   int Co = d->o.overflow_slots > 0 ? d->o.overflow_slots : std::max(std::max(C, 32768), 4 * d->alpha);
   d->C_ovf = std::max(64, (Co + 3) / 4 * 4);
   d->FCAP = d->C + d->C_ovf;
-  d->TMAX = d->o.max_frames > 0 ? d->o.max_frames : 2048;
+  d->TMAX = d->o.max_frames > 0 ? d->o.max_frames : 4096;
   int64_t per_frame = d->alpha > 0 ? std::min<int64_t>((int64_t)d->alpha * 5 / 4 + 1024, d->FCAP) : d->FCAP;
   if (d->o.records_per_stream > 0) {
     d->R_cap = d->o.records_per_stream;
@@ -278,7 +313,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     d->R_cap = (int64_t)(d->TMAX / 4 + 1) * per_frame;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-      int64_t per_lane_other = (int64_t)d->FCAP * (32 + 4 + 8 + 16 + 16 + 4 + 8) + (int64_t)d->C_ovf * 8 +
+      int64_t per_lane_other = (int64_t)d->FCAP * (32 + 4 + 8 + 16 + 8) + (int64_t)d->C_ovf * 8 +
                                (int64_t)d->TMAX * 60;
       int64_t budget = (int64_t)(free_b / 2) / n_streams - per_lane_other;
       int64_t cap = budget / (int64_t)(sizeof(int2) + (d->o.debug_costs ? 4 : 0));
@@ -308,8 +343,6 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   size_t i_claim = add(L * FC * 4);
   size_t i_win = add(L * FC * 8);
   size_t i_tmp = add(L * FC * sizeof(int4));
-  size_t i_gmap = add(L * 2 * FC * 8);
-  size_t i_fix = add(L * FC * 4);
   size_t i_ovf = add(L * (size_t)d->C_ovf * 8);
   size_t i_wl = add(L * 2 * FC * 4);
   size_t i_rec = add(L * (size_t)d->R_cap * sizeof(int2));
@@ -353,8 +386,6 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.claim = (uint32_t*)(base + parts[i_claim].off);
   kp.win = (u64*)(base + parts[i_win].off);
   kp.tmp = (int4*)(base + parts[i_tmp].off);
-  kp.gmap = (u64*)(base + parts[i_gmap].off);
-  kp.epsfix = (int32_t*)(base + parts[i_fix].off);
   kp.ovf = (u64*)(base + parts[i_ovf].off);
   kp.wl = (uint32_t*)(base + parts[i_wl].off);
   kp.rec = (int2*)(base + parts[i_rec].off);
@@ -721,7 +752,7 @@ wfst_status wfst_debug_layer(wfst_decoder_t d, int32_t stream, int32_t layer, in
   }
   for (int i = 0; i < info.y; i++) {
     int32_t a = r[i].x;
-    if (states) states[i] = a < 0 ? d->g->start : d->g->h_dst[a];
+    if (states) states[i] = r[i].y;
     if (arcs) arcs[i] = a;
     if (costs) costs[i] = c[i];
   }

@@ -64,12 +64,10 @@ struct KParams {
   int4* front;        // [lane][2][FCAP]  {state, cost bits, e_begin, n_emit}, cost-bucketed
   uint32_t* claim;    // [lane][FCAP]     slot | has_eps << 31, one per distinct state
   u64* win;           // [lane][FCAP]     per slot: min (ord(cost) << 32 | canonical arc id)
-  int4* tmp;          // [lane][FCAP]     contraction scratch {state, cost, arc, has_eps | bucket}
-  u64* gmap;          // [lane][2*FCAP]   state -> index maps when they do not fit on chip
-  int32_t* epsfix;    // [lane][FCAP]     positions of survivors won by an epsilon arc
+  int4* tmp;          // [lane][FCAP]     contraction scratch {state, cost, arc, bucket}
   u64* ovf;           // [lane][C_ovf]    global overflow token table
   uint32_t* wl;       // [lane][2][FCAP]  epsilon worklists (slots)
-  int2* rec;          // [lane][R_cap]    traceback records {arc, prev}
+  int2* rec;          // [lane][R_cap]    traceback records {winning arc (-1: start), state}
   float* rec_cost;    // [lane][R_cap]    (debug) survivor cost
   float* fstats;      // [lane][TMAX][3]
   long long* fcounts; // [lane][TMAX][5]
@@ -80,7 +78,7 @@ struct SmemCtl {
   int32_t item, lane, b, status;
   uint32_t best_ord;
   int32_t theta;
-  int32_t n_claim, n_claim_emit, n_ovf, n_surv, n_in, n_wl, n_wl_next, n_big, n_fix, next_group;
+  int32_t n_claim, n_claim_emit, n_ovf, n_surv, n_in, n_wl, n_wl_next, n_big, next_group;
   int32_t bucket_base[kNBuck];
   long long t_mark;
   unsigned long long row_mbar;   // mbarrier of the row's bulk copy
@@ -332,8 +330,6 @@ struct Frame {
   uint32_t* claim;
   u64* win;
   int4* tmp;
-  u64* gmap;
-  int32_t* epsfix;
   u64* ovf;
   uint32_t* wl0;      // epsilon worklist 0; worklist 1 follows at +FCAP
   int2* rec;
@@ -376,8 +372,6 @@ struct Frame {
     claim = p.claim + L * FC;
     win = p.win + L * FC;
     tmp = p.tmp + L * FC;
-    gmap = p.gmap + L * 2 * FC;
-    epsfix = p.epsfix + L * FC;
     ovf = p.ovf + L * (size_t)p.C_ovf;
     wl0 = p.wl + L * 2 * FC;
     rec = p.rec + L * (size_t)p.R_cap;
@@ -806,42 +800,13 @@ struct Frame {
     if (tid == 0) S.eps_relax = tot;
   }
 
-  // state -> index open-addressing map (8 B entries {state, index}), on chip or global
-  __device__ __forceinline__ void map_put(bool sm, uint32_t base_sa, u64* gbase, uint32_t cap, uint32_t q,
-                                          int idx) const {
-    const u64 e = ((u64)(uint32_t)idx << 32) | q;
-    uint32_t h = __umulhi(q * 0x9E3779B1u, cap);
-    while (true) {
-      u64 old;
-      if (sm) old = atom_cas_s(base_sa + 8u * h, kEmpty, e);
-      else old = atomicCAS(gbase + h, kEmpty, e);
-      if (old == kEmpty) return;
-      h = (h + 1 == cap) ? 0 : h + 1;
-    }
-  }
-  __device__ __forceinline__ int map_get(bool sm, uint32_t base_sa, const u64* gbase, uint32_t cap,
-                                         uint32_t q) const {
-    uint32_t h = __umulhi(q * 0x9E3779B1u, cap);
-    for (uint32_t n = 0; n < cap; n++) {
-      const u64 v = sm ? lds64(base_sa + 8u * h) : __ldcg(gbase + h);
-      if (v == kEmpty) return -1;
-      if ((uint32_t)v == q) return (int)(v >> 32);
-      h = (h + 1 == cap) ? 0 : h + 1;
-    }
-    return -1;
-  }
-
   // ---- rows a4 + a6: contraction into the next frontier (cost-bucketed) + records ----
-  // Back-pointers: an emitting winner's source is a token of the previous layer (map M1:
-  // state -> token, built here from that frontier); an epsilon winner's source is a survivor
-  // of this layer (map M2 over the survivors whose state has epsilon arcs).  Both maps live in
-  // the drained token table when they fit.
+  // A traceback record is {winning arc, state}: the predecessor is the record of src(arc) in
+  // the previous layer (emitting arc) or in the same layer (epsilon arc), found by the
+  // end-of-stream traceback -- nothing per frame has to map states to records.
   __device__ void contract() {
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int n_claim = min(S.n_claim, p.FCAP);
-    const int n_front = S.L.n_front;
-    const int4* Fin = F0 + (size_t)S.L.cur * p.FCAP;
-    const int32_t prev_base = S.L.layer_base;
     const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
     // bucket range [best, cutoff) for the cost order of the next frontier
     const float bk_ref = float_of_ord(S.best_ord);
@@ -851,14 +816,12 @@ struct Frame {
     if (tid < kNBuck) S.bucket_base[tid] = 0;
     if (tid == 0) {
       S.n_surv = 0;
-      S.n_fix = 0;
       S.min_surv = INFINITY;
     }
     __syncthreads();
     float mn = INFINITY;
-    int n_eps_surv = 0;
     constexpr int U = 4;
-    // pass 1: drain the tables; survivors -> tmp {state, cost, arc, has_eps << 31 | bucket}
+    // pass 1: drain the tables; survivors -> tmp {state, cost, arc, bucket}
     for (int i0 = 0; i0 < n_claim; i0 += BS * U) {
       uint32_t cl[U];
       u64 v[U], w[U];
@@ -888,7 +851,7 @@ struct Frame {
                             : kNBuck;
         {   // warp-aggregated bucket count
           const unsigned grp = __match_any_sync(0xffffffffu, bk);
-          if (bk < kNBuck && (tid & 31) == __ffs(grp) - 1) red_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
+          if (bk < kNBuck && lane == __ffs(grp) - 1) red_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
         }
         if (!k[u]) continue;
         if (r >= p.FCAP) {
@@ -897,16 +860,15 @@ struct Frame {
         }
         // the winner word's cost must be the slot's final cost (every improving insert RED's)
         const int32_t arc = (uint32_t)(w[u] >> 32) == (uint32_t)(v[u] >> 32) ? (int32_t)(uint32_t)w[u] : -2;
-        tmp[r] = make_int4((int)(uint32_t)v[u], __float_as_int(c), arc, (int)(cl[u] & 0x80000000u) | bk);
-        n_eps_surv += (cl[u] >> 31);
+        if (arc == -2) S.status = WFST_ERR_STATE;
+        tmp[r] = make_int4((int)(uint32_t)v[u], __float_as_int(c), arc, bk);
         mn = fminf(mn, c);
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     if ((tid & 31) == 0) S.warp_tmp[tid >> 5] = __float_as_int(mn);
-    const long long n_eps_tot = block_sum64<BS>(n_eps_surv, S.warp_tmp64);   // barriers
-    mark(6);   // drain done
+    __syncthreads();
     if (tid == 0) {
       float m = INFINITY;
       for (int w = 0; w < NW; w++) m = fminf(m, __int_as_float(S.warp_tmp[w]));
@@ -918,6 +880,8 @@ struct Frame {
         acc += n;
       }
     }
+    mark(6);   // drain done
+    __syncthreads();
     const int n_surv = min(S.n_surv, p.FCAP);
     const int32_t rb = S.L.rec_used;
     if ((long long)rb + n_surv > p.R_cap) {
@@ -925,37 +889,7 @@ struct Frame {
       __syncthreads();
       return;
     }
-    // maps in the drained table: M1 (prev tokens) then M2 (this layer's epsilon-capable states)
-    // load <= 1/2 on chip when there is room (linear probing); global maps otherwise
-    const uint32_t cap2 = (uint32_t)max((int)n_eps_tot * 2 + 32, 64);
-    uint32_t cap1 = (uint32_t)max(2 * n_front + 32, 64);
-    if (cap1 + cap2 > (uint32_t)p.C) cap1 = max((uint32_t)p.C - cap2, (uint32_t)(n_front + (n_front >> 2) + 32));
-    const bool sm = (size_t)(cap1 + cap2) <= (size_t)p.C;
-    const uint32_t m1_sa = tab_sa, m2_sa = tab_sa + 8u * cap1;
-    u64* g1 = gmap;
-    u64* g2 = gmap + cap1;
-    if (!sm && cap1 + cap2 > 2u * (uint32_t)p.FCAP) {
-      if (tid == 0) S.status = WFST_ERR_CAPACITY;
-      __syncthreads();
-      return;
-    }
-    if (!sm)
-      for (uint32_t i = tid; i < cap1 + cap2; i += BS) gmap[i] = kEmpty;
-    __syncthreads();
-    for (int i0 = 0; i0 < n_front; i0 += BS * U) {
-      uint32_t q[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int i = i0 + u * BS + tid;
-        q[u] = i < n_front ? (uint32_t)__ldcg(&Fin[i].x) : 0xFFFFFFFFu;
-      }
-#pragma unroll
-      for (int u = 0; u < U; u++)
-        if (q[u] != 0xFFFFFFFFu) map_put(sm, m1_sa, g1, cap1, q[u], i0 + u * BS + tid);
-    }
-    __syncthreads();
-    mark(7);   // M1 built
-    // pass 2: place survivors in cost-bucket order, state records, emitting back-pointers
+    // pass 2: place survivors in cost-bucket order; state records; traceback records
     int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
     long long epsd = 0;
     for (int r0 = 0; r0 < n_surv; r0 += BS * U) {   // warp-uniform trip count
@@ -968,64 +902,29 @@ struct Frame {
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {   // warp-aggregated bucket cursors
-        const int bk = t[u].w & 0xFFFF;
+        const int bk = t[u].w;
         const unsigned grp = __match_any_sync(0xffffffffu, bk);
         const int leader = __ffs(grp) - 1;
         int base = 0;
-        if (bk < kNBuck && (threadIdx.x & 31) == leader) base = atom_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
+        if (bk < kNBuck && lane == leader) base = atom_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
         base = __shfl_sync(0xffffffffu, base, leader);
-        pos[u] = base + __popc(grp & ((1u << (threadIdx.x & 31)) - 1u));
+        pos[u] = base + __popc(grp & ((1u << lane) - 1u));
       }
-      int4 si[U], ar[U];
+      int4 si[U];
 #pragma unroll
-      for (int u = 0; u < U; u++) {
-        si[u] = t[u].x >= 0 ? __ldg(p.state_info + t[u].x) : make_int4(0, 0, 0, 0);
-        ar[u] = t[u].z >= 0 ? __ldg(p.arcs + t[u].z) : make_int4(0, 0, 0, 0);
-      }
+      for (int u = 0; u < U; u++) si[u] = t[u].x >= 0 ? __ldg(p.state_info + t[u].x) : make_int4(0, 0, 0, 0);
 #pragma unroll
       for (int u = 0; u < U; u++) {
         if (t[u].x < 0) continue;
         Fout[pos[u]] = make_int4(t[u].x, t[u].y, si[u].x, si[u].y - si[u].x);
         epsd += si[u].z - si[u].y;
-        if (t[u].w & 0x80000000) map_put(sm, m2_sa, g2, cap2, (uint32_t)t[u].x, pos[u]);
-        int32_t arc = t[u].z, prev = -1;
-        if (arc >= 0) {
-          const uint32_t src = (uint32_t)ar[u].w & 0x7FFFFFFFu;
-          if (ar[u].z >= 0) {   // emitting winner: source token in the previous layer
-            const int ti = map_get(sm, m1_sa, g1, cap1, src);
-            prev = ti >= 0 ? prev_base + ti : -3;
-          } else {              // epsilon winner: resolved in pass 3
-            prev = (int32_t)(src | 0x80000000u);
-            const int fi = atomicAdd(&S.n_fix, 1);
-            epsfix[fi] = pos[u];
-          }
-        } else if (arc == -2) {
-          prev = -3;            // inconsistent winner word (must not happen)
-        }
-        if (prev == -3) S.status = WFST_ERR_STATE;
-        rec[rb + pos[u]] = make_int2(arc, prev);
+        rec[rb + pos[u]] = make_int2(t[u].z, t[u].x);
         if (rec_cost) rec_cost[rb + pos[u]] = __int_as_float(t[u].y);
       }
     }
     const long long eps_deg = block_sum64<BS>(epsd, S.warp_tmp64);   // barriers
     if (tid == 0) S.eps_deg = eps_deg;
-    mark(8);   // pass 2 done
-    // pass 3: epsilon back-pointers -> record of the source survivor in this layer
-    const int n_fix = S.n_fix;
-    for (int k = tid; k < n_fix; k += BS) {
-      const int pos = epsfix[k];
-      int2 e = rec[rb + pos];
-      const int si = map_get(sm, m2_sa, g2, cap2, (uint32_t)e.y & 0x7FFFFFFFu);
-      if (si < 0) S.status = WFST_ERR_STATE;
-      e.y = rb + si;
-      rec[rb + pos] = e;
-    }
-    __syncthreads();
-    mark(9);   // pass 3 done
-    // give the table memory back (empty slots)
-    if (sm)
-      for (uint32_t i = tid; i < cap1 + cap2; i += BS) sts64(tab_sa + 8u * i, kEmpty);
-    __syncthreads();
+    mark(8);   // placement done
   }
 
   __device__ void begin_frame(float beam_cut_fixed) {
@@ -1171,6 +1070,11 @@ struct Frame {
   // t_next < 0: no prefetch of the next frame's row
   __device__ void run_frame(int t, int t_next) {
     const int tid = threadIdx.x;
+    if (S.L.frames >= p.TMAX) {   // layer boundaries of longer utterances are not kept
+      if (tid == 0) S.L.status = WFST_ERR_CAPACITY;
+      __syncthreads();
+      return;
+    }
     long long t0 = clock64();
     if (tid == 0 && !S.row_pending) row_issue(row_ptr(t));   // first frame of a work item
     begin_frame(INFINITY);
