@@ -62,7 +62,7 @@ struct KParams {
   int32_t TMAX;
   LaneState* lanes_st;
   int4* front;        // [lane][2][FCAP]  {state, cost bits, e_begin, n_emit}, cost-bucketed
-  uint32_t* claim;    // [lane][FCAP]     slot | has_eps << 31, one per distinct state
+  uint32_t* claim;    // [lane][C_ovf]    overflow-table slots claimed this frame
   u64* win;           // [lane][FCAP]     per slot: min (ord(cost) << 32 | canonical arc id)
   int4* tmp;          // [lane][FCAP]     contraction scratch {state, cost, arc, bucket}
   u64* ovf;           // [lane][C_ovf]    global overflow token table
@@ -78,7 +78,7 @@ struct SmemCtl {
   int32_t item, lane, b, status;
   uint32_t best_ord;
   int32_t theta;
-  int32_t n_claim, n_claim_emit, n_ovf, n_surv, n_in, n_wl, n_wl_next, n_big, next_group;
+  int32_t n_claim, n_claim_emit, n_ovf, n_oclaim, n_surv, n_in, n_wl, n_wl_next, n_big, next_group;
   int32_t bucket_base[kNBuck];
   long long t_mark;
   unsigned long long row_mbar;   // mbarrier of the row's bulk copy
@@ -369,7 +369,7 @@ struct Frame {
   __device__ void bind(int lane) {
     const size_t L = (size_t)lane, FC = (size_t)p.FCAP;
     F0 = p.front + L * 2 * FC;
-    claim = p.claim + L * FC;
+    claim = p.claim + L * (size_t)p.C_ovf;
     win = p.win + L * FC;
     tmp = p.tmp + L * FC;
     ovf = p.ovf + L * (size_t)p.C_ovf;
@@ -410,11 +410,14 @@ struct Frame {
     if (lane == leader) base = atom_add_s(saddr(&S.n_claim), __popc(m));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (claimed) {
-      const int ci = base + __popc(m & ((1u << lane) - 1u));
-      if (ci < p.FCAP) claim[ci] = (uint32_t)slot | (eps_flag << 31);
-      else S.status = WFST_ERR_CAPACITY;
+      if (slot >= p.C) {   // the on-chip table is scanned directly; only overflow slots are listed
+        const int oi = atomicAdd(&S.n_oclaim, 1);
+        if (oi < p.C_ovf) claim[oi] = (uint32_t)slot;
+        else S.status = WFST_ERR_CAPACITY;
+      }
       if (bin >= 0) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
     }
+    (void)eps_flag;
     const int end = base + __popc(m);
     return p.alpha > 0 && end >= p.alpha && (end >> 10) != (base >> 10);
   }
@@ -461,7 +464,8 @@ struct Frame {
                       bin < lds32(theta_sa);
       if (ok) {
         if (o < bo) red_min_s32(best_sa, o);
-        slot = insert((uint32_t)e.x, ((u64)o << 32) | (uint32_t)e.x, claimed, logit, strict);
+        const uint32_t qf = (uint32_t)e.x | (flag << 31);   // state | has-epsilon flag
+        slot = insert(qf, ((u64)o << 32) | qf, claimed, logit, strict);
         if (slot >= 0 && logit) red_min_g64(win + slot, ((u64)o << 32) | (uint32_t)e.z);
         if (slot < 0) claimed = false;
       }
@@ -626,6 +630,39 @@ struct Frame {
     mark(4);   // hub tokens done
   }
 
+  // Visit every live token-table entry: the on-chip table is scanned directly (strided, so a
+  // warp reads consecutive slots), then the overflow slots listed this frame.  f(slot, value)
+  // is called by every lane with value == kEmpty for empty/out-of-range positions, U entries
+  // per lane per step so the loads overlap (warp-collective callbacks are allowed).
+  template <int U, typename Fn>
+  __device__ __forceinline__ void scan_entries(Fn f) {
+    const int tid = threadIdx.x;
+    for (int i0 = 0; i0 < p.C; i0 += BS * U) {
+      u64 v[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int i = i0 + u * BS + tid;
+        v[u] = i < p.C ? lds64(tab_sa + 8u * (uint32_t)i) : kEmpty;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) f(i0 + u * BS + tid, v[u]);
+    }
+    const int no = min(S.n_oclaim, p.C_ovf);
+    for (int i0 = 0; i0 < no; i0 += BS * U) {
+      int sl[U];
+      u64 v[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int i = i0 + u * BS + tid;
+        sl[u] = i < no ? (int)__ldcg(claim + i) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) v[u] = sl[u] >= 0 ? read_slot(sl[u]) : kEmpty;
+#pragma unroll
+      for (int u = 0; u < U; u++) f(sl[u], v[u]);
+    }
+  }
+
   // ---- row a3: beam + exact max-active (readings R5, R6) ----
   __device__ void select_cutoff() {
     const int tid = threadIdx.x;
@@ -658,22 +695,12 @@ struct Frame {
       __syncthreads();
       const uint32_t prefix = (uint32_t)S.radix_prefix;
       const uint32_t hmask = (shift + 10 >= 32) ? 0u : (0xFFFFFFFFu << (shift + 10));
-      constexpr int U = 4;
-      for (int i0 = 0; i0 < n_claim; i0 += BS * U) {
-        u64 v[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-          const int i = i0 + u * BS + tid;
-          v[u] = i < n_claim ? read_slot((int)(__ldcg(claim + i) & 0x7FFFFFFFu)) : kEmpty;
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-          if (v[u] == kEmpty || !(key_cost(v[u]) < beam_cut)) continue;
-          if (first) cnt++;
-          const uint32_t rk = (uint32_t)(v[u] >> 32) - ob;
-          if ((rk & hmask) == (prefix & hmask)) red_add_s(hist_sa + 4u * ((rk >> shift) & 1023u), 1);
-        }
-      }
+      scan_entries<4>([&](int, u64 v) {
+        if (v == kEmpty || !(key_cost(v) < beam_cut)) return;
+        if (first) cnt++;
+        const uint32_t rk = (uint32_t)(v >> 32) - ob;
+        if ((rk & hmask) == (prefix & hmask)) red_add_s(hist_sa + 4u * ((rk >> shift) & 1023u), 1);
+      });
       if (first) {
         const long long n_in = block_sum64<BS>(cnt, S.warp_tmp64);   // includes a barrier
         if (tid == 0) S.n_in = (int)n_in;
@@ -724,19 +751,14 @@ struct Frame {
   // ---- row a5: epsilon closure under the fixed cutoff (reading R7) ----
   __device__ void eps_closure() {
     const int tid = threadIdx.x;
-    const int n_claim = min(S.n_claim, p.FCAP);
     const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
-    for (int i0 = 0; i0 < n_claim; i0 += BS) {   // warp-uniform trip count (warp_append)
-      const int i = i0 + tid;
-      const uint32_t cl = i < n_claim ? __ldcg(claim + i) : 0u;
-      bool need = false;
-      if (cl & 0x80000000u) {
-        const float c = key_cost(read_slot((int)(cl & 0x7FFFFFFFu)));
-        need = c < cut_b && c <= cut_a;
-      }
+    // seed: kept entries whose state has epsilon arcs (flag in bit 31 of the state word)
+    scan_entries<4>([&](int slot, u64 v) {
+      const float c = key_cost(v);
+      const bool need = v != kEmpty && ((uint32_t)v & 0x80000000u) && c < cut_b && c <= cut_a;
       const int idx = warp_append(need, saddr(&S.n_wl));
-      if (need) wl0[idx] = cl & 0x7FFFFFFFu;
-    }
+      if (need) wl0[idx] = (uint32_t)slot;
+    });
     __syncthreads();
     int cur = 0;
     long long relax = 0;
@@ -755,7 +777,7 @@ struct Frame {
         if (i < n_wl) {
           const u64 v = read_slot((int)__ldcg(W + i));
           cp = key_cost(v);
-          const int4 si = __ldg(p.state_info + (uint32_t)v);
+          const int4 si = __ldg(p.state_info + ((uint32_t)v & 0x7FFFFFFFu));
           e0 = si.y;
           e1 = si.z;
         }
@@ -775,7 +797,7 @@ struct Frame {
             relax++;
             if (c < cut_b && c <= cut_a) {
               const uint32_t o = ord_of(c);
-              const uint32_t q = (uint32_t)arc.x;
+              const uint32_t q = (uint32_t)arc.x | ((uint32_t)arc.w & 0x80000000u);   // state | has-eps
               slot = insert(q, ((u64)o << 32) | q, claimed, logit, strict);
               if (slot >= 0 && logit) red_min_g64(win + slot, ((u64)o << 32) | (uint32_t)(e0 + k));
               if (slot < 0) claimed = strict = false;
@@ -806,7 +828,6 @@ struct Frame {
   // end-of-stream traceback -- nothing per frame has to map states to records.
   __device__ void contract() {
     const int tid = threadIdx.x, lane = tid & 31;
-    const int n_claim = min(S.n_claim, p.FCAP);
     const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
     // bucket range [best, cutoff) for the cost order of the next frontier
     const float bk_ref = float_of_ord(S.best_ord);
@@ -822,49 +843,32 @@ struct Frame {
     float mn = INFINITY;
     constexpr int U = 4;
     // pass 1: drain the tables; survivors -> tmp {state, cost, arc, bucket}
-    for (int i0 = 0; i0 < n_claim; i0 += BS * U) {
-      uint32_t cl[U];
-      u64 v[U], w[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int i = i0 + u * BS + tid;
-        cl[u] = i < n_claim ? __ldcg(claim + i) : 0xFFFFFFFFu;
+    scan_entries<4>([&](int slot, u64 v) {
+      const bool live = v != kEmpty;
+      const float c = key_cost(v);
+      const bool k = live && c < cut_b && c <= cut_a;
+      if (live) clear_slot(slot);
+      u64 w = kEmpty;
+      if (k) w = atomicExch(win + slot, kEmpty);        // read + reset in one transaction
+      else if (live) win[slot] = kEmpty;
+      const int r = warp_append(k, saddr(&S.n_surv));
+      const int bk = k ? (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1))
+                       : kNBuck;
+      {   // warp-aggregated bucket count
+        const unsigned grp = __match_any_sync(0xffffffffu, bk);
+        if (bk < kNBuck && lane == __ffs(grp) - 1) red_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
       }
-#pragma unroll
-      for (int u = 0; u < U; u++) {   // winner word read and reset in one L2 transaction
-        const int slot = (int)(cl[u] & 0x7FFFFFFFu);
-        v[u] = cl[u] != 0xFFFFFFFFu ? read_slot(slot) : kEmpty;
-        w[u] = cl[u] != 0xFFFFFFFFu ? atomicExch(win + slot, kEmpty) : kEmpty;
+      if (!k) return;
+      if (r >= p.FCAP) {
+        S.status = WFST_ERR_CAPACITY;
+        return;
       }
-      bool k[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        if (cl[u] != 0xFFFFFFFFu) clear_slot((int)(cl[u] & 0x7FFFFFFFu));
-        const float c = key_cost(v[u]);
-        k[u] = cl[u] != 0xFFFFFFFFu && c < cut_b && c <= cut_a;
-      }
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int r = warp_append(k[u], saddr(&S.n_surv));
-        const float c = key_cost(v[u]);
-        const int bk = k[u] ? (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1))
-                            : kNBuck;
-        {   // warp-aggregated bucket count
-          const unsigned grp = __match_any_sync(0xffffffffu, bk);
-          if (bk < kNBuck && lane == __ffs(grp) - 1) red_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
-        }
-        if (!k[u]) continue;
-        if (r >= p.FCAP) {
-          S.status = WFST_ERR_CAPACITY;
-          continue;
-        }
-        // the winner word's cost must be the slot's final cost (every improving insert RED's)
-        const int32_t arc = (uint32_t)(w[u] >> 32) == (uint32_t)(v[u] >> 32) ? (int32_t)(uint32_t)w[u] : -2;
-        if (arc == -2) S.status = WFST_ERR_STATE;
-        tmp[r] = make_int4((int)(uint32_t)v[u], __float_as_int(c), arc, bk);
-        mn = fminf(mn, c);
-      }
-    }
+      // the winner word's cost must be the slot's final cost (every improving insert RED's)
+      const int32_t arc = (uint32_t)(w >> 32) == (uint32_t)(v >> 32) ? (int32_t)(uint32_t)w : -2;
+      if (arc == -2) S.status = WFST_ERR_STATE;
+      tmp[r] = make_int4((int)((uint32_t)v & 0x7FFFFFFFu), __float_as_int(c), arc, bk);
+      mn = fminf(mn, c);
+    });
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     if ((tid & 31) == 0) S.warp_tmp[tid >> 5] = __float_as_int(mn);
@@ -934,6 +938,7 @@ struct Frame {
       S.best_ord = 0xFFFFFFFFu;
       S.theta = kNB;
       S.n_claim = 0;
+      S.n_oclaim = 0;
       S.n_ovf = 0;
       S.n_big = 0;
       S.next_group = 0;
@@ -1024,9 +1029,10 @@ struct Frame {
       const uint32_t o = ord_of(0.0f);
       uint32_t flag = 0;
       if (tid == 0) {
-        slot = insert((uint32_t)p.start, ((u64)o << 32) | (uint32_t)p.start, claimed, logit, strict);
         const int4 si = __ldg(p.state_info + p.start);
         flag = si.z > si.y ? 1u : 0u;
+        const uint32_t qf = (uint32_t)p.start | (flag << 31);
+        slot = insert(qf, ((u64)o << 32) | qf, claimed, logit, strict);
         if (slot >= 0) win[slot] = ((u64)o << 32) | 0xFFFFFFFFull;   // the start token (arc -1)
         else claimed = false;
       }
