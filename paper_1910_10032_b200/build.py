@@ -31,6 +31,8 @@ def _stale(obj: str, deps: list[str]) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    if os.environ.get("WFST_NO_BUILD") and os.path.exists(LIB) and not force:
+        return LIB   # A/B experiments swap prebuilt libraries in place
     os.makedirs(BUILD, exist_ok=True)
     jobs = []
     for s in SOURCES:
