@@ -278,6 +278,12 @@ def gpu_arm(args):
         return None
 
     peak, peak_src = _peaks()
+    traffic, traffic_src = args.traffic, None
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if traffic is None and os.path.exists(tpath) and args.config == "c3" and args.preset == "clean":
+        with open(tpath) as f:
+            t = json.load(f)
+        traffic, traffic_src = t["dram_bytes_per_launch"], "profiles/r01_traffic.json (ncu --set full, same launch)"
     frames_per_step = B * T
     abytes = algorithmic_bytes(st, frames_per_step * args.steps, P) / args.steps
     kmean = statistics.mean(kern_ms)
@@ -301,7 +307,7 @@ def gpu_arm(args):
         "decoder_opts": decoder_opts(args),
         "roofline": {"bound": "hbm", "kernel": "frame_kernel", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": args.traffic, "algorithmic_bytes_per_launch": int(abytes),
+                     "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": int(abytes),
                      "kernel_ms": round(kmean, 3), "kernel_share_of_step": round(kmean / (ms_max / args.steps), 3),
                      "peak_source": peak_src},
         "counters_per_step": {k: v / args.steps for k, v in st.items()

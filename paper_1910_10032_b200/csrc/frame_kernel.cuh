@@ -1089,6 +1089,7 @@ struct Frame {
     tick(t0, 11);
     if (tid == 0) S.t_mark = clock64();
     expand();
+    if (tid == 0) t0 = clock64();   // expansion itself is timed by the marks inside expand()
     if (tid == 0 && t_next >= 0) row_issue(row_ptr(t_next));   // overlaps the frame's tail
     tick(t0, 0);
     if (tid == 0) {
