@@ -29,6 +29,7 @@ constexpr int kStage = 32;         // per-warp staging buffer (candidates awaiti
 #define WFST_NBUCK 16
 #endif
 constexpr int kNBuck = WFST_NBUCK; // cost buckets ordering the next frontier
+constexpr int kSmallClaims = 2048; // frames with at most this many claims use an on-chip claim list
 
 struct LaneState {
   int32_t status;       // wfst_status, sticky
@@ -86,7 +87,8 @@ struct SmemCtl {
   float beam_cut, kalpha, ref, inv_w, min_surv;
   int32_t use_alpha;
   int32_t radix_prefix, radix_k;
-  long long emit_arcs, eps_deg, eps_relax;
+  unsigned long long emit_arcs, eps_deg, eps_relax;
+  uint32_t sclaim[kSmallClaims];   // claimed slots while the frame is small
   int32_t warp_tmp[32];
   long long warp_tmp64[32];
   int32_t big[kBigCap];
@@ -146,6 +148,14 @@ __device__ __forceinline__ int atom_add_s(uint32_t a, int v) {
 }
 __device__ __forceinline__ void red_min_s32(uint32_t a, uint32_t v) {
   asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_s64(uint32_t a, unsigned long long v) {
+  asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 __device__ __forceinline__ void red_add_s(uint32_t a, int v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -410,6 +420,8 @@ struct Frame {
     if (lane == leader) base = atom_add_s(saddr(&S.n_claim), __popc(m));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (claimed) {
+      const int ci = base + __popc(m & ((1u << lane) - 1u));
+      if (ci < kSmallClaims) S.sclaim[ci] = (uint32_t)slot;
       if (slot >= p.C) {   // the on-chip table is scanned directly; only overflow slots are listed
         const int oi = atomicAdd(&S.n_oclaim, 1);
         if (oi < p.C_ovf) claim[oi] = (uint32_t)slot;
@@ -624,8 +636,10 @@ struct Frame {
     }
     __syncwarp();
     if (staged > 0) flush(staged, beam, best_sa, theta_sa);
-    arcs_total = block_sum64<BS>(arcs_total, S.warp_tmp64);
-    if (tid == 0) S.emit_arcs = arcs_total;
+    {
+      const unsigned long long wsum = warp_sum64((unsigned long long)arcs_total);
+      if (lane == 0 && wsum) red_add_s64(saddr(&S.emit_arcs), wsum);
+    }
     __syncthreads();
     mark(4);   // hub tokens done
   }
@@ -637,6 +651,23 @@ struct Frame {
   template <int U, typename Fn>
   __device__ __forceinline__ void scan_entries(Fn f) {
     const int tid = threadIdx.x;
+    const int nc = S.n_claim;
+    if (nc <= kSmallClaims) {   // small frame: the on-chip claim list names every live slot
+      for (int i0 = 0; i0 < nc; i0 += BS * U) {
+        int sl[U];
+        u64 v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int i = i0 + u * BS + tid;
+          sl[u] = i < nc ? (int)S.sclaim[i] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) v[u] = sl[u] >= 0 ? read_slot(sl[u]) : kEmpty;
+#pragma unroll
+        for (int u = 0; u < U; u++) f(sl[u], v[u]);
+      }
+      return;
+    }
     for (int i0 = 0; i0 < p.C; i0 += BS * U) {
       u64 v[U];
 #pragma unroll
@@ -818,8 +849,10 @@ struct Frame {
       cur ^= 1;
       __syncthreads();
     }
-    const long long tot = block_sum64<BS>(relax, S.warp_tmp64);
-    if (tid == 0) S.eps_relax = tot;
+    {
+      const unsigned long long wsum = warp_sum64((unsigned long long)relax);
+      if ((tid & 31) == 0 && wsum) red_add_s64(saddr(&S.eps_relax), wsum);
+    }
   }
 
   // ---- rows a4 + a6: contraction into the next frontier (cost-bucketed) + records ----
@@ -926,8 +959,11 @@ struct Frame {
         if (rec_cost) rec_cost[rb + pos[u]] = __int_as_float(t[u].y);
       }
     }
-    const long long eps_deg = block_sum64<BS>(epsd, S.warp_tmp64);   // barriers
-    if (tid == 0) S.eps_deg = eps_deg;
+    {
+      const unsigned long long wsum = warp_sum64((unsigned long long)epsd);
+      if (lane == 0 && wsum) red_add_s64(saddr(&S.eps_deg), wsum);
+    }
+    __syncthreads();
     mark(8);   // placement done
   }
 
@@ -948,6 +984,7 @@ struct Frame {
       S.beam_cut = beam_cut_fixed;
       S.emit_arcs = 0;
       S.eps_relax = 0;
+      S.eps_deg = 0;
       S.n_in = -1;
       const float half = isinf(p.beam) ? 32.0f : 0.5f * p.beam;
       S.ref = S.L.front_best - half;
