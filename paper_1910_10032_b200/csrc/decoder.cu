@@ -288,7 +288,11 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
                                   (size_t)prop.sharedMemPerMultiprocessor / d->ctas_per_sm);
   // the staged log-likelihood row: columns 0..max_pdf (+16 B alignment slack on each side)
   const int row_floats = std::max(g->max_pdf + 1, 1);
+#if WFST_ROWSMEM
   const int row_bytes = (row_floats * 4 + 15) / 16 * 16 + 32;
+#else
+  const int row_bytes = 32;
+#endif
   int C = d->o.table_slots > 0 ? d->o.table_slots
                                : (int)((per_cta - static_smem - (size_t)kNB * 4 - (size_t)row_bytes) / 8);
   C = std::max(64, C / 256 * 256);

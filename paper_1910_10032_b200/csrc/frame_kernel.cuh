@@ -19,7 +19,13 @@ using wfst::kArcNone;
 
 constexpr u64 kEmpty = 0xFFFFFFFFFFFFFFFFull;
 constexpr int kNB = 1024;          // cost bins of the max-active bound
-constexpr int kMaxProbeS = 32;     // buckets probed in the on-chip table before overflowing
+#ifndef WFST_MAXPROBE
+#define WFST_MAXPROBE 32
+#endif
+#ifndef WFST_ROWSMEM
+#define WFST_ROWSMEM 1
+#endif
+constexpr int kMaxProbeS = WFST_MAXPROBE;   // buckets probed in the on-chip table before overflowing
 constexpr int kMaxProbeG = 512;    // buckets probed in the global overflow table
 constexpr int kModeFrames = 0, kModeInit = 1;
 constexpr int kBig = 64;           // tokens with more emitting arcs are expanded CTA-wide
@@ -83,7 +89,7 @@ struct SmemCtl {
   int32_t bucket_base[kNBuck];
   long long t_mark;
   unsigned long long row_mbar;   // mbarrier of the row's bulk copy
-  int32_t row_parity, row_pending, row_off;
+  int32_t row_parity, row_pending, row_off, t_cur;
   float beam_cut, kalpha, ref, inv_w, min_surv;
   int32_t use_alpha;
   int32_t radix_prefix, radix_k;
@@ -366,6 +372,14 @@ struct Frame {
     bulk_g2s(row_sa, (const void*)s, bytes, saddr(&S.row_mbar));
     S.row_pending = 1;
   }
+  const float* rowg;   // the frame's row in global memory (gathers when it is not staged)
+  __device__ __forceinline__ float row_ll(uint32_t rowp, int pdf) const {
+#if WFST_ROWSMEM
+    return __int_as_float(lds32(rowp + 4u * (uint32_t)pdf));
+#else
+    return __ldg(rowg + pdf);
+#endif
+  }
   // all threads: wait for the pending row (caller guarantees one is pending)
   __device__ void row_wait() {
     mbar_wait(saddr(&S.row_mbar), S.row_parity);
@@ -519,6 +533,7 @@ struct Frame {
     const int4* Fin = F0 + (size_t)S.L.cur * p.FCAP;
     const float ref = S.ref, inv_w = S.inv_w, beam = p.beam;
     const uint32_t rowp = row_sa + (uint32_t)S.row_off;
+    rowg = row_ptr(S.t_cur);
     const uint32_t best_sa = saddr(&S.best_ord), theta_sa = saddr(&S.theta);
     long long arcs_total = 0;
     int staged = 0;   // warp-uniform
@@ -581,7 +596,7 @@ struct Frame {
         for (int u = 0; u < R; u++) arc[u] = v[u] ? __ldg(p.arcs + a[u]) : make_int4(0, 0, 0, 0);
         float L[R];
 #pragma unroll
-        for (int u = 0; u < R; u++) L[u] = v[u] ? __int_as_float(lds32(rowp + 4u * (uint32_t)arc[u].z)) : 0.0f;
+        for (int u = 0; u < R; u++) L[u] = v[u] ? row_ll(rowp, arc[u].z) : 0.0f;
         const uint32_t bo = (uint32_t)lds32(best_sa);
         const int th = lds32(theta_sa);
         const float bound = bo == 0xFFFFFFFFu ? INFINITY : __fadd_rn(float_of_ord(bo), beam);
@@ -619,7 +634,7 @@ struct Frame {
         }
         float L[R];
 #pragma unroll
-        for (int u = 0; u < R; u++) L[u] = v[u] ? __int_as_float(lds32(rowp + 4u * (uint32_t)arc[u].z)) : 0.0f;
+        for (int u = 0; u < R; u++) L[u] = v[u] ? row_ll(rowp, arc[u].z) : 0.0f;
         const uint32_t bo = (uint32_t)lds32(best_sa);
         const int th = lds32(theta_sa);
         const float bound = bo == 0xFFFFFFFFu ? INFINITY : __fadd_rn(float_of_ord(bo), beam);
@@ -1119,15 +1134,22 @@ struct Frame {
       return;
     }
     long long t0 = clock64();
+    if (tid == 0) S.t_cur = t;
+#if WFST_ROWSMEM
     if (tid == 0 && !S.row_pending) row_issue(row_ptr(t));   // first frame of a work item
+#endif
     begin_frame(INFINITY);
     tick(t0, 5);
+#if WFST_ROWSMEM
     row_wait();
+#endif
     tick(t0, 11);
     if (tid == 0) S.t_mark = clock64();
     expand();
     if (tid == 0) t0 = clock64();   // expansion itself is timed by the marks inside expand()
+#if WFST_ROWSMEM
     if (tid == 0 && t_next >= 0) row_issue(row_ptr(t_next));   // overlaps the frame's tail
+#endif
     tick(t0, 0);
     if (tid == 0) {
       S.n_claim_emit = S.n_claim;
