@@ -317,7 +317,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     d->R_cap = (int64_t)(d->TMAX / 4 + 1) * per_frame;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-      int64_t per_lane_other = (int64_t)d->FCAP * (32 + 4 + 8 + 16 + 8) + (int64_t)d->C_ovf * 8 +
+      int64_t per_lane_other = (int64_t)d->FCAP * (32 + 4 + 8 + 8) + (int64_t)d->C_ovf * 8 +
                                (int64_t)d->TMAX * 60;
       int64_t budget = (int64_t)(free_b / 2) / n_streams - per_lane_other;
       int64_t cap = budget / (int64_t)(sizeof(int2) + (d->o.debug_costs ? 4 : 0));
@@ -346,7 +346,6 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   size_t i_front = add(L * 2 * FC * sizeof(int4));
   size_t i_claim = add(L * FC * 4);
   size_t i_win = add(L * FC * 8);
-  size_t i_tmp = add(L * FC * sizeof(int4));
   size_t i_ovf = add(L * (size_t)d->C_ovf * 8);
   size_t i_wl = add(L * 2 * FC * 4);
   size_t i_rec = add(L * (size_t)d->R_cap * sizeof(int2));
@@ -389,7 +388,6 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.front = (int4*)(base + parts[i_front].off);
   kp.claim = (uint32_t*)(base + parts[i_claim].off);
   kp.win = (u64*)(base + parts[i_win].off);
-  kp.tmp = (int4*)(base + parts[i_tmp].off);
   kp.ovf = (u64*)(base + parts[i_ovf].off);
   kp.wl = (uint32_t*)(base + parts[i_wl].off);
   kp.rec = (int2*)(base + parts[i_rec].off);

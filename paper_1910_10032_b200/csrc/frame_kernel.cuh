@@ -20,7 +20,7 @@ using wfst::kArcNone;
 constexpr u64 kEmpty = 0xFFFFFFFFFFFFFFFFull;
 constexpr int kNB = 1024;          // cost bins of the max-active bound
 #ifndef WFST_MAXPROBE
-#define WFST_MAXPROBE 32
+#define WFST_MAXPROBE 8
 #endif
 #ifndef WFST_ROWSMEM
 #define WFST_ROWSMEM 1
@@ -71,7 +71,6 @@ struct KParams {
   int4* front;        // [lane][2][FCAP]  {state, cost bits, e_begin, n_emit}, cost-bucketed
   uint32_t* claim;    // [lane][C_ovf]    overflow-table slots claimed this frame
   u64* win;           // [lane][FCAP]     per slot: min (ord(cost) << 32 | canonical arc id)
-  int4* tmp;          // [lane][FCAP]     contraction scratch {state, cost, arc, bucket}
   u64* ovf;           // [lane][C_ovf]    global overflow token table
   uint32_t* wl;       // [lane][2][FCAP]  epsilon worklists (slots)
   int2* rec;          // [lane][R_cap]    traceback records {winning arc (-1: start), state}
@@ -345,7 +344,6 @@ struct Frame {
   int4* F0;           // frontier buffer 0; buffer 1 follows at +FCAP
   uint32_t* claim;
   u64* win;
-  int4* tmp;
   u64* ovf;
   uint32_t* wl0;      // epsilon worklist 0; worklist 1 follows at +FCAP
   int2* rec;
@@ -395,7 +393,6 @@ struct Frame {
     F0 = p.front + L * 2 * FC;
     claim = p.claim + L * (size_t)p.C_ovf;
     win = p.win + L * FC;
-    tmp = p.tmp + L * FC;
     ovf = p.ovf + L * (size_t)p.C_ovf;
     wl0 = p.wl + L * 2 * FC;
     rec = p.rec + L * (size_t)p.R_cap;
@@ -889,33 +886,15 @@ struct Frame {
     }
     __syncthreads();
     float mn = INFINITY;
-    constexpr int U = 4;
-    // pass 1: drain the tables; survivors -> tmp {state, cost, arc, bucket}
+    // pass 1: count the survivors of each cost bucket (the table is only read)
     scan_entries<4>([&](int slot, u64 v) {
-      const bool live = v != kEmpty;
       const float c = key_cost(v);
-      const bool k = live && c < cut_b && c <= cut_a;
-      if (live) clear_slot(slot);
-      u64 w = kEmpty;
-      if (k) w = atomicExch(win + slot, kEmpty);        // read + reset in one transaction
-      else if (live) win[slot] = kEmpty;
-      const int r = warp_append(k, saddr(&S.n_surv));
+      const bool k = v != kEmpty && c < cut_b && c <= cut_a;
       const int bk = k ? (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1))
                        : kNBuck;
-      {   // warp-aggregated bucket count
-        const unsigned grp = __match_any_sync(0xffffffffu, bk);
-        if (bk < kNBuck && lane == __ffs(grp) - 1) red_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
-      }
-      if (!k) return;
-      if (r >= p.FCAP) {
-        S.status = WFST_ERR_CAPACITY;
-        return;
-      }
-      // the winner word's cost must be the slot's final cost (every improving insert RED's)
-      const int32_t arc = (uint32_t)(w >> 32) == (uint32_t)(v >> 32) ? (int32_t)(uint32_t)w : -2;
-      if (arc == -2) S.status = WFST_ERR_STATE;
-      tmp[r] = make_int4((int)((uint32_t)v & 0x7FFFFFFFu), __float_as_int(c), arc, bk);
-      mn = fminf(mn, c);
+      const unsigned grp = __match_any_sync(0xffffffffu, bk);
+      if (bk < kNBuck && lane == __ffs(grp) - 1) red_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
+      if (k) mn = fminf(mn, c);
     });
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -931,51 +910,52 @@ struct Frame {
         S.bucket_base[b] = acc;
         acc += n;
       }
+      S.n_surv = acc;
     }
-    mark(6);   // drain done
+    mark(6);   // counts done
     __syncthreads();
-    const int n_surv = min(S.n_surv, p.FCAP);
+    const int n_surv = S.n_surv;
     const int32_t rb = S.L.rec_used;
-    if ((long long)rb + n_surv > p.R_cap) {
+    if (n_surv > p.FCAP || (long long)rb + n_surv > p.R_cap) {
       if (tid == 0) S.status = WFST_ERR_CAPACITY;
       __syncthreads();
       return;
     }
-    // pass 2: place survivors in cost-bucket order; state records; traceback records
+    // pass 2: drain the tables and place each survivor at its bucket cursor: frontier entry
+    // (with the state's emitting range, prepared for the next frame: P:78) and traceback record
     int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
-    long long epsd = 0;
-    for (int r0 = 0; r0 < n_surv; r0 += BS * U) {   // warp-uniform trip count
-      int4 t[U];
-      int pos[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int r = r0 + u * BS + tid;
-        t[u] = r < n_surv ? __ldcg(tmp + r) : make_int4(-1, 0, -1, kNBuck);
+    unsigned long long epsd = 0;
+    scan_entries<4>([&](int slot, u64 v) {
+      const bool live = v != kEmpty;
+      const float c = key_cost(v);
+      const bool k = live && c < cut_b && c <= cut_a;
+      const int bk = k ? (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1))
+                       : kNBuck;
+      const unsigned grp = __match_any_sync(0xffffffffu, bk);
+      const int leader = __ffs(grp) - 1;
+      int base = 0;
+      if (bk < kNBuck && lane == leader) base = atom_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (!live) return;
+      clear_slot(slot);
+      if (!k) {
+        win[slot] = kEmpty;
+        return;
       }
-#pragma unroll
-      for (int u = 0; u < U; u++) {   // warp-aggregated bucket cursors
-        const int bk = t[u].w;
-        const unsigned grp = __match_any_sync(0xffffffffu, bk);
-        const int leader = __ffs(grp) - 1;
-        int base = 0;
-        if (bk < kNBuck && lane == leader) base = atom_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        pos[u] = base + __popc(grp & ((1u << lane) - 1u));
-      }
-      int4 si[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) si[u] = t[u].x >= 0 ? __ldg(p.state_info + t[u].x) : make_int4(0, 0, 0, 0);
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        if (t[u].x < 0) continue;
-        Fout[pos[u]] = make_int4(t[u].x, t[u].y, si[u].x, si[u].y - si[u].x);
-        epsd += si[u].z - si[u].y;
-        rec[rb + pos[u]] = make_int2(t[u].z, t[u].x);
-        if (rec_cost) rec_cost[rb + pos[u]] = __int_as_float(t[u].y);
-      }
-    }
+      const int pos = base + __popc(grp & ((1u << lane) - 1u));
+      const uint32_t q = (uint32_t)v & 0x7FFFFFFFu;
+      const u64 w = atomicExch(win + slot, kEmpty);   // winner word read + reset in one transaction
+      const int4 si = __ldg(p.state_info + q);
+      // the winner word's cost must be the slot's final cost (every improving insert RED's)
+      const int32_t arc = (uint32_t)(w >> 32) == (uint32_t)(v >> 32) ? (int32_t)(uint32_t)w : -2;
+      if (arc == -2) S.status = WFST_ERR_STATE;
+      Fout[pos] = make_int4((int)q, __float_as_int(c), si.x, si.y - si.x);
+      rec[rb + pos] = make_int2(arc, (int)q);
+      if (rec_cost) rec_cost[rb + pos] = __int_as_float(c);
+      epsd += (unsigned long long)(si.z - si.y);
+    });
     {
-      const unsigned long long wsum = warp_sum64((unsigned long long)epsd);
+      const unsigned long long wsum = warp_sum64(epsd);
       if (lane == 0 && wsum) red_add_s64(saddr(&S.eps_deg), wsum);
     }
     __syncthreads();
