@@ -951,7 +951,7 @@ struct Frame {
       if (arc == -2) S.status = WFST_ERR_STATE;
       Fout[pos] = make_int4((int)q, __float_as_int(c), si.x, si.y - si.x);
       rec[rb + pos] = make_int2(arc, (int)q);
-      if (rec_cost) rec_cost[rb + pos] = __int_as_float(c);
+      if (rec_cost) rec_cost[rb + pos] = c;
       epsd += (unsigned long long)(si.z - si.y);
     });
     {
