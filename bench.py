@@ -203,11 +203,14 @@ def gpu_arm(args):
     ll = device_loglikes(W, torch, wl, dev)
     cap = 4 * T + 64
 
+    chunk = wl["c"].get("chunk") or T   # online configs (C4/C5) arrive in frame chunks
+
     def step(ev=None):
         D.reset()
         if ev is not None:
             ev[0].record()
-        D.decode_frames(ll)
+        for t0 in range(0, T, chunk):
+            D.decode_frames(ll[t0:t0 + chunk] if chunk < T else ll)
         if ev is not None:
             ev[1].record()
         return D.best_paths(cap=cap, raise_on_error=False)
@@ -298,12 +301,13 @@ def gpu_arm(args):
                                f" per GPU, beam {wl['beam']}, max_active {wl['alpha']}, preset {args.preset})",
                    "streams_per_gpu": B, "frames": T, "pdfs": P, "beam": wl["beam"], "max_active": wl["alpha"],
                    "preset": args.preset, "frame_ms": 10, "parallelism": f"streams partitioned over {world} GPU(s)",
-                   "l2": "inputs larger than L2 (log-likelihoods %.2f GB per GPU)" % (T * B * P * 4 / 1e9)},
+                   "l2": "inputs larger than L2 (log-likelihoods %.2f GB per GPU)" % (T * B * P * 4 / 1e9),
+                   "frames_per_call": chunk},
         "rtfx_30ms": round(value * 3, 1),
         "arcs_per_s": round(arcs_all * 1e3 / (ms_max), 1) if ms_max else None,
         "frames_per_s": round(args.steps * frames_per_step * world / (ms_max / 1e3), 1),
         "e2e": e2e,
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": (2 + (T + chunk - 1) // chunk) * args.steps,
         "decoder_opts": decoder_opts(args),
         "roofline": {"bound": "hbm", "kernel": "frame_kernel", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),

@@ -286,3 +286,41 @@ def test_tie_heavy_dyadic(W, torch, oracle_mod):
         D, res = _gpu_run(W, torch, g, ll, beam, alpha)
         for b in range(B):
             _compare(og, ll, beam, alpha, res, b)
+
+
+@pytest.mark.slow
+def test_c4_large_graph_memory_and_chunks(W, torch, oracle_mod):
+    """C4 (BASELINE configs[3]): a large-LM-shaped graph (~50M states / ~150M arcs) and 1024
+    streams decoded in 50-frame chunks.  Checks the device footprint against Eq. 1
+    and sampled streams against the oracle."""
+    c = I.CONFIGS["c4"]
+    g = I.config_graph("c4")
+    T, B, P = 100, c["streams"], c["n_pdfs"]
+    G = W.Graph.from_arrays(g)
+    info = G.info()
+    assert info.n_states == g.n_states and info.n_arcs == g.n_arcs
+    # device layout: 16 B per state + 16 B per arc + 4 B olabel per arc, vs Eq. 1's 12|Q|+8|E|+4|E_E|
+    assert info.device_bytes == 16 * info.n_states + 20 * info.n_arcs
+    assert info.eq1_bytes == 12 * info.n_states + 8 * info.n_arcs + 4 * info.n_emitting
+    pl = I.planted_walks(g, 8, T, seed=c["ll_seed"])
+    D = W.Decoder(G, B, c["beam"], c["max_active"], records_per_stream=T * 12000)
+    ll = torch.empty((T, B, P), dtype=torch.float32, device="cuda")
+    ids = torch.arange(0, B, dtype=torch.int32, device="cuda")
+    plb = np.zeros((T, B), np.int32)
+    plb[:, :8] = pl
+    W.synth_loglikes(ll, ids, 0, c["ll_seed"], torch.from_numpy(plb).cuda(), **I.preset(c["preset"]))
+    D.reset()
+    for t0 in range(0, T, c["chunk"]):
+        D.decode_frames(ll[t0:t0 + c["chunk"]])
+    res = D.best_paths(cap=4 * T + 64)
+    assert res["rc"] == 0
+    st = D.stats()
+    assert st["frames"] == T * B and st["device_bytes"] > 0
+    og = oracle_mod.OracleGraph(g)
+    for b in (0, 3, 7):
+        llh = I.loglikes_stream(c["ll_seed"], b, T, P, pl[:, b], **I.preset(c["preset"]))
+        r = og.decode(llh, c["beam"], c["max_active"])
+        n = res["n_arcs"][b]
+        assert res["reached_final"][b] == r.reached_final
+        assert list(res["arcs"][b, :n]) == list(r.arcs)
+        assert res["cost"][b] == r.cost32
