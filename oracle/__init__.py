@@ -54,6 +54,8 @@ def lib():
         L.oracle_decode.argtypes = [P, P, I64, I32, I32, F32, I32, P, P, P, I32, P, P, I32, P,
                                     P, P, P, P, P, P, I64, P]
         L.oracle_decode_batch.argtypes = [P, P, I32, I32, I32, F32, I32, I32, P, P, P, P, P, I32, P]
+        L.oracle_lattice.argtypes = [P, P, I64, I32, F32, F32, P, P, P, P, P, P, P, P, P, I64, P]
+        L.oracle_lattice_finalize.argtypes = [P, I32, P, P, P, P, P, P, P, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -139,6 +141,51 @@ class OracleGraph:
             res.layers = [(sst[offs[k]:offs[k + 1]].copy(), sar[offs[k]:offs[k + 1]].copy(),
                            sco[offs[k]:offs[k + 1]].copy()) for k in range(T + 1)]
         return res
+
+    def lattice(self, ll: np.ndarray, beam: float, max_active: int, lattice_beam: float,
+                cap: int | None = None) -> OracleResult:
+        """Row f1: decode (survivors kept) + per-frame lattice segments + the end-of-utterance
+        backward sweep (oracle_lattice / oracle_lattice_finalize; readings R13-R14).
+        Returns the decode result with .segments[k] = (arc, src, dst, slack) arrays (grouped by
+        dst, arc ascending), .gamma[k] per token of layer k, .pslack[k] per arc of segment k."""
+        ll = np.ascontiguousarray(ll, dtype=np.float32)
+        T = ll.shape[0]
+        r = self.decode(ll, beam, max_active, survivors=True)
+        sn = np.array([len(L[0]) for L in r.layers], np.int32)
+        sst = np.ascontiguousarray(np.concatenate([L[0] for L in r.layers]).astype(np.int32))
+        sco = np.ascontiguousarray(np.concatenate([L[2] for L in r.layers]).astype(np.float32))
+        fst = np.ascontiguousarray(r.frame_stats if T else np.zeros((1, 3), np.float32))
+        if cap is None:
+            cap = int(max(1, sum(len(L[0]) for L in r.layers) * max(1, self.g.n_arcs // max(1, self.g.n_states)) * 4))
+        seg_n = np.zeros(T + 1, np.int32)
+        la, ls, ld = (np.zeros(cap, np.int32) for _ in range(3))
+        lsl = np.zeros(cap, np.float32)
+        n = np.zeros(1, np.int64)
+        rc = lib().oracle_lattice(self.h, _p(ll) if T else None, ll.shape[1] if T else 0, T, float(beam),
+                                  float(lattice_beam), _p(fst), _p(sn), _p(sst), _p(sco), _p(seg_n),
+                                  _p(la), _p(ls), _p(ld), _p(lsl), cap, _p(n))
+        if rc == 6:
+            return self.lattice(ll, beam, max_active, lattice_beam, cap=int(n[0]) + 1)
+        if rc:
+            raise OracleError(rc, "lattice")
+        m = int(n[0])
+        gamma = np.zeros(max(1, len(sst)), np.float32)
+        pslack = np.zeros(max(1, m), np.float32)
+        best = np.zeros(1, np.float32)
+        reached = np.zeros(1, np.int32)
+        rc = lib().oracle_lattice_finalize(self.h, T, _p(sn), _p(sst), _p(sco), _p(seg_n), _p(la), _p(ls),
+                                           _p(ld), _p(lsl), _p(gamma), _p(pslack), _p(best), _p(reached))
+        if rc:
+            raise OracleError(rc, "lattice_finalize")
+        so = np.concatenate([[0], np.cumsum(seg_n)])
+        lo = np.concatenate([[0], np.cumsum(sn)])
+        r.segments = [(la[so[k]:so[k + 1]].copy(), ls[so[k]:so[k + 1]].copy(), ld[so[k]:so[k + 1]].copy(),
+                       lsl[so[k]:so[k + 1]].copy()) for k in range(T + 1)]
+        r.gamma = [gamma[lo[k]:lo[k + 1]].copy() for k in range(T + 1)]
+        r.pslack = [pslack[so[k]:so[k + 1]].copy() for k in range(T + 1)]
+        r.lattice_best = float(best[0])
+        r.lattice_beam = float(lattice_beam)
+        return r
 
     def decode_batch(self, ll: np.ndarray, beam: float, max_active: int, n_threads: int,
                      arcs_cap: int = 0):

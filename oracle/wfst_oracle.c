@@ -402,6 +402,175 @@ done:
   return rc;
 }
 
+/* ---- row f1 (NEXT): lattice segments and the end-of-utterance lattice ----
+ *
+ * oracle_lattice builds the per-frame lattice segments of one stream (Fig. 1 "Preprocess
+ * Lattice"; "detecting tokens linked to the same FST state, listing them in the
+ * CSR format, designing a unique representative for each FST state, and computing extra costs";
+ * lattice-beam P:146; readings R13-R14 in DESIGN.md).  Its inputs are oracle_decode's outputs for
+ * the same stream: the layers (surv_n, surv_state, surv_cost; each layer sorted by state, its
+ * tokens are the representatives) and fstats (the cutoff of each frame).  Segment k (k = 0: the
+ * initial closure, k = t+1: frame t) lists every arc a such that
+ *   - a is emitting, leaves the token i of layer k-1 and c = (cost_i + w) - L[k-1][pdf], or
+ *     a is non-emitting, leaves the token i of layer k and c = cost_i + w  (R1 arithmetic);
+ *   - c passes frame k's keep() (R5/R6; k = 0: c < fl(0 + beam));
+ *   - s = c - cost_j <= lattice_beam, j the token of dst(a) in layer k (s is the arc's
+ *     forward extra cost; the representative j has the smallest c, so s >= 0).
+ * Soft pruning: only representatives have out-arcs, which is what "leaves the token i"
+ * means.  Output: for k = 0..T, seg_n[k] arcs (arc, i, j, s), grouped by j (CSR order) and by
+ * arc id inside a group; i and j index the layers as output by oracle_decode. */
+typedef struct { int32_t arc, src, dst; float slack; } LArc;
+
+static int cmp_larc(const void *x, const void *y) {
+  const LArc *a = (const LArc *)x, *b = (const LArc *)y;
+  if (a->dst != b->dst) return (a->dst > b->dst) - (a->dst < b->dst);
+  return (a->arc > b->arc) - (a->arc < b->arc);
+}
+
+static int32_t sorted_find(const int32_t *st, int32_t n, int32_t q) {
+  int32_t lo = 0, hi = n - 1;
+  while (lo <= hi) {
+    int32_t m = (lo + hi) / 2;
+    if (st[m] == q) return m;
+    if (st[m] < q) lo = m + 1; else hi = m - 1;
+  }
+  return -1;
+}
+
+int oracle_lattice(void *gp, const float *ll, int64_t ll_stride, int32_t T, float beam,
+                   float lattice_beam, const float *fstats, const int32_t *surv_n,
+                   const int32_t *surv_state, const float *surv_cost, int32_t *seg_n,
+                   int32_t *l_arc, int32_t *l_src, int32_t *l_dst, float *l_slack, int64_t cap,
+                   int64_t *n_total) {
+  const OGraph *g = (const OGraph *)gp;
+  if (!g || T < 0 || !surv_n || !surv_state || !surv_cost || !seg_n || !n_total) return O_INVALID;
+  int64_t *off = (int64_t *)malloc(((size_t)T + 2) * 8);
+  if (!off) return O_OOM;
+  off[0] = 0;
+  for (int32_t k = 0; k <= T; k++) off[k + 1] = off[k] + surv_n[k];
+  int rc = O_OK;
+  int64_t out = 0;
+  for (int32_t k = 0; k <= T && rc == O_OK; k++) {
+    Keep kp = {0.0f + beam, INFINITY, 0};
+    if (k > 0) {
+      kp.beam_cut = fstats[3 * (k - 1) + 1];
+      kp.kalpha = fstats[3 * (k - 1) + 2];
+      kp.use_alpha = kp.kalpha < INFINITY;
+    }
+    const int32_t *st_k = surv_state + off[k];
+    const float *co_k = surv_cost + off[k];
+    const int32_t n_k = surv_n[k];
+    /* candidate arcs: emitting from layer k-1, then non-emitting from layer k */
+    int64_t n_cand = 0;
+    if (k > 0)
+      for (int32_t i = 0; i < surv_n[k - 1]; i++) n_cand += g->n_emit[surv_state[off[k - 1] + i]];
+    for (int32_t i = 0; i < n_k; i++) {
+      int32_t p = st_k[i];
+      n_cand += (g->first[p + 1] - g->first[p]) - g->n_emit[p];
+    }
+    LArc *buf = (LArc *)malloc((size_t)(n_cand ? n_cand : 1) * sizeof(LArc));
+    if (!buf) { rc = O_OOM; break; }
+    int64_t nb = 0;
+    for (int pass = 0; pass < 2 && rc == O_OK; pass++) {
+      if (pass == 0 && k == 0) continue;
+      const int32_t *st_s = pass == 0 ? surv_state + off[k - 1] : st_k;
+      const float *co_s = pass == 0 ? surv_cost + off[k - 1] : co_k;
+      const int32_t n_s = pass == 0 ? surv_n[k - 1] : n_k;
+      const float *row = pass == 0 ? ll + (int64_t)(k - 1) * ll_stride : NULL;
+      for (int32_t i = 0; i < n_s; i++) {
+        int32_t p = st_s[i];
+        int64_t a0 = pass == 0 ? g->first[p] : g->first[p] + g->n_emit[p];
+        int64_t a1 = pass == 0 ? g->first[p] + g->n_emit[p] : g->first[p + 1];
+        for (int64_t a = a0; a < a1; a++) {
+          float c = pass == 0 ? (co_s[i] + g->weight[a]) - row[g->ilabel[a] - 1] : co_s[i] + g->weight[a];
+          if (!keep(&kp, c)) continue;
+          int32_t j = sorted_find(st_k, n_k, g->dst[a]);
+          if (j < 0) { rc = O_INVALID; break; }   /* a kept candidate must have a kept dst */
+          float s = c - co_k[j];
+          if (!(s <= lattice_beam)) continue;
+          LArc e = {(int32_t)a, i, j, s};
+          buf[nb++] = e;
+        }
+      }
+    }
+    if (rc == O_OK) {
+      qsort(buf, (size_t)nb, sizeof(LArc), cmp_larc);
+      for (int64_t m = 0; m < nb; m++, out++) {
+        if (out >= cap) continue;
+        l_arc[out] = buf[m].arc; l_src[out] = buf[m].src; l_dst[out] = buf[m].dst;
+        l_slack[out] = buf[m].slack;
+      }
+      seg_n[k] = (int32_t)nb;
+    }
+    free(buf);
+  }
+  free(off);
+  *n_total = out;
+  if (rc == O_OK && out > cap) rc = O_CAPACITY;
+  return rc;
+}
+
+/* End of utterance ("moved to the host and used to generate the final lattice at the end
+ * of utterance"; reading R14).  gamma(j) = the slack of the best complete path through token j:
+ *   last layer T: gamma(j) = (cost_j + F(q_j)) - best   (reached_final; +inf for non-final q_j)
+ *                 gamma(j) = cost_j - best               (no final survivor, R10)
+ *   else          gamma(i) = min over lattice arcs a leaving i of  s_a + gamma(dst(a)),
+ * emitting arcs into layer k+1 first, then the epsilon arcs inside layer k to a fixed point
+ * (Bellman-Ford; epsilon arcs of a layer may form positive cycles).  An arc's path slack is
+ * s_a + gamma(dst(a)); the final lattice keeps the arcs with path slack <= lattice_beam.
+ * In: the segments of oracle_lattice (seg_n, l_arc, l_src, l_dst, l_slack), the layers.
+ * Out: gamma[sum surv_n] per token, pslack[n arcs] per arc, *best. */
+int oracle_lattice_finalize(void *gp, int32_t T, const int32_t *surv_n, const int32_t *surv_state,
+                            const float *surv_cost, const int32_t *seg_n, const int32_t *l_arc,
+                            const int32_t *l_src, const int32_t *l_dst, const float *l_slack,
+                            float *gamma, float *pslack, float *best_out, int32_t *reached_out) {
+  const OGraph *g = (const OGraph *)gp;
+  if (!g || T < 0 || !surv_n || !seg_n || !gamma || !pslack) return O_INVALID;
+  int64_t *off = (int64_t *)malloc(((size_t)T + 2) * 8), *soff = (int64_t *)malloc(((size_t)T + 2) * 8);
+  if (!off || !soff) { free(off); free(soff); return O_OOM; }
+  off[0] = soff[0] = 0;
+  for (int32_t k = 0; k <= T; k++) { off[k + 1] = off[k] + surv_n[k]; soff[k + 1] = soff[k] + seg_n[k]; }
+  /* best (R10) */
+  const int64_t lt = off[T];
+  float best = INFINITY;
+  int reached = 0;
+  for (int32_t j = 0; j < surv_n[T]; j++) {
+    float F = g->final[surv_state[lt + j]];
+    if (F < INFINITY) { float c = surv_cost[lt + j] + F; if (!reached || c < best) best = c; reached = 1; }
+  }
+  if (!reached)
+    for (int32_t j = 0; j < surv_n[T]; j++) if (surv_cost[lt + j] < best) best = surv_cost[lt + j];
+  for (int64_t m = 0; m < off[T + 1]; m++) gamma[m] = INFINITY;
+  for (int32_t j = 0; j < surv_n[T]; j++) {
+    float F = g->final[surv_state[lt + j]];
+    if (reached) gamma[lt + j] = F < INFINITY ? (surv_cost[lt + j] + F) - best : INFINITY;
+    else gamma[lt + j] = surv_cost[lt + j] - best;
+  }
+  for (int32_t k = T; k >= 0; k--) {
+    if (k < T)   /* emitting arcs of segment k+1 leave layer k */
+      for (int64_t m = soff[k + 1]; m < soff[k + 2]; m++) {
+        if (g->ilabel[l_arc[m]] == 0) continue;
+        float v = l_slack[m] + gamma[off[k + 1] + l_dst[m]];
+        if (v < gamma[off[k] + l_src[m]]) gamma[off[k] + l_src[m]] = v;
+      }
+    int changed = 1;   /* epsilon arcs of segment k stay inside layer k */
+    while (changed) {
+      changed = 0;
+      for (int64_t m = soff[k]; m < soff[k + 1]; m++) {
+        if (g->ilabel[l_arc[m]] != 0) continue;
+        float v = l_slack[m] + gamma[off[k] + l_dst[m]];
+        if (v < gamma[off[k] + l_src[m]]) { gamma[off[k] + l_src[m]] = v; changed = 1; }
+      }
+    }
+  }
+  for (int32_t k = 0; k <= T; k++)
+    for (int64_t m = soff[k]; m < soff[k + 1]; m++) pslack[m] = l_slack[m] + gamma[off[k] + l_dst[m]];
+  if (best_out) *best_out = best;
+  if (reached_out) *reached_out = reached;
+  free(off); free(soff);
+  return O_OK;
+}
+
 /* ---- multi-core driver for cpu_baseline: streams split over pthreads ---- */
 typedef struct {
   void *g; const float *ll; int64_t ll_stride; int32_t T, P; float beam; int32_t max_active;
