@@ -12,8 +12,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libwfst_gpu.so")
+BUILD = os.path.join(HERE, "_build" + ("_" + os.environ["WFST_BUILD_TAG"] if os.environ.get("WFST_BUILD_TAG") else ""))
+LIB = os.environ.get("WFST_LIB_OUT") or os.path.join(HERE, "libwfst_gpu.so")
 SOURCES = ["graph.cu", "decoder.cu", "synth.cu"]
 HEADERS = [os.path.join(ROOT, "include", "wfst_gpu.h"), os.path.join(CSRC, "wfst_internal.h"),
            os.path.join(CSRC, "frame_kernel.cuh")]
@@ -21,6 +21,8 @@ NVCC = os.environ.get("NVCC", "nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "--fmad=false",
          "-I", os.path.join(ROOT, "include")]
+# experiment builds: extra -D macros (e.g. WFST_DEFS="-DWFST_RHUB=8"), output to WFST_LIB_OUT
+FLAGS += os.environ.get("WFST_DEFS", "").split()
 
 
 def _stale(obj: str, deps: list[str]) -> bool:

@@ -185,6 +185,7 @@ struct wfst_decoder_s {
   int32_t C = 0, C_ovf = 0, FCAP = 0, TMAX = 0, row_floats = 0, row_bytes = 0;
   int64_t R_cap = 0;
   int n_sm = 0, threads = 512, ctas_per_sm = 1;
+  int n_scratch = 0;   // persistent CTAs (= per-CTA scratch sets)
   const WfstVariant* variant = nullptr;
   size_t smem_bytes = 0;
   KParams kp{};
@@ -233,7 +234,7 @@ const WfstVariant* find_variant(int bs, int ctas) {
 }
 
 cudaError_t launch_frames(wfst_decoder_t d, KParams kp, cudaStream_t st) {
-  int grid = std::min(kp.n_items, d->o.max_ctas > 0 ? d->o.max_ctas : d->n_sm * d->ctas_per_sm);
+  int grid = std::min(kp.n_items, d->n_scratch);
   if (grid <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(kp.q_head, 0, sizeof(int32_t), st);
   if (e != cudaSuccess) return e;
@@ -276,6 +277,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   }
   d->n_sm = prop.multiProcessorCount;
   d->ctas_per_sm = d->o.ctas_per_sm > 0 ? d->o.ctas_per_sm : 1;
+  d->n_scratch = d->o.max_ctas > 0 ? d->o.max_ctas : d->n_sm * d->ctas_per_sm;
   d->threads = d->o.threads > 0 ? d->o.threads : (d->ctas_per_sm == 1 ? 1024 : 256);
   d->variant = find_variant(d->threads, d->ctas_per_sm);
   if (!d->variant) {
@@ -317,8 +319,8 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     d->R_cap = (int64_t)(d->TMAX / 4 + 1) * per_frame;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-      int64_t per_lane_other = (int64_t)d->FCAP * (32 + 4 + 8 + 8) + (int64_t)d->C_ovf * 8 +
-                               (int64_t)d->TMAX * 60;
+      int64_t per_lane_other = (int64_t)d->FCAP * 32 + (int64_t)d->TMAX * 60 +
+                               ((int64_t)d->FCAP * (4 + 8 + 8) + (int64_t)d->C_ovf * 8) * d->n_scratch / n_streams;
       int64_t budget = (int64_t)(free_b / 2) / n_streams - per_lane_other;
       int64_t cap = budget / (int64_t)(sizeof(int2) + (d->o.debug_costs ? 4 : 0));
       if (cap < d->R_cap) d->R_cap = std::max<int64_t>(cap, per_frame);
@@ -344,10 +346,14 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     return parts.size() - 1;
   };
   size_t i_front = add(L * 2 * FC * sizeof(int4));
-  size_t i_claim = add(L * FC * 4);
-  size_t i_win = add(L * FC * 8);
-  size_t i_ovf = add(L * (size_t)d->C_ovf * 8);
-  size_t i_wl = add(L * 2 * FC * 4);
+  // intra-frame scratch (claim list, winner words, overflow table, epsilon worklists) is reset
+  // by the end of every frame, so it belongs to the persistent CTA, not to the lane: its
+  // working set stays L2-resident however many lanes there are
+  const size_t NS = (size_t)d->n_scratch;
+  size_t i_claim = add(NS * FC * 4);
+  size_t i_win = add(NS * FC * 8);
+  size_t i_ovf = add(NS * (size_t)d->C_ovf * 8);
+  size_t i_wl = add(NS * 2 * FC * 4);
   size_t i_rec = add(L * (size_t)d->R_cap * sizeof(int2));
   size_t i_rcost = d->o.debug_costs ? add(L * (size_t)d->R_cap * 4) : (size_t)-1;
   size_t i_fst = add(L * (size_t)d->TMAX * 3 * 4);

@@ -69,10 +69,11 @@ struct KParams {
   int32_t TMAX;
   LaneState* lanes_st;
   int4* front;        // [lane][2][FCAP]  {state, cost bits, e_begin, n_emit}, cost-bucketed
-  uint32_t* claim;    // [lane][C_ovf]    overflow-table slots claimed this frame
-  u64* win;           // [lane][FCAP]     per slot: min (ord(cost) << 32 | canonical arc id)
-  u64* ovf;           // [lane][C_ovf]    global overflow token table
-  uint32_t* wl;       // [lane][2][FCAP]  epsilon worklists (slots)
+  uint32_t* claim;    // [cta][C_ovf]     overflow-table slots claimed this frame
+                      // (claim, win, ovf, wl: one set per persistent CTA, reset by the end of every frame)
+  u64* win;           // [cta][FCAP]      per slot: min (ord(cost) << 32 | canonical arc id)
+  u64* ovf;           // [cta][C_ovf]     global overflow token table
+  uint32_t* wl;       // [cta][2][FCAP]   epsilon worklists (slots)
   int2* rec;          // [lane][R_cap]    traceback records {winning arc (-1: start), state}
   float* rec_cost;    // [lane][R_cap]    (debug) survivor cost
   float* fstats;      // [lane][TMAX][3]
@@ -388,13 +389,16 @@ struct Frame {
     }
   }
 
+  __device__ void bind_scratch() {   // intra-frame scratch of this persistent CTA
+    const size_t X = (size_t)blockIdx.x, FC = (size_t)p.FCAP;
+    claim = p.claim + X * (size_t)p.C_ovf;
+    win = p.win + X * FC;
+    ovf = p.ovf + X * (size_t)p.C_ovf;
+    wl0 = p.wl + X * 2 * FC;
+  }
   __device__ void bind(int lane) {
     const size_t L = (size_t)lane, FC = (size_t)p.FCAP;
     F0 = p.front + L * 2 * FC;
-    claim = p.claim + L * (size_t)p.C_ovf;
-    win = p.win + L * FC;
-    ovf = p.ovf + L * (size_t)p.C_ovf;
-    wl0 = p.wl + L * 2 * FC;
     rec = p.rec + L * (size_t)p.R_cap;
     rec_cost = p.rec_cost ? p.rec_cost + L * (size_t)p.R_cap : nullptr;
   }
@@ -661,7 +665,7 @@ struct Frame {
   // is called by every lane with value == kEmpty for empty/out-of-range positions, U entries
   // per lane per step so the loads overlap (warp-collective callbacks are allowed).
   template <int U, typename Fn>
-  __device__ __forceinline__ void scan_entries(Fn f) {
+  __device__ __forceinline__ void scan_batches(Fn f) {
     const int tid = threadIdx.x;
     const int nc = S.n_claim;
     if (nc <= kSmallClaims) {   // small frame: the on-chip claim list names every live slot
@@ -675,20 +679,19 @@ struct Frame {
         }
 #pragma unroll
         for (int u = 0; u < U; u++) v[u] = sl[u] >= 0 ? read_slot(sl[u]) : kEmpty;
-#pragma unroll
-        for (int u = 0; u < U; u++) f(sl[u], v[u]);
+        f(sl, v);
       }
       return;
     }
     for (int i0 = 0; i0 < p.C; i0 += BS * U) {
+      int sl[U];
       u64 v[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        const int i = i0 + u * BS + tid;
-        v[u] = i < p.C ? lds64(tab_sa + 8u * (uint32_t)i) : kEmpty;
+        sl[u] = i0 + u * BS + tid;
+        v[u] = sl[u] < p.C ? lds64(tab_sa + 8u * (uint32_t)sl[u]) : kEmpty;
       }
-#pragma unroll
-      for (int u = 0; u < U; u++) f(i0 + u * BS + tid, v[u]);
+      f(sl, v);
     }
     const int no = min(S.n_oclaim, p.C_ovf);
     for (int i0 = 0; i0 < no; i0 += BS * U) {
@@ -701,9 +704,19 @@ struct Frame {
       }
 #pragma unroll
       for (int u = 0; u < U; u++) v[u] = sl[u] >= 0 ? read_slot(sl[u]) : kEmpty;
+      f(sl, v);
+    }
+  }
+  // Visit every live token-table entry: the on-chip table is scanned directly (strided, so a
+  // warp reads consecutive slots), then the overflow slots listed this frame.  f(slot, value)
+  // is called by every lane with value == kEmpty for empty/out-of-range positions, U entries
+  // per lane per step so the loads overlap (warp-collective callbacks are allowed).
+  template <int U, typename Fn>
+  __device__ __forceinline__ void scan_entries(Fn f) {
+    scan_batches<U>([&](const int* sl, const u64* v) {
 #pragma unroll
       for (int u = 0; u < U; u++) f(sl[u], v[u]);
-    }
+    });
   }
 
   // ---- row a3: beam + exact max-active (readings R5, R6) ----
@@ -925,34 +938,47 @@ struct Frame {
     // (with the state's emitting range, prepared for the next frame: P:78) and traceback record
     int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
     unsigned long long epsd = 0;
-    scan_entries<4>([&](int slot, u64 v) {
-      const bool live = v != kEmpty;
-      const float c = key_cost(v);
-      const bool k = live && c < cut_b && c <= cut_a;
-      const int bk = k ? (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1))
-                       : kNBuck;
-      const unsigned grp = __match_any_sync(0xffffffffu, bk);
-      const int leader = __ffs(grp) - 1;
-      int base = 0;
-      if (bk < kNBuck && lane == leader) base = atom_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (!live) return;
-      clear_slot(slot);
-      if (!k) {
-        win[slot] = kEmpty;
-        return;
+    constexpr int U2 = 2;
+    scan_batches<U2>([&](const int* sl, const u64* v) {
+      int pos[U2];
+      u64 w[U2];
+      int4 si[U2];
+#pragma unroll
+      for (int u = 0; u < U2; u++) {   // placement + every global round trip issued up front
+        const bool live = v[u] != kEmpty;
+        const float c = key_cost(v[u]);
+        const bool k = live && c < cut_b && c <= cut_a;
+        const int bk = k ? (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1))
+                         : kNBuck;
+        const unsigned grp = __match_any_sync(0xffffffffu, bk);
+        const int leader = __ffs(grp) - 1;
+        int base = 0;
+        if (bk < kNBuck && lane == leader) base = atom_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        pos[u] = k ? base + __popc(grp & ((1u << lane) - 1u)) : (live ? -1 : -2);
+        if (live) clear_slot(sl[u]);
+        w[u] = kEmpty;
+        si[u] = make_int4(0, 0, 0, 0);
+        if (k) {
+          w[u] = atomicExch(win + sl[u], kEmpty);   // winner word read + reset in one transaction
+          si[u] = __ldg(p.state_info + ((uint32_t)v[u] & 0x7FFFFFFFu));
+        } else if (live) {
+          win[sl[u]] = kEmpty;
+        }
       }
-      const int pos = base + __popc(grp & ((1u << lane) - 1u));
-      const uint32_t q = (uint32_t)v & 0x7FFFFFFFu;
-      const u64 w = atomicExch(win + slot, kEmpty);   // winner word read + reset in one transaction
-      const int4 si = __ldg(p.state_info + q);
-      // the winner word's cost must be the slot's final cost (every improving insert RED's)
-      const int32_t arc = (uint32_t)(w >> 32) == (uint32_t)(v >> 32) ? (int32_t)(uint32_t)w : -2;
-      if (arc == -2) S.status = WFST_ERR_STATE;
-      Fout[pos] = make_int4((int)q, __float_as_int(c), si.x, si.y - si.x);
-      rec[rb + pos] = make_int2(arc, (int)q);
-      if (rec_cost) rec_cost[rb + pos] = c;
-      epsd += (unsigned long long)(si.z - si.y);
+#pragma unroll
+      for (int u = 0; u < U2; u++) {
+        if (pos[u] < 0) continue;
+        const uint32_t q = (uint32_t)v[u] & 0x7FFFFFFFu;
+        const float c = key_cost(v[u]);
+        // the winner word's cost must be the slot's final cost (every improving insert RED's)
+        const int32_t arc = (uint32_t)(w[u] >> 32) == (uint32_t)(v[u] >> 32) ? (int32_t)(uint32_t)w[u] : -2;
+        if (arc == -2) S.status = WFST_ERR_STATE;
+        Fout[pos[u]] = make_int4((int)q, __float_as_int(c), si[u].x, si[u].y - si[u].x);
+        rec[rb + pos[u]] = make_int2(arc, (int)q);
+        if (rec_cost) rec_cost[rb + pos[u]] = c;
+        epsd += (unsigned long long)(si[u].z - si[u].y);
+      }
     });
     {
       const unsigned long long wsum = warp_sum64(epsd);
@@ -1177,6 +1203,7 @@ __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
   }
   __syncthreads();
   Frame<BS, R> fr(p, S, tab_sa, hist, s_wbuf + (tid & ~31), saddr(s_stage + (tid >> 5) * kStage), saddr(rowmem));
+  fr.bind_scratch();
   while (true) {
     if (tid == 0) S.item = atomicAdd(p.q_head, 1);
     __syncthreads();
