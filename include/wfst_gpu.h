@@ -86,6 +86,9 @@ typedef struct {
   int32_t debug_costs;       /* 1: also keep each survivor's cost (wfst_debug_layer)              */
   int32_t ctas_per_sm;       /* resident lanes per SM (1-4; default 1); the on-chip table is sized
                                 from the SM's shared memory divided by this                       */
+  int32_t lattice;           /* 1: build lattice segments every frame (row f1)    */
+  float lattice_beam;        /* lattice-beam (P:146 uses 8) when lattice = 1; may be 0 or +INF     */
+  int64_t lattice_arcs_per_stream; /* segment arena per stream (default 4 x records_per_stream)   */
 } wfst_decoder_opts_t;
 
 typedef struct {
@@ -193,6 +196,37 @@ wfst_status wfst_decoder_frame_stats(wfst_decoder_t d, int32_t stream, float* fs
  * arc (-1 = start token), cost (only if opts.debug_costs, else NaN).  Order unspecified. */
 wfst_status wfst_debug_layer(wfst_decoder_t d, int32_t stream, int32_t layer, int32_t* states,
                              int32_t* arcs, float* costs, int32_t cap, int32_t* n);
+
+/* ---- lattice (row f1 of SURVEY §8, NEXT) ----------------
+ * With opts.lattice = 1 every reset and decode call also builds, per stream and frame, the lattice
+ * segment of that frame (one extra launch after the frame kernel, same CUDA stream): every arc
+ * that leaves a representative token (P:139 soft pruning), passes the frame's cutoff and whose
+ * extra cost s = c - cost(representative of dst) is <= lattice_beam, listed in CSR order by
+ * destination token, arc id ascending inside a group ("listing them in the CSR format",
+ * "computing extra costs").  Readings R13-R14 of DESIGN.md.
+ *
+ * wfst_get_lattice runs the end-of-utterance backward sweep on the device ("used to generate
+ * the final lattice at the end of utterance"): gamma(token) = slack of the best complete path
+ * through it (R10 best: final states if any survive), pslack(arc) = s + gamma(dst).  The final
+ * lattice is the set of arcs with pslack <= lattice_beam.  The sweep and the device->host copies
+ * run on the decoder's copy stream after the lane's last lattice launch: the compute stream is
+ * NOT synchronised, so other lanes keep decoding (the lane itself must not be decoded further
+ * until the call returns).
+ * Outputs (host, caller-owned; layer k = 0..T, T = frames decoded):
+ *   seg_n[k]                  arcs of segment k (layers_cap entries; *n_layers = T + 1)
+ *   arc/src/dst/slack/pslack  concatenated segments (arcs_cap entries; *n_arcs total): canonical
+ *                             arc id; src = token index in layer k-1 (emitting arc) or layer k
+ *                             (epsilon arc); dst = token index in layer k; token indices are the
+ *                             positions of wfst_debug_layer's output.  pslack nullable.
+ *   gamma                     per token, layers concatenated (gamma_cap; *n_tokens); nullable
+ *   best, reached_final       the best complete cost and whether it ends in a final state (R10)
+ * Errors: INVALID_ARG (lattice off, bad stream, a cap too small: the sizes are still written),
+ * STATE (stream not reset), CAPACITY (the segment arena or records overflowed), or the lane's
+ * sticky decode error. */
+wfst_status wfst_get_lattice(wfst_decoder_t d, int32_t stream, int32_t* seg_n, int32_t layers_cap,
+                             int32_t* n_layers, int32_t* arc, int32_t* src, int32_t* dst, float* slack,
+                             float* pslack, int64_t arcs_cap, int64_t* n_arcs, float* gamma,
+                             int64_t gamma_cap, int64_t* n_tokens, float* best, int32_t* reached_final);
 
 /* ---- synthetic inputs (not part of the method) ------------------------------ */
 

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "frame_kernel.cuh"
+#include "lattice_kernel.cuh"
 #include "wfst_internal.h"
 
 using namespace wfst;
@@ -202,6 +203,20 @@ struct wfst_decoder_s {
   size_t stage_bytes = 0;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_use[2] = {nullptr, nullptr};
+  // lattice (row f1)
+  bool lattice = false;
+  int64_t S_cap = 0;
+  int lat_grid = 0;
+  size_t lat_smem = 0;
+  LatParams lp{};
+  float* kp_pslack = nullptr;
+  uint32_t* kp_gamma = nullptr;
+  int32_t* d_lat_q = nullptr;       // work-queue head of the lattice launch
+  int32_t* d_lat_lane = nullptr;    // lane id of the finalize launch
+  float* d_lat_out = nullptr;       // finalize outputs {best, reached, status}
+  cudaEvent_t ev_lat = nullptr;     // after the last lattice launch (compute stream)
+  void* h_lat_stage = nullptr;      // pinned D2H staging
+  size_t h_lat_bytes = 0;
   std::vector<int32_t> h_initialized;
   std::vector<int32_t> cur_ids;    // mapping currently in d_lane_ids
   int64_t device_bytes = 0;
@@ -242,6 +257,40 @@ cudaError_t launch_frames(wfst_decoder_t d, KParams kp, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   d->variant->launch(grid, d->smem_bytes, st, kp);
   return cudaGetLastError();
+}
+
+// a lane starts a new utterance: its lattice arena and status restart
+__global__ void lat_reset_kernel(const int32_t* lanes, int32_t n, unsigned long long* cursor, int32_t* status) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    cursor[lanes[i]] = 0;
+    status[lanes[i]] = WFST_OK;
+  }
+}
+
+// row f1: the lattice segments of the layers the last frame-kernel launch produced
+cudaError_t launch_lattice(wfst_decoder_t d, const float* ll, int32_t T, int32_t B, int32_t P, int mode,
+                           cudaStream_t st) {
+  LatParams lp = d->lp;
+  lp.ll = ll;
+  lp.T = T;
+  lp.B = B;
+  lp.P = P;
+  lp.lanes = d->d_lane_ids;
+  lp.mode = mode;
+  lp.n_items = mode == kModeInit ? B : T * B;
+  lp.q_head = d->d_lat_q;
+  cudaError_t e = cudaSuccess;
+  if (mode == kModeInit) {
+    lat_reset_kernel<<<(B + 255) / 256, 256, 0, st>>>(d->d_lane_ids, B, lp.seg_cursor, lp.lat_status);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemsetAsync(d->d_lat_q, 0, 4, st);
+  if (e != cudaSuccess) return e;
+  lattice_kernel<1024><<<std::min(d->lat_grid, lp.n_items), 1024, d->lat_smem, st>>>(lp);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaEventRecord(d->ev_lat, st);
+  return e;
 }
 
 size_t smem_for(int C, int row_bytes) { return (size_t)C * 8 + (size_t)kNB * 4 + (size_t)row_bytes; }
@@ -322,7 +371,11 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
       int64_t per_lane_other = (int64_t)d->FCAP * 32 + (int64_t)d->TMAX * 60 +
                                ((int64_t)d->FCAP * (4 + 8 + 8) + (int64_t)d->C_ovf * 8) * d->n_scratch / n_streams;
       int64_t budget = (int64_t)(free_b / 2) / n_streams - per_lane_other;
-      int64_t cap = budget / (int64_t)(sizeof(int2) + (d->o.debug_costs ? 4 : 0));
+      // bytes per record: {arc, state} (+ cost with debug_costs or lattice, + gamma and 4 arena
+      // entries of 20 B with lattice)
+      int64_t per_rec = (int64_t)sizeof(int2) + (d->o.debug_costs || d->o.lattice ? 4 : 0) +
+                        (d->o.lattice ? 4 + 4 * 20 : 0);
+      int64_t cap = budget / per_rec;
       if (cap < d->R_cap) d->R_cap = std::max<int64_t>(cap, per_frame);
     }
   }
@@ -355,7 +408,27 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   size_t i_ovf = add(NS * (size_t)d->C_ovf * 8);
   size_t i_wl = add(NS * 2 * FC * 4);
   size_t i_rec = add(L * (size_t)d->R_cap * sizeof(int2));
-  size_t i_rcost = d->o.debug_costs ? add(L * (size_t)d->R_cap * 4) : (size_t)-1;
+  d->lattice = d->o.lattice != 0;
+  if (d->lattice) {
+    d->S_cap = d->o.lattice_arcs_per_stream > 0 ? d->o.lattice_arcs_per_stream : 4 * d->R_cap;
+    if (!(d->o.lattice_beam >= 0.0f)) {
+      delete d;
+      return fail(WFST_ERR_INVALID_ARG, "lattice_beam must be >= 0 (may be +inf)");
+    }
+  }
+  size_t i_rcost = (d->o.debug_costs || d->lattice) ? add(L * (size_t)d->R_cap * 4) : (size_t)-1;
+  // lattice: arena {arc, src, dst, slack} + path slack per entry, cursor, segment index, status,
+  // gamma per record; fallback token maps of the lattice CTAs for layers beyond shared memory
+  const size_t NLAT = d->lattice ? (size_t)d->n_sm : 0;
+  const int64_t lat_gcap = 2 * (int64_t)d->FCAP + 32;
+  size_t i_seg = d->lattice ? add(L * (size_t)d->S_cap * sizeof(int4)) : 0;
+  size_t i_psl = d->lattice ? add(L * (size_t)d->S_cap * 4) : 0;
+  size_t i_scur = d->lattice ? add(L * 8) : 0;
+  size_t i_sidx = d->lattice ? add(L * (size_t)(d->TMAX + 1) * sizeof(int2)) : 0;
+  size_t i_lst = d->lattice ? add(L * 4) : 0;
+  size_t i_gam = d->lattice ? add(L * (size_t)d->R_cap * 4) : 0;
+  size_t i_gtab = d->lattice ? add(NLAT * (size_t)lat_gcap * 8) : 0;
+  size_t i_gcnt = d->lattice ? add(NLAT * (size_t)d->FCAP * 4) : 0;
   size_t i_fst = add(L * (size_t)d->TMAX * 3 * 4);
   size_t i_fcn = add(L * (size_t)d->TMAX * 5 * 8);
   size_t i_linfo = add(L * (size_t)(d->TMAX + 1) * sizeof(int2));
@@ -403,6 +476,45 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.layer_info = (int2*)(base + parts[i_linfo].off);
   kp.q_head = d->d_qhead;
   kp.lane_round = d->d_round;
+  if (d->lattice) {
+    LatParams& lp = d->lp;
+    lp.state_info = g->d_state;
+    lp.arcs = g->d_arcs;
+    lp.beam = beam;
+    lp.lattice_beam = d->o.lattice_beam;
+    lp.lanes_st = d->d_lanes;
+    lp.rec = kp.rec;
+    lp.rec_cost = kp.rec_cost;
+    lp.R_cap = d->R_cap;
+    lp.layer_info = kp.layer_info;
+    lp.TMAX = d->TMAX;
+    lp.fstats = kp.fstats;
+    lp.seg = (int4*)(base + parts[i_seg].off);
+    lp.S_cap = d->S_cap;
+    lp.seg_cursor = (unsigned long long*)(base + parts[i_scur].off);
+    lp.seg_index = (int2*)(base + parts[i_sidx].off);
+    lp.lat_status = (int32_t*)(base + parts[i_lst].off);
+    lp.g_tab = (u64*)(base + parts[i_gtab].off);
+    lp.g_cnt = (int32_t*)(base + parts[i_gcnt].off);
+    lp.g_cap = (int32_t)lat_gcap;
+    lp.FCAP = d->FCAP;
+    d->lat_grid = (int)NLAT;
+    d->lat_smem = std::min((size_t)prop.sharedMemPerBlockOptin, (size_t)200 * 1024);
+    lp.smem_bytes = (int32_t)d->lat_smem;
+    d->kp_pslack = (float*)(base + parts[i_psl].off);
+    d->kp_gamma = (uint32_t*)(base + parts[i_gam].off);
+    e = cudaFuncSetAttribute(lattice_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d->lat_smem);
+    if (e == cudaSuccess) e = cudaMalloc(&d->d_lat_q, 4);
+    if (e == cudaSuccess) e = cudaMalloc(&d->d_lat_lane, 4);
+    if (e == cudaSuccess) e = cudaMalloc(&d->d_lat_out, 16);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_lat, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMemset(lp.seg_cursor, 0, L * 8);
+    if (e == cudaSuccess) e = cudaMemset(lp.lat_status, 0, L * 4);
+    if (e != cudaSuccess) {
+      wfst_decoder_destroy(d);
+      return cuda_fail(e, "lattice allocation");
+    }
+  }
   e = cudaMemset(base + parts[i_ovf].off, 0xFF, parts[i_ovf].bytes);
   if (e == cudaSuccess) e = cudaMemset(base + parts[i_win].off, 0xFF, parts[i_win].bytes);
   if (e == cudaSuccess) e = cudaMemset(d->d_lanes, 0, sizeof(LaneState) * L);
@@ -429,6 +541,11 @@ void wfst_decoder_destroy(wfst_decoder_t d) {
   cudaFree(d->d_path);
   cudaFree(d->d_host_stage[0]);
   cudaFree(d->d_host_stage[1]);
+  cudaFree(d->d_lat_q);
+  cudaFree(d->d_lat_lane);
+  cudaFree(d->d_lat_out);
+  if (d->ev_lat) cudaEventDestroy(d->ev_lat);
+  if (d->h_lat_stage) cudaFreeHost(d->h_lat_stage);
   if (d->copy_stream) cudaStreamDestroy(d->copy_stream);
   for (int i = 0; i < 2; i++) {
     if (d->ev_copy[i]) cudaEventDestroy(d->ev_copy[i]);
@@ -478,6 +595,10 @@ wfst_status wfst_decoder_reset(wfst_decoder_t d, const int32_t* streams, int32_t
   kp.n_items = B;
   cudaError_t e = launch_frames(d, kp, st);
   if (e != cudaSuccess) return cuda_fail(e, "reset launch");
+  if (d->lattice) {
+    e = launch_lattice(d, nullptr, 0, B, 0, kModeInit, st);
+    if (e != cudaSuccess) return cuda_fail(e, "lattice launch");
+  }
   for (int32_t i = 0; i < B; i++) d->h_initialized[streams ? streams[i] : i] = 1;
   return WFST_OK;
 }
@@ -511,7 +632,23 @@ wfst_status wfst_decode_frames(wfst_decoder_t d, const float* d_loglikes, int32_
   kp.n_items = (int32_t)items;
   cudaError_t e = launch_frames(d, kp, st);
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");
+  if (d->lattice) {
+    e = launch_lattice(d, d_loglikes, T, B, P, kModeFrames, st);
+    if (e != cudaSuccess) return cuda_fail(e, "lattice launch");
+  }
   return WFST_OK;
+}
+
+static cudaError_t ensure_copy_stream(wfst_decoder_t d) {
+  cudaError_t e = cudaSuccess;
+  if (!d->copy_stream) {
+    e = cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; i++) {
+      e = cudaEventCreateWithFlags(&d->ev_copy[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_use[i], cudaEventDisableTiming);
+    }
+  }
+  return e;
 }
 
 wfst_status wfst_decode_frames_host(wfst_decoder_t d, const float* h_loglikes, int32_t T, int32_t B, int32_t P,
@@ -537,14 +674,8 @@ wfst_status wfst_decode_frames_host(wfst_decoder_t d, const float* h_loglikes, i
     if (e != cudaSuccess) return cuda_fail(e, "staging allocation");
     d->stage_bytes = need;
   }
-  if (!d->copy_stream) {
-    e = cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking);
-    for (int i = 0; i < 2 && e == cudaSuccess; i++) {
-      e = cudaEventCreateWithFlags(&d->ev_copy[i], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_use[i], cudaEventDisableTiming);
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "copy stream");
-  }
+  e = ensure_copy_stream(d);
+  if (e != cudaSuccess) return cuda_fail(e, "copy stream");
   // the staging buffers may still be read by earlier work on st
   e = cudaEventRecord(d->ev_use[0], st);
   if (e == cudaSuccess) e = cudaEventRecord(d->ev_use[1], st);
@@ -764,6 +895,122 @@ wfst_status wfst_debug_layer(wfst_decoder_t d, int32_t stream, int32_t layer, in
     if (arcs) arcs[i] = a;
     if (costs) costs[i] = c[i];
   }
+  return WFST_OK;
+}
+
+wfst_status wfst_get_lattice(wfst_decoder_t d, int32_t stream, int32_t* seg_n, int32_t layers_cap,
+                             int32_t* n_layers, int32_t* arc, int32_t* src, int32_t* dst, float* slack,
+                             float* pslack, int64_t arcs_cap, int64_t* n_arcs, float* gamma, int64_t gamma_cap,
+                             int64_t* n_tokens, float* best, int32_t* reached_final) {
+  if (!d || stream < 0 || stream >= d->n_lanes || !n_layers || !n_arcs || !best || !reached_final)
+    return fail(WFST_ERR_INVALID_ARG, "bad argument");
+  if (!d->lattice) return fail(WFST_ERR_INVALID_ARG, "decoder created without opts.lattice");
+  if (!d->h_initialized[stream]) return fail(WFST_ERR_STATE, "stream not reset");
+  DeviceGuard dg(d->device);
+  cudaError_t e = ensure_copy_stream(d);
+  cudaStream_t cs = d->copy_stream;
+  // the backward sweep and the copies run on the copy stream after the lane's last lattice
+  // launch; the compute stream is left running
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, d->ev_lat, 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d->d_lat_lane, &stream, 4, cudaMemcpyHostToDevice, cs);
+  LatFinParams fp{};
+  fp.state_info = d->lp.state_info;
+  fp.arcs = d->lp.arcs;
+  fp.lanes = d->d_lat_lane;
+  fp.lanes_st = d->d_lanes;
+  fp.rec = d->kp.rec;
+  fp.rec_cost = d->kp.rec_cost;
+  fp.R_cap = d->R_cap;
+  fp.layer_info = d->kp.layer_info;
+  fp.TMAX = d->TMAX;
+  fp.seg = d->lp.seg;
+  fp.S_cap = d->S_cap;
+  fp.seg_index = d->lp.seg_index;
+  fp.gamma = d->kp_gamma;
+  fp.pslack = d->kp_pslack;
+  fp.best_out = d->d_lat_out;
+  fp.reached_out = (int32_t*)(d->d_lat_out + 1);
+  fp.status_out = (int32_t*)(d->d_lat_out + 2);
+  fp.lat_status = d->lp.lat_status;
+  if (e == cudaSuccess) {
+    lattice_final_kernel<1024><<<1, 1024, 0, cs>>>(fp);
+    e = cudaGetLastError();
+  }
+  auto stage = [&](size_t bytes) -> cudaError_t {
+    if (bytes <= d->h_lat_bytes) return cudaSuccess;
+    cudaError_t x = cudaStreamSynchronize(cs);
+    if (d->h_lat_stage) cudaFreeHost(d->h_lat_stage);
+    d->h_lat_stage = nullptr;
+    d->h_lat_bytes = 0;
+    if (x == cudaSuccess) x = cudaMallocHost(&d->h_lat_stage, bytes);
+    if (x == cudaSuccess) d->h_lat_bytes = bytes;
+    return x;
+  };
+  struct Head { LaneState L; float out[4]; unsigned long long cursor; };
+  if (e == cudaSuccess) e = stage(std::max(sizeof(Head), (size_t)1 << 20));
+  Head* h = (Head*)d->h_lat_stage;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h->L, d->d_lanes + stream, sizeof(LaneState), cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->out, d->d_lat_out, 16, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h->cursor, d->lp.seg_cursor + stream, 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) return cuda_fail(e, "lattice finalize");
+  const Head H = *h;
+  int32_t st_out;
+  memcpy(&st_out, &H.out[2], 4);
+  if (st_out != WFST_OK)
+    return fail((wfst_status)st_out, "stream " + std::to_string(stream) + ": lattice " +
+                                         wfst_status_string((wfst_status)st_out));
+  const int T = H.L.frames;
+  const int64_t n_tok = H.L.rec_used;
+  const int64_t n_used = (int64_t)H.cursor;
+  *best = H.out[0];
+  memcpy(reached_final, &H.out[1], 4);
+  *n_layers = T + 1;
+  if (n_tokens) *n_tokens = n_tok;
+  // layer index, arena and gamma in one staging buffer
+  const size_t o_sidx = 0, o_lay = o_sidx + 8 * (size_t)(T + 1), o_seg = o_lay + 8 * (size_t)(T + 1);
+  const size_t o_psl = o_seg + 16 * (size_t)n_used, o_gam = o_psl + 4 * (size_t)n_used;
+  const size_t total = o_gam + 4 * (size_t)n_tok;
+  e = stage(total);
+  char* hb = (char*)d->h_lat_stage;
+  const size_t lo = (size_t)stream * (d->TMAX + 1);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(hb + o_sidx, d->lp.seg_index + lo, 8 * (size_t)(T + 1), cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(hb + o_lay, d->kp.layer_info + lo, 8 * (size_t)(T + 1), cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess && n_used)
+    e = cudaMemcpyAsync(hb + o_seg, d->lp.seg + (size_t)stream * d->S_cap, 16 * (size_t)n_used,
+                        cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess && n_used)
+    e = cudaMemcpyAsync(hb + o_psl, d->kp_pslack + (size_t)stream * d->S_cap, 4 * (size_t)n_used,
+                        cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess && n_tok)
+    e = cudaMemcpyAsync(hb + o_gam, d->kp_gamma + (size_t)stream * d->R_cap, 4 * (size_t)n_tok,
+                        cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) return cuda_fail(e, "lattice D2H");
+  const int2* sidx = (const int2*)(hb + o_sidx);
+  const int4* sg = (const int4*)(hb + o_seg);
+  const float* ps = (const float*)(hb + o_psl);
+  int64_t n = 0;
+  for (int k = 0; k <= T; k++) n += sidx[k].y;
+  *n_arcs = n;
+  if ((seg_n && T + 1 > layers_cap) || n > arcs_cap || (gamma && n_tok > gamma_cap))
+    return fail(WFST_ERR_INVALID_ARG, "lattice output capacity too small");
+  // segments in layer order (the arena is filled in completion order)
+  int64_t m = 0;
+  for (int k = 0; k <= T; k++) {
+    if (seg_n) seg_n[k] = sidx[k].y;
+    for (int i = 0; i < sidx[k].y; i++, m++) {
+      const int4 v = sg[sidx[k].x + i];
+      if (arc) arc[m] = v.x;
+      if (src) src[m] = v.y;
+      if (dst) dst[m] = v.z;
+      if (slack) memcpy(&slack[m], &v.w, 4);
+      if (pslack) pslack[m] = ps[sidx[k].x + i];
+    }
+  }
+  if (gamma && n_tok) memcpy(gamma, hb + o_gam, 4 * (size_t)n_tok);
   return WFST_OK;
 }
 

@@ -1,0 +1,365 @@
+// lattice_kernel.cuh -- row f1 (NEXT) of SURVEY §8: per-frame lattice segments and the
+// end-of-utterance backward sweep; included by decoder.cu after frame_kernel.cuh.
+//
+// Segment k of a stream (k = 0: the initial closure, k = t+1: frame t) lists every arc a that
+//   * leaves a representative token i (P:139 soft pruning: only representatives have out-arcs) --
+//     of layer k-1 if a is emitting, c = (cost_i + w) - L[t][pdf], of layer k if a is an epsilon
+//     arc, c = cost_i + w (R1 arithmetic, bit-identical to the frame kernel);
+//   * passes frame k's keep() (the cutoff the frame kernel used, R5/R6);
+//   * has extra cost s = c - cost_j <= lattice_beam, j the token (representative) of dst(a) in
+//     layer k ("computing extra costs", lattice-beam P:146),
+// listed in CSR order by j ("listing them in the CSR format"), arc id ascending inside a
+// group.  Readings R13-R14 of DESIGN.md.  The segments of one decode call are built by one
+// launch after the frame kernel (one work item per (stream, frame)); the frame kernel is not
+// touched: it only keeps each survivor's cost beside its record.
+#pragma once
+#include "frame_kernel.cuh"
+
+namespace wfst_dev {
+
+struct LatParams {
+  const int4* __restrict__ state_info;
+  const int4* __restrict__ arcs;
+  const float* ll;          // the call's log-likelihoods [T][B][P] (mode frames)
+  int32_t T, B, P;
+  const int32_t* lanes;     // batch index -> lane
+  int32_t mode;             // kModeFrames: layers of the call's T frames; kModeInit: layer 0
+  int32_t n_items;
+  int32_t* q_head;
+  float beam, lattice_beam;
+  const LaneState* lanes_st;
+  const int2* rec;          // [lane][R_cap] {arc, state}
+  const float* rec_cost;    // [lane][R_cap]
+  int64_t R_cap;
+  const int2* layer_info;   // [lane][TMAX+1] {record base, n}
+  int32_t TMAX;
+  const float* fstats;      // [lane][TMAX][3]
+  int4* seg;                // [lane][S_cap] {arc, src token, dst token, slack bits}
+  int64_t S_cap;
+  unsigned long long* seg_cursor;   // [lane] arena entries used
+  int2* seg_index;          // [lane][TMAX+1] {arena offset, n} of segment k
+  int32_t* lat_status;      // [lane] sticky lattice status
+  u64* g_tab;               // [cta][g_cap] global fallback token map for large layers
+  int32_t* g_cnt;           // [cta][FCAP]
+  int32_t g_cap, FCAP;
+  int32_t smem_bytes;       // dynamic shared memory of the launch
+};
+
+__device__ __forceinline__ uint32_t lat_bucket(uint32_t q, uint32_t n) { return __umulhi(q * 0x9E3779B1u, n); }
+
+// token map of layer k: state -> token index (states are unique in a layer: insert never matches)
+__device__ __forceinline__ void lat_put(u64* tab, uint32_t cap, uint32_t q, uint32_t i) {
+  uint32_t b = lat_bucket(q, cap);
+  const u64 key = ((u64)q << 32) | i;
+  while (atomicCAS(tab + b, kEmpty, key) != kEmpty) b = (b + 1 == cap) ? 0 : b + 1;
+}
+__device__ __forceinline__ int lat_get(const u64* tab, uint32_t cap, uint32_t q) {
+  uint32_t b = lat_bucket(q, cap);
+  for (uint32_t n = 0; n < cap; n++) {
+    const u64 x = tab[b];
+    if (x == kEmpty) return -1;
+    if ((uint32_t)(x >> 32) == q) return (int)(uint32_t)x;
+    b = (b + 1 == cap) ? 0 : b + 1;
+  }
+  return -1;
+}
+
+template <int BS>
+__device__ int block_excl_scan(int x, int* s_tmp /* 33 ints */, int& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int incl = warp_incl_scan(x);
+  if (lane == 31) s_tmp[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int v = lane < BS / 32 ? s_tmp[lane] : 0;
+    const int vi = warp_incl_scan(v);
+    if (lane < BS / 32) s_tmp[lane] = vi - v;
+    if (lane == 31) s_tmp[32] = vi;
+  }
+  __syncthreads();
+  const int r = s_tmp[w] + incl - x;
+  total = s_tmp[32];
+  __syncthreads();
+  return r;
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS, 1) lattice_kernel(LatParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_item, s_skip, s_err, s_scan[33];
+  __shared__ long long s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = BS / 32;
+  while (true) {
+    if (tid == 0) s_item = atomicAdd(p.q_head, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= p.n_items) break;
+    const int b = p.mode == kModeInit ? item : item % p.B;
+    const int tl = p.mode == kModeInit ? 0 : item / p.B;
+    const int ln = p.lanes[b];
+    const LaneState* Lp = p.lanes_st + ln;
+    const int frames = __ldcg(&Lp->frames);
+    const int k = p.mode == kModeInit ? 0 : frames - p.T + 1 + tl;
+    if (tid == 0) s_skip = (__ldcg(&Lp->status) != WFST_OK || k < 0 || k > frames || k > p.TMAX ||
+                            __ldcg(p.lat_status + ln) != WFST_OK);
+    __syncthreads();
+    if (s_skip) continue;
+    const size_t lo = (size_t)ln * (p.TMAX + 1);
+    const int2 Lk = p.layer_info[lo + k];
+    const int2 Lp1 = k > 0 ? p.layer_info[lo + k - 1] : make_int2(0, 0);
+    const int2* rec = p.rec + (size_t)ln * p.R_cap;
+    const float* rco = p.rec_cost + (size_t)ln * p.R_cap;
+    float cut_b = __fadd_rn(0.0f, p.beam), cut_a = INFINITY;
+    if (k > 0) {
+      const float* fs = p.fstats + ((size_t)ln * p.TMAX + (k - 1)) * 3;
+      cut_b = fs[1];
+      cut_a = fs[2];
+    }
+    const float* row = k > 0 ? p.ll + ((size_t)tl * p.B + b) * (size_t)p.P : nullptr;
+    // token map + per-token counts: shared memory when the layer fits, else this CTA's scratch
+    const int n_k = Lk.y;
+    uint32_t cap = 2u * (uint32_t)n_k + 32u;
+    u64* tab;
+    int* cnt;
+    if ((size_t)cap * 8 + (size_t)n_k * 4 <= (size_t)p.smem_bytes) {
+      tab = (u64*)smem_raw;
+      cnt = (int*)(tab + cap);
+    } else {
+      cap = (uint32_t)p.g_cap;
+      tab = p.g_tab + (size_t)blockIdx.x * p.g_cap;
+      cnt = p.g_cnt + (size_t)blockIdx.x * p.FCAP;
+    }
+    for (uint32_t i = tid; i < cap; i += BS) tab[i] = kEmpty;
+    for (int i = tid; i < n_k; i += BS) cnt[i] = 0;
+    if (tid == 0) s_err = WFST_OK;
+    __syncthreads();
+    for (int i = tid; i < n_k; i += BS) lat_put(tab, cap, (uint32_t)__ldcg(&rec[Lk.x + i].y), (uint32_t)i);
+    __syncthreads();
+    // virtual source tokens: u < n_e -> layer k-1 (emitting arcs), else layer k (epsilon arcs)
+    const int n_e = k > 0 ? Lp1.y : 0;
+    const int n_src = n_e + n_k;
+    for (int pass = 0; pass < 2; pass++) {
+      for (int u0 = warp * 32; u0 < n_src; u0 += NW * 32) {
+        const int u = u0 + lane;
+        int e0 = 0, deg = 0;
+        float co = 0.f;
+        if (u < n_src) {
+          const bool em = u < n_e;
+          const int r = em ? Lp1.x + u : Lk.x + (u - n_e);
+          const int q = __ldcg(&rec[r].y);
+          co = __ldcg(rco + r);
+          const int4 si = __ldg(p.state_info + q);
+          e0 = em ? si.x : si.y;
+          deg = em ? si.y - si.x : si.z - si.y;
+        }
+        const int incl = warp_incl_scan(deg);
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int j0 = 0; j0 < total; j0 += 32) {
+          const int j = j0 + lane;
+          // owner = first lane whose inclusive prefix exceeds j (binary search over the warp)
+          int lo_l = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int v = __shfl_sync(0xffffffffu, incl, lo_l + step - 1);
+            if (v <= j) lo_l += step;
+          }
+          const int own = min(lo_l, 31);
+          const int ex_o = __shfl_sync(0xffffffffu, incl - deg, own);
+          const int eb_o = __shfl_sync(0xffffffffu, e0, own);
+          const float co_o = __shfl_sync(0xffffffffu, co, own);
+          if (j >= total) continue;
+          const int a = eb_o + (j - ex_o);
+          const int4 arc = __ldg(p.arcs + a);
+          const bool em = arc.z >= 0;
+          const float c = em ? __fadd_rn(__fsub_rn(__fadd_rn(co_o, __int_as_float(arc.y)), row[arc.z]), 0.0f)
+                             : __fadd_rn(__fadd_rn(co_o, __int_as_float(arc.y)), 0.0f);
+          if (!(c < cut_b && c <= cut_a)) continue;
+          const int jt = lat_get(tab, cap, (uint32_t)arc.x);
+          if (jt < 0) {   // a kept candidate always has a kept destination
+            s_err = WFST_ERR_STATE;
+            continue;
+          }
+          const float s = __fsub_rn(c, __ldcg(rco + Lk.x + jt));
+          if (!(s <= p.lattice_beam)) continue;
+          if (pass == 0) {
+            atomicAdd(cnt + jt, 1);
+          } else {
+            const int pos = atomicAdd(cnt + jt, 1);
+            const int src_tok = (u0 + own) < n_e ? (u0 + own) : (u0 + own) - n_e;
+            p.seg[(size_t)ln * p.S_cap + s_base + pos] = make_int4(a, src_tok, jt, __float_as_int(s));
+          }
+        }
+      }
+      __syncthreads();
+      if (pass == 0) {   // counts -> CSR offsets; reserve the segment in the stream's arena
+        int run = 0;
+        for (int i0 = 0; i0 < n_k; i0 += BS) {
+          const int i = i0 + tid;
+          const int x = i < n_k ? cnt[i] : 0;
+          int tot;
+          const int ex = block_excl_scan<BS>(x, s_scan, tot);
+          if (i < n_k) cnt[i] = run + ex;
+          run += tot;
+        }
+        if (tid == 0) {
+          const unsigned long long base = atomicAdd(p.seg_cursor + ln, (unsigned long long)run);
+          if (base + run > (unsigned long long)p.S_cap || s_err != WFST_OK) {
+            p.lat_status[ln] = s_err != WFST_OK ? s_err : WFST_ERR_CAPACITY;
+            s_base = -1;
+          } else {
+            s_base = (long long)base;
+          }
+          p.seg_index[lo + k] = make_int2(s_base < 0 ? -1 : (int)s_base, run);
+        }
+        __syncthreads();
+        if (s_base < 0) break;
+      }
+    }
+    if (s_base < 0) continue;
+    if (s_err != WFST_OK && tid == 0) p.lat_status[ln] = s_err;
+    // group j now spans [cnt[j-1], cnt[j]): order it by arc id (groups are small)
+    int4* sg = p.seg + (size_t)ln * p.S_cap + s_base;
+    for (int j = tid; j < n_k; j += BS) {
+      const int g0 = j > 0 ? cnt[j - 1] : 0, g1 = cnt[j];
+      for (int x = g0 + 1; x < g1; x++) {
+        const int4 v = sg[x];
+        int y = x - 1;
+        while (y >= g0 && sg[y].x > v.x) {
+          sg[y + 1] = sg[y];
+          y--;
+        }
+        sg[y + 1] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// End of utterance ("used to generate the final lattice at the end of utterance"; R14):
+// gamma(j) = slack of the best complete path through token j, swept backwards over the layers
+// (emitting arcs of segment k+1 leave layer k; epsilon arcs of segment k to a fixed point), then
+// each arc's path slack s_a + gamma(dst(a)).  One CTA per stream.  gamma is kept as orderable u32
+// so the per-token minimum is an integer atomic.
+struct LatFinParams {
+  const int4* __restrict__ state_info;
+  const int4* __restrict__ arcs;
+  const int32_t* lanes;
+  const LaneState* lanes_st;
+  const int2* rec;
+  const float* rec_cost;
+  int64_t R_cap;
+  const int2* layer_info;
+  int32_t TMAX;
+  const int4* seg;
+  int64_t S_cap;
+  const int2* seg_index;
+  uint32_t* gamma;          // [lane][R_cap] orderable
+  float* pslack;            // [lane][S_cap]
+  float* best_out;          // [n]
+  int32_t* reached_out;     // [n]
+  int32_t* status_out;      // [n]
+  const int32_t* lat_status;
+};
+
+template <int BS>
+__global__ void __launch_bounds__(BS, 1) lattice_final_kernel(LatFinParams p) {
+  __shared__ uint32_t s_fin, s_any;
+  __shared__ int s_changed, s_status;
+  const int tid = threadIdx.x;
+  const int ln = p.lanes[blockIdx.x];
+  const LaneState* Lp = p.lanes_st + ln;
+  const int T = __ldcg(&Lp->frames);
+  if (tid == 0) {
+    s_fin = s_any = 0xFFFFFFFFu;
+    s_status = __ldcg(&Lp->status) != WFST_OK ? __ldcg(&Lp->status)
+               : !__ldcg(&Lp->initialized)    ? WFST_ERR_STATE
+               : T > p.TMAX                   ? WFST_ERR_CAPACITY
+                                              : p.lat_status[ln];
+  }
+  __syncthreads();
+  if (s_status != WFST_OK) {
+    if (tid == 0) {
+      p.status_out[blockIdx.x] = s_status;
+      p.best_out[blockIdx.x] = INFINITY;
+      p.reached_out[blockIdx.x] = 0;
+    }
+    return;
+  }
+  const size_t lo = (size_t)ln * (p.TMAX + 1);
+  const int2* rec = p.rec + (size_t)ln * p.R_cap;
+  const float* rco = p.rec_cost + (size_t)ln * p.R_cap;
+  uint32_t* gam = p.gamma + (size_t)ln * p.R_cap;
+  const int4* seg = p.seg + (size_t)ln * p.S_cap;
+  float* psl = p.pslack + (size_t)ln * p.S_cap;
+  const int2 LT = p.layer_info[lo + T];
+  // best (R10): min over final survivors of c + F, else min c
+  for (int i = tid; i < LT.y; i += BS) {
+    const float c = rco[LT.x + i];
+    const float F = __int_as_float(__ldg(&p.state_info[rec[LT.x + i].y].w));
+    if (F < INFINITY) atomicMin(&s_fin, ord_of(__fadd_rn(c, F)));
+    atomicMin(&s_any, ord_of(c));
+  }
+  const int n_rec = LT.x + LT.y;
+  for (int i = tid; i < n_rec; i += BS) gam[i] = 0xFFFFFFFFu;   // ord(+inf) < 0xFFFFFFFF: "unset"
+  __syncthreads();
+  const bool reached = s_fin != 0xFFFFFFFFu;
+  const float best = float_of_ord(reached ? s_fin : s_any);
+  for (int i = tid; i < LT.y; i += BS) {
+    const float c = rco[LT.x + i];
+    const float F = __int_as_float(__ldg(&p.state_info[rec[LT.x + i].y].w));
+    const float g = reached ? (F < INFINITY ? __fsub_rn(__fadd_rn(c, F), best) : INFINITY) : __fsub_rn(c, best);
+    gam[LT.x + i] = ord_of(g);
+  }
+  __syncthreads();
+  auto gval = [&](int r) {
+    const uint32_t o = __ldcg(gam + r);
+    return o == 0xFFFFFFFFu ? INFINITY : float_of_ord(o);
+  };
+  for (int k = T; k >= 0; k--) {
+    const int2 Lk = p.layer_info[lo + k];
+    if (k < T) {   // emitting arcs of segment k+1: token of layer k -> token of layer k+1
+      const int2 Ln = p.layer_info[lo + k + 1];
+      const int2 sx = p.seg_index[lo + k + 1];
+      for (int m = tid; m < sx.y; m += BS) {
+        const int4 e = seg[sx.x + m];
+        if (__ldg(&p.arcs[e.x].z) < 0) continue;
+        const float v = __fadd_rn(__int_as_float(e.w), gval(Ln.x + e.z));
+        if (v < INFINITY) atomicMin(gam + Lk.x + e.y, ord_of(v));
+      }
+      __syncthreads();
+    }
+    const int2 sx = p.seg_index[lo + k];
+    while (true) {   // epsilon arcs of segment k stay inside layer k
+      if (tid == 0) s_changed = 0;
+      __syncthreads();
+      for (int m = tid; m < sx.y; m += BS) {
+        const int4 e = seg[sx.x + m];
+        if (__ldg(&p.arcs[e.x].z) >= 0) continue;
+        const float v = __fadd_rn(__int_as_float(e.w), gval(Lk.x + e.z));
+        if (v < gval(Lk.x + e.y)) {
+          atomicMin(gam + Lk.x + e.y, ord_of(v));
+          s_changed = 1;
+        }
+      }
+      __syncthreads();
+      if (!s_changed) break;
+    }
+    for (int m = tid; m < sx.y; m += BS) {
+      const int4 e = seg[sx.x + m];
+      psl[sx.x + m] = __fadd_rn(__int_as_float(e.w), gval(Lk.x + e.z));
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < n_rec; i += BS) {   // hand gamma out as fp32 (+inf: no complete path)
+    const float g = gval(i);
+    gam[i] = __float_as_uint(g);
+  }
+  if (tid == 0) {
+    p.status_out[blockIdx.x] = WFST_OK;
+    p.best_out[blockIdx.x] = best;
+    p.reached_out[blockIdx.x] = reached ? 1 : 0;
+  }
+}
+
+}  // namespace wfst_dev

@@ -24,7 +24,7 @@ SYMBOLS = ["wfst_load_graph", "wfst_graph_from_arrays", "wfst_graph_info", "wfst
            "wfst_decode_frames_host", "wfst_decoder_sync", "wfst_decoder_status", "wfst_get_best_path",
            "wfst_get_best_paths", "wfst_decoder_stats", "wfst_decoder_reset_stats", "wfst_decoder_frame_stats",
            "wfst_debug_layer", "wfst_synth_loglikes", "wfst_last_error", "wfst_status_string",
-           "wfst_abi_version"]
+           "wfst_abi_version", "wfst_get_lattice"]
 
 
 class WfstError(RuntimeError):
@@ -43,7 +43,8 @@ class GraphInfo(C.Structure):
 class DecoderOpts(C.Structure):
     _fields_ = [("table_slots", C.c_int32), ("overflow_slots", C.c_int32), ("records_per_stream", C.c_int64),
                 ("max_frames", C.c_int32), ("threads", C.c_int32), ("frames_per_item", C.c_int32),
-                ("max_ctas", C.c_int32), ("debug_costs", C.c_int32), ("ctas_per_sm", C.c_int32)]
+                ("max_ctas", C.c_int32), ("debug_costs", C.c_int32), ("ctas_per_sm", C.c_int32),
+                ("lattice", C.c_int32), ("lattice_beam", C.c_float), ("lattice_arcs_per_stream", C.c_int64)]
 
 
 class Stats(C.Structure):
@@ -97,6 +98,7 @@ def lib():
             "wfst_last_error": [],
             "wfst_status_string": [C.c_int],
             "wfst_abi_version": [],
+            "wfst_get_lattice": [P, I32, P, I32, P, P, P, P, P, P, I64, P, P, I64, P, P, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -222,7 +224,7 @@ class Decoder:
         h = C.c_void_p()
         o = DecoderOpts()
         for k, v in opts.items():
-            setattr(o, k, int(v))
+            setattr(o, k, float(v) if k == "lattice_beam" else int(v))
         _check(lib().wfst_decoder_create_ex(graph.h, n_streams, float(beam), int(max_active or 0), C.byref(o),
                                             C.byref(h)))
         self.h = h
@@ -321,6 +323,30 @@ class Decoder:
         _check(lib().wfst_debug_layer(self.h, stream, layer, _ptr(st), _ptr(ar), _ptr(co), cap, _ptr(n)))
         k = int(n[0])
         return st[:k].copy(), ar[:k].copy(), co[:k].copy()
+
+
+    def lattice(self, stream: int, arcs_cap: int = 1 << 20, layers_cap: int = 1 << 14,
+                gamma_cap: int = 1 << 22) -> dict:
+        """Row f1: the lattice of one stream (wfst_get_lattice): per layer k the segment
+        (arc, src, dst, slack, pslack) and gamma per token, token indices in debug_layer order."""
+        seg_n = np.zeros(layers_cap, np.int32)
+        arc, src, dst = (np.zeros(arcs_cap, np.int32) for _ in range(3))
+        sl, ps = np.zeros(arcs_cap, np.float32), np.zeros(arcs_cap, np.float32)
+        gam = np.zeros(gamma_cap, np.float32)
+        nl, na, nt = np.zeros(1, np.int32), np.zeros(1, np.int64), np.zeros(1, np.int64)
+        best, rf = np.zeros(1, np.float32), np.zeros(1, np.int32)
+        rc = lib().wfst_get_lattice(self.h, stream, _ptr(seg_n), layers_cap, _ptr(nl), _ptr(arc), _ptr(src), _ptr(dst),
+                                    _ptr(sl), _ptr(ps), arcs_cap, _ptr(na), _ptr(gam), gamma_cap, _ptr(nt),
+                                    _ptr(best), _ptr(rf))
+        if rc == 1 and (na[0] > arcs_cap or nl[0] > layers_cap or nt[0] > gamma_cap):
+            return self.lattice(stream, int(na[0]) + 1, int(nl[0]) + 1, int(nt[0]) + 1)
+        _check(rc)
+        so = np.concatenate([[0], np.cumsum(seg_n[: nl[0]])])
+        segs = [(arc[so[k]:so[k + 1]].copy(), src[so[k]:so[k + 1]].copy(), dst[so[k]:so[k + 1]].copy(),
+                 sl[so[k]:so[k + 1]].copy()) for k in range(int(nl[0]))]
+        psl = [ps[so[k]:so[k + 1]].copy() for k in range(int(nl[0]))]
+        return dict(segments=segs, pslack=psl, gamma=gam[: nt[0]].copy(), best=best[0], reached_final=int(rf[0]),
+                    n_layers=int(nl[0]))
 
 
 def synth_loglikes(out, stream_ids, t0: int, seed: int, planted=None, sigma: float = 1.0, boost: float = 0.0,
