@@ -174,6 +174,9 @@ def decoder_opts(args) -> dict:
         v = getattr(args, k, 0)
         if v:
             o[k] = v
+    if getattr(args, "lattice", None) is not None:   # row f1: segments built inside every decode call
+        o["lattice"] = 1
+        o["lattice_beam"] = args.lattice
     return o
 
 
@@ -400,6 +403,8 @@ def main(argv=None):
     ap.add_argument("--chunk", type=int, default=25, help="frames per H2D chunk in the e2e leg")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch (from profiles/)")
     ap.add_argument("--threads", type=int, default=0, help="frame-kernel CTA size (default by variant)")
+    ap.add_argument("--lattice", type=float, default=None,
+                    help="also build lattice segments with this lattice-beam (row f1; not the headline)")
     ap.add_argument("--ctas-per-sm", dest="ctas_per_sm", type=int, default=0)
     ap.add_argument("--table-slots", dest="table_slots", type=int, default=0)
     ap.add_argument("--frames-per-item", dest="frames_per_item", type=int, default=0)

@@ -88,7 +88,7 @@ typedef struct {
                                 from the SM's shared memory divided by this                       */
   int32_t lattice;           /* 1: build lattice segments every frame (row f1)    */
   float lattice_beam;        /* lattice-beam (P:146 uses 8) when lattice = 1; may be 0 or +INF     */
-  int64_t lattice_arcs_per_stream; /* segment arena per stream (default 4 x records_per_stream)   */
+  int64_t lattice_arcs_per_stream; /* segment arena per stream (default 2 x records_per_stream)   */
 } wfst_decoder_opts_t;
 
 typedef struct {

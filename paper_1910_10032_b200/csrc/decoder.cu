@@ -374,7 +374,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
       // bytes per record: {arc, state} (+ cost with debug_costs or lattice, + gamma and 4 arena
       // entries of 20 B with lattice)
       int64_t per_rec = (int64_t)sizeof(int2) + (d->o.debug_costs || d->o.lattice ? 4 : 0) +
-                        (d->o.lattice ? 4 + 4 * 20 : 0);
+                        (d->o.lattice ? 4 + 2 * 20 : 0);
       int64_t cap = budget / per_rec;
       if (cap < d->R_cap) d->R_cap = std::max<int64_t>(cap, per_frame);
     }
@@ -410,7 +410,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   size_t i_rec = add(L * (size_t)d->R_cap * sizeof(int2));
   d->lattice = d->o.lattice != 0;
   if (d->lattice) {
-    d->S_cap = d->o.lattice_arcs_per_stream > 0 ? d->o.lattice_arcs_per_stream : 4 * d->R_cap;
+    d->S_cap = d->o.lattice_arcs_per_stream > 0 ? d->o.lattice_arcs_per_stream : 2 * d->R_cap;
     if (!(d->o.lattice_beam >= 0.0f)) {
       delete d;
       return fail(WFST_ERR_INVALID_ARG, "lattice_beam must be >= 0 (may be +inf)");
@@ -429,6 +429,8 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   size_t i_gam = d->lattice ? add(L * (size_t)d->R_cap * 4) : 0;
   size_t i_gtab = d->lattice ? add(NLAT * (size_t)lat_gcap * 8) : 0;
   size_t i_gcnt = d->lattice ? add(NLAT * (size_t)d->FCAP * 4) : 0;
+  const int64_t lat_stage = 4 * (int64_t)d->FCAP;
+  size_t i_gstg = d->lattice ? add(NLAT * (size_t)lat_stage * sizeof(int4)) : 0;
   size_t i_fst = add(L * (size_t)d->TMAX * 3 * 4);
   size_t i_fcn = add(L * (size_t)d->TMAX * 5 * 8);
   size_t i_linfo = add(L * (size_t)(d->TMAX + 1) * sizeof(int2));
@@ -497,9 +499,11 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     lp.g_tab = (u64*)(base + parts[i_gtab].off);
     lp.g_cnt = (int32_t*)(base + parts[i_gcnt].off);
     lp.g_cap = (int32_t)lat_gcap;
+    lp.g_stage = (int4*)(base + parts[i_gstg].off);
+    lp.stage_cap = (int32_t)lat_stage;
     lp.FCAP = d->FCAP;
     d->lat_grid = (int)NLAT;
-    d->lat_smem = std::min((size_t)prop.sharedMemPerBlockOptin, (size_t)200 * 1024);
+    d->lat_smem = std::min((size_t)prop.sharedMemPerBlockOptin, (size_t)220 * 1024);
     lp.smem_bytes = (int32_t)d->lat_smem;
     d->kp_pslack = (float*)(base + parts[i_psl].off);
     d->kp_gamma = (uint32_t*)(base + parts[i_gam].off);

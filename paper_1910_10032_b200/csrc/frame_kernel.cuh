@@ -403,12 +403,13 @@ struct Frame {
     rec_cost = p.rec_cost ? p.rec_cost + L * (size_t)p.R_cap : nullptr;
   }
 
-  __device__ __forceinline__ u64 read_slot(int slot) const {
-    return slot < p.C ? lds64(tab_sa + 8u * (uint32_t)slot) : ldg_volatile64(ovf + (slot - p.C));
-  }
+  __device__ __forceinline__ u64 slot_key(int i) const { return lds64(tab_sa + 8u * (uint32_t)i); }
   __device__ __forceinline__ void clear_slot(int slot) const {
     if (slot < p.C) sts64(tab_sa + 8u * (uint32_t)slot, kEmpty);
     else ovf[slot - p.C] = kEmpty;
+  }
+  __device__ __forceinline__ u64 read_slot(int slot) const {
+    return slot < p.C ? slot_key(slot) : ldg_volatile64(ovf + (slot - p.C));
   }
 
   __device__ __forceinline__ int insert(uint32_t q, u64 key, bool& claimed, bool& logit, bool& strict) {
@@ -426,10 +427,15 @@ struct Frame {
   // claim bookkeeping (warp-collective: every lane of the warp calls it).  Returns true on
   // the warp whose append crossed a multiple of 1024 claims at or beyond alpha: that warp
   // refreshes the max-active bound.
-  __device__ __forceinline__ bool add_claim(int slot, bool claimed, uint32_t eps_flag, int bin) {
+  __device__ __forceinline__ bool add_claim(int slot, bool claimed, uint32_t eps_flag, int bin, bool seed = true) {
     const int lane = threadIdx.x & 31;
     const unsigned m = __ballot_sync(0xffffffffu, claimed);
     if (m == 0) return false;
+    if (seed) {   // claimed states with epsilon arcs seed the closure (no table scan later)
+      const bool e = claimed && eps_flag;
+      const int idx = warp_append(e, saddr(&S.n_wl));
+      if (e) wl0[idx] = (uint32_t)slot;
+    }
     const int leader = __ffs(m) - 1;
     int base = 0;
     if (lane == leader) base = atom_add_s(saddr(&S.n_claim), __popc(m));
@@ -444,7 +450,6 @@ struct Frame {
       }
       if (bin >= 0) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
     }
-    (void)eps_flag;
     const int end = base + __popc(m);
     return p.alpha > 0 && end >= p.alpha && (end >> 10) != (base >> 10);
   }
@@ -689,7 +694,7 @@ struct Frame {
 #pragma unroll
       for (int u = 0; u < U; u++) {
         sl[u] = i0 + u * BS + tid;
-        v[u] = sl[u] < p.C ? lds64(tab_sa + 8u * (uint32_t)sl[u]) : kEmpty;
+        v[u] = sl[u] < p.C ? slot_key(sl[u]) : kEmpty;
       }
       f(sl, v);
     }
@@ -808,13 +813,8 @@ struct Frame {
   __device__ void eps_closure() {
     const int tid = threadIdx.x;
     const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
-    // seed: kept entries whose state has epsilon arcs (flag in bit 31 of the state word)
-    scan_entries<4>([&](int slot, u64 v) {
-      const float c = key_cost(v);
-      const bool need = v != kEmpty && ((uint32_t)v & 0x80000000u) && c < cut_b && c <= cut_a;
-      const int idx = warp_append(need, saddr(&S.n_wl));
-      if (need) wl0[idx] = (uint32_t)slot;
-    });
+    // seed: the emitting phase listed every claimed state with epsilon arcs (flag in bit 31 of
+    // the state word) in worklist 0; the ones the cutoff drops are skipped below
     __syncthreads();
     int cur = 0;
     long long relax = 0;
@@ -833,9 +833,11 @@ struct Frame {
         if (i < n_wl) {
           const u64 v = read_slot((int)__ldcg(W + i));
           cp = key_cost(v);
-          const int4 si = __ldg(p.state_info + ((uint32_t)v & 0x7FFFFFFFu));
-          e0 = si.y;
-          e1 = si.z;
+          if (cp < cut_b && cp <= cut_a) {   // only kept tokens relax (R7)
+            const int4 si = __ldg(p.state_info + ((uint32_t)v & 0x7FFFFFFFu));
+            e0 = si.y;
+            e1 = si.z;
+          }
         }
         // each thread relaxes its token's epsilon arcs (epsilon out-degrees are small)
         const int n_more = e1 - e0;
@@ -860,7 +862,7 @@ struct Frame {
             }
           }
           const uint32_t has_eps = (uint32_t)arc.w >> 31;
-          add_claim(slot, claimed, has_eps, -1);
+          add_claim(slot, claimed, has_eps, -1, false);
           const bool push = strict && has_eps;
           const int wi = warp_append(push, saddr(&S.n_wl_next));
           if (push) {

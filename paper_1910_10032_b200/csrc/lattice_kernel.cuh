@@ -42,6 +42,8 @@ struct LatParams {
   u64* g_tab;               // [cta][g_cap] global fallback token map for large layers
   int32_t* g_cnt;           // [cta][FCAP]
   int32_t g_cap, FCAP;
+  int4* g_stage;            // [cta][stage_cap] the segment's arcs before placement
+  int32_t stage_cap;
   int32_t smem_bytes;       // dynamic shared memory of the launch
 };
 
@@ -83,10 +85,12 @@ __device__ int block_excl_scan(int x, int* s_tmp /* 33 ints */, int& total) {
   return r;
 }
 
+constexpr int kLatBig = 64, kLatBigCap = 64;   // tokens with more arcs are expanded CTA-wide
+
 template <int BS>
 __global__ void __launch_bounds__(BS, 1) lattice_kernel(LatParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int s_item, s_skip, s_err, s_scan[33];
+  __shared__ int s_item, s_skip, s_err, s_scan[33], s_nbig, s_nst, s_big[kLatBigCap];
   __shared__ long long s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = BS / 32;
@@ -117,109 +121,156 @@ __global__ void __launch_bounds__(BS, 1) lattice_kernel(LatParams p) {
       cut_a = fs[2];
     }
     const float* row = k > 0 ? p.ll + ((size_t)tl * p.B + b) * (size_t)p.P : nullptr;
-    // token map + per-token counts: shared memory when the layer fits, else this CTA's scratch
+    // the frame's log-likelihood row, the token map and the per-token counts live in shared
+    // memory when they fit (else in the CTA's global scratch)
     const int n_k = Lk.y;
-    uint32_t cap = 2u * (uint32_t)n_k + 32u;
+    const int row_bytes = (k > 0 && p.P * 4 <= 48 * 1024) ? (p.P * 4 + 15) / 16 * 16 : 0;
+    uint32_t cap = (3u * (uint32_t)n_k) / 2u + 32u;
     u64* tab;
     int* cnt;
-    if ((size_t)cap * 8 + (size_t)n_k * 4 <= (size_t)p.smem_bytes) {
-      tab = (u64*)smem_raw;
+    const float* cost_k = rco + Lk.x;
+    float* s_cost = nullptr;
+    if ((size_t)row_bytes + (size_t)cap * 8 + (size_t)n_k * 8 <= (size_t)p.smem_bytes) {
+      tab = (u64*)(smem_raw + row_bytes);
       cnt = (int*)(tab + cap);
+      s_cost = (float*)(cnt + n_k);
+      cost_k = s_cost;
     } else {
       cap = (uint32_t)p.g_cap;
       tab = p.g_tab + (size_t)blockIdx.x * p.g_cap;
       cnt = p.g_cnt + (size_t)blockIdx.x * p.FCAP;
     }
+    int4* stg = p.g_stage + (size_t)blockIdx.x * p.stage_cap;
+    const float* rowp = row;
+    if (row_bytes) {
+      float* srow = (float*)smem_raw;
+      for (int i = tid; i < p.P; i += BS) srow[i] = __ldg(row + i);
+      rowp = srow;
+    }
     for (uint32_t i = tid; i < cap; i += BS) tab[i] = kEmpty;
     for (int i = tid; i < n_k; i += BS) cnt[i] = 0;
-    if (tid == 0) s_err = WFST_OK;
+    if (tid == 0) {
+      s_err = WFST_OK;
+      s_nbig = 0;
+      s_nst = 0;
+    }
     __syncthreads();
-    for (int i = tid; i < n_k; i += BS) lat_put(tab, cap, (uint32_t)__ldcg(&rec[Lk.x + i].y), (uint32_t)i);
+    for (int i = tid; i < n_k; i += BS) {
+      lat_put(tab, cap, (uint32_t)__ldcg(&rec[Lk.x + i].y), (uint32_t)i);
+      if (s_cost) s_cost[i] = __ldcg(rco + Lk.x + i);
+    }
     __syncthreads();
     // virtual source tokens: u < n_e -> layer k-1 (emitting arcs), else layer k (epsilon arcs)
     const int n_e = k > 0 ? Lp1.y : 0;
     const int n_src = n_e + n_k;
-    for (int pass = 0; pass < 2; pass++) {
-      for (int u0 = warp * 32; u0 < n_src; u0 += NW * 32) {
-        const int u = u0 + lane;
-        int e0 = 0, deg = 0;
-        float co = 0.f;
-        if (u < n_src) {
-          const bool em = u < n_e;
-          const int r = em ? Lp1.x + u : Lk.x + (u - n_e);
-          const int q = __ldcg(&rec[r].y);
-          co = __ldcg(rco + r);
-          const int4 si = __ldg(p.state_info + q);
-          e0 = em ? si.x : si.y;
-          deg = em ? si.y - si.x : si.z - si.y;
-        }
-        const int incl = warp_incl_scan(deg);
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        for (int j0 = 0; j0 < total; j0 += 32) {
-          const int j = j0 + lane;
-          // owner = first lane whose inclusive prefix exceeds j (binary search over the warp)
-          int lo_l = 0;
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1) {
-            const int v = __shfl_sync(0xffffffffu, incl, lo_l + step - 1);
-            if (v <= j) lo_l += step;
-          }
-          const int own = min(lo_l, 31);
-          const int ex_o = __shfl_sync(0xffffffffu, incl - deg, own);
-          const int eb_o = __shfl_sync(0xffffffffu, e0, own);
-          const float co_o = __shfl_sync(0xffffffffu, co, own);
-          if (j >= total) continue;
-          const int a = eb_o + (j - ex_o);
-          const int4 arc = __ldg(p.arcs + a);
-          const bool em = arc.z >= 0;
-          const float c = em ? __fadd_rn(__fsub_rn(__fadd_rn(co_o, __int_as_float(arc.y)), row[arc.z]), 0.0f)
-                             : __fadd_rn(__fadd_rn(co_o, __int_as_float(arc.y)), 0.0f);
-          if (!(c < cut_b && c <= cut_a)) continue;
-          const int jt = lat_get(tab, cap, (uint32_t)arc.x);
+    // one arc: R1 cost, keep(), destination token, extra cost; staged with its group count
+    // (warp-collective: every lane calls it, v = the lane has an arc)
+    auto proc = [&](bool v, int a, float co, int u) {
+      bool ok = false;
+      int jt = -1;
+      float s = 0.f;
+      if (v) {
+        const int4 arc = __ldg(p.arcs + a);
+        const bool em = arc.z >= 0;
+        const float c = em ? __fadd_rn(__fsub_rn(__fadd_rn(co, __int_as_float(arc.y)), rowp[arc.z]), 0.0f)
+                           : __fadd_rn(__fadd_rn(co, __int_as_float(arc.y)), 0.0f);
+        if (c < cut_b && c <= cut_a) {
+          jt = lat_get(tab, cap, (uint32_t)arc.x);
           if (jt < 0) {   // a kept candidate always has a kept destination
             s_err = WFST_ERR_STATE;
-            continue;
-          }
-          const float s = __fsub_rn(c, __ldcg(rco + Lk.x + jt));
-          if (!(s <= p.lattice_beam)) continue;
-          if (pass == 0) {
-            atomicAdd(cnt + jt, 1);
           } else {
-            const int pos = atomicAdd(cnt + jt, 1);
-            const int src_tok = (u0 + own) < n_e ? (u0 + own) : (u0 + own) - n_e;
-            p.seg[(size_t)ln * p.S_cap + s_base + pos] = make_int4(a, src_tok, jt, __float_as_int(s));
+            s = __fsub_rn(c, cost_k[jt]);
+            ok = s <= p.lattice_beam;
           }
         }
       }
-      __syncthreads();
-      if (pass == 0) {   // counts -> CSR offsets; reserve the segment in the stream's arena
-        int run = 0;
-        for (int i0 = 0; i0 < n_k; i0 += BS) {
-          const int i = i0 + tid;
-          const int x = i < n_k ? cnt[i] : 0;
-          int tot;
-          const int ex = block_excl_scan<BS>(x, s_scan, tot);
-          if (i < n_k) cnt[i] = run + ex;
-          run += tot;
+      const int x = warp_append(ok, saddr(&s_nst));
+      if (ok) {
+        atomicAdd(cnt + jt, 1);
+        if (x < p.stage_cap) stg[x] = make_int4(a, u < n_e ? u : u - n_e, jt, __float_as_int(s));
+      }
+    };
+    auto src_of = [&](int u, int& e0, int& deg, float& co) {
+      const bool em = u < n_e;
+      const int r = em ? Lp1.x + u : Lk.x + (u - n_e);
+      const int q = __ldcg(&rec[r].y);
+      co = __ldcg(rco + r);
+      const int4 si = __ldg(p.state_info + q);
+      e0 = em ? si.x : si.y;
+      deg = em ? si.y - si.x : si.z - si.y;
+    };
+    // tokens of small out-degree: 32 per warp, arcs flattened over the warp
+    for (int u0 = warp * 32; u0 < n_src; u0 += NW * 32) {
+      const int u = u0 + lane;
+      int e0 = 0, deg = 0;
+      float co = 0.f;
+      if (u < n_src) src_of(u, e0, deg, co);
+      if (deg > kLatBig) {   // hub tokens are expanded CTA-wide below (if the list has room)
+        const int x = atomicAdd(&s_nbig, 1);
+        if (x < kLatBigCap) {
+          s_big[x] = u;
+          deg = 0;
         }
-        if (tid == 0) {
-          const unsigned long long base = atomicAdd(p.seg_cursor + ln, (unsigned long long)run);
-          if (base + run > (unsigned long long)p.S_cap || s_err != WFST_OK) {
-            p.lat_status[ln] = s_err != WFST_OK ? s_err : WFST_ERR_CAPACITY;
-            s_base = -1;
-          } else {
-            s_base = (long long)base;
-          }
-          p.seg_index[lo + k] = make_int2(s_base < 0 ? -1 : (int)s_base, run);
+      }
+      const int incl = warp_incl_scan(deg);
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      for (int j0 = 0; j0 < total; j0 += 32) {
+        const int j = j0 + lane;
+        // owner = first lane whose inclusive prefix exceeds j (binary search over the warp)
+        int lo_l = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int v = __shfl_sync(0xffffffffu, incl, lo_l + step - 1);
+          if (v <= j) lo_l += step;
         }
-        __syncthreads();
-        if (s_base < 0) break;
+        const int own = min(lo_l, 31);
+        const int ex_o = __shfl_sync(0xffffffffu, incl - deg, own);
+        const int eb_o = __shfl_sync(0xffffffffu, e0, own);
+        const float co_o = __shfl_sync(0xffffffffu, co, own);
+        proc(j < total, eb_o + (j - ex_o), co_o, u0 + own);
       }
     }
+    __syncthreads();
+    const int nbig = min(s_nbig, kLatBigCap);
+    for (int x = 0; x < nbig; x++) {
+      const int u = s_big[x];
+      int e0, deg;
+      float co;
+      src_of(u, e0, deg, co);
+      for (int j0 = 0; j0 < deg; j0 += BS) proc(j0 + tid < deg, e0 + j0 + tid, co, u);
+    }
+    __syncthreads();
+    // counts -> CSR offsets; reserve the segment in the stream's arena; scatter the staged arcs
+    const int n_st = s_nst;
+    int run = 0;
+    for (int i0 = 0; i0 < n_k; i0 += BS) {
+      const int i = i0 + tid;
+      const int x = i < n_k ? cnt[i] : 0;
+      int tot;
+      const int ex = block_excl_scan<BS>(x, s_scan, tot);
+      if (i < n_k) cnt[i] = run + ex;
+      run += tot;
+    }
+    if (tid == 0) {
+      const int err = s_err != WFST_OK ? s_err : n_st > p.stage_cap ? WFST_ERR_CAPACITY : WFST_OK;
+      const unsigned long long base = atomicAdd(p.seg_cursor + ln, (unsigned long long)run);
+      if (base + run > (unsigned long long)p.S_cap || err != WFST_OK) {
+        p.lat_status[ln] = err != WFST_OK ? err : WFST_ERR_CAPACITY;
+        s_base = -1;
+      } else {
+        s_base = (long long)base;
+      }
+      p.seg_index[lo + k] = make_int2(s_base < 0 ? -1 : (int)s_base, run);
+    }
+    __syncthreads();
     if (s_base < 0) continue;
-    if (s_err != WFST_OK && tid == 0) p.lat_status[ln] = s_err;
-    // group j now spans [cnt[j-1], cnt[j]): order it by arc id (groups are small)
     int4* sg = p.seg + (size_t)ln * p.S_cap + s_base;
+    for (int i = tid; i < n_st; i += BS) {
+      const int4 e = __ldcg(stg + i);
+      sg[atomicAdd(cnt + e.z, 1)] = e;
+    }
+    __syncthreads();
+    // group j now spans [cnt[j-1], cnt[j]): order it by arc id (groups are small)
     for (int j = tid; j < n_k; j += BS) {
       const int g0 = j > 0 ? cnt[j - 1] : 0, g1 = cnt[j];
       for (int x = g0 + 1; x < g1; x++) {
