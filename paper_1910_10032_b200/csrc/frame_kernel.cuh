@@ -31,10 +31,7 @@ constexpr int kModeFrames = 0, kModeInit = 1;
 constexpr int kBig = 64;           // tokens with more emitting arcs are expanded CTA-wide
 constexpr int kBigCap = 256;
 constexpr int kStage = 32;         // per-warp staging buffer (candidates awaiting insertion)
-#ifndef WFST_NBUCK
-#define WFST_NBUCK 16
-#endif
-constexpr int kNBuck = WFST_NBUCK; // cost buckets ordering the next frontier
+constexpr int kPlace = 64;         // coarse cost bins ordering the next frontier (kNB / 16 each)
 constexpr int kSmallClaims = 2048; // frames with at most this many claims use an on-chip claim list
 
 struct LaneState {
@@ -86,7 +83,9 @@ struct SmemCtl {
   uint32_t best_ord;
   int32_t theta;
   int32_t n_claim, n_claim_emit, n_ovf, n_oclaim, n_surv, n_in, n_wl, n_wl_next, n_big, next_group;
-  int32_t bucket_base[kNBuck];
+  int32_t pl[kPlace];        // placement histogram: live entries per coarse cost bin
+  int32_t pl_base[kPlace];   // placement cursors
+  int32_t n_app;             // survivors appended in the cutoff's bin
   long long t_mark;
   unsigned long long row_mbar;   // mbarrier of the row's bulk copy
   int32_t row_parity, row_pending, row_off, t_cur;
@@ -94,6 +93,7 @@ struct SmemCtl {
   int32_t use_alpha;
   int32_t radix_prefix, radix_k;
   unsigned long long emit_arcs, eps_deg, eps_relax;
+  unsigned long long dbg[2];   // WFST_COUNT instrumentation: hub candidates staged, table inserts
   uint32_t sclaim[kSmallClaims];   // claimed slots while the frame is small
   int32_t warp_tmp[32];
   long long warp_tmp64[32];
@@ -210,7 +210,7 @@ __device__ __forceinline__ int bin_of(float c, float ref, float inv_w) {
 // Returns the slot, or -1 when the probe limit is reached.  claimed: the slot was empty;
 // logit: the cost is <= the slot's (an improvement or a tie); strict: <.
 __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q, u64 key, bool& claimed,
-                                        bool& logit, bool& strict) {
+                                        bool& logit, bool& strict, uint32_t& old_hi) {
   uint32_t b = bucket_of(q, nb);
   const uint32_t hi = (uint32_t)(key >> 32);
   claimed = logit = strict = false;
@@ -232,6 +232,7 @@ __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q
       const u64 old = atom_cas_s(ba + 8 * j, kEmpty, key);
       if (old == kEmpty) {
         claimed = logit = strict = true;
+        old_hi = 0xFFFFFFFFu;
         return (int)(b * 4 + j);
       }
       if ((uint32_t)old != q) continue;   // lost the slot to another state: re-read this bucket
@@ -245,13 +246,14 @@ __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q
     const uint32_t old = atom_min_s_u32(ba + 8 * j + 4, hi);
     logit = hi <= old;
     strict = hi < old;
+    old_hi = old;
     return (int)(b * 4 + j);
   }
   return -1;
 }
 
 __device__ __forceinline__ int insert_g(u64* tab, uint32_t nb, uint32_t q, u64 key, bool& claimed, bool& logit,
-                                        bool& strict) {
+                                        bool& strict, uint32_t& old_hi) {
   uint32_t b = bucket_of(q, nb);
   claimed = logit = strict = false;
 #pragma unroll 1
@@ -266,6 +268,7 @@ __device__ __forceinline__ int insert_g(u64* tab, uint32_t nb, uint32_t q, u64 k
         u64 old = atomicMin(bk + j, key);
         logit = key <= old;
         strict = key < old;
+        old_hi = (uint32_t)(old >> 32);
         return (int)(b * 4 + j);
       }
 #pragma unroll
@@ -274,12 +277,14 @@ __device__ __forceinline__ int insert_g(u64* tab, uint32_t nb, uint32_t q, u64 k
         u64 old = atomicCAS(bk + j, kEmpty, key);
         if (old == kEmpty) {
           claimed = logit = strict = true;
+          old_hi = 0xFFFFFFFFu;
           return (int)(b * 4 + j);
         }
         if ((uint32_t)old == q) {
           old = atomicMin(bk + j, key);
           logit = key <= old;
           strict = key < old;
+          old_hi = (uint32_t)(old >> 32);
           return (int)(b * 4 + j);
         }
       }
@@ -412,15 +417,37 @@ struct Frame {
     return slot < p.C ? slot_key(slot) : ldg_volatile64(ovf + (slot - p.C));
   }
 
+  // coarse placement bin of a cost: kNB/kPlace consecutive max-active bins (monotone in c)
+  __device__ __forceinline__ int pbin(float c) const { return bin_of(c, S.ref, S.inv_w) / (kNB / kPlace); }
+  // keep the placement histogram equal to the table's current costs: +1 on a claim, a move
+  // between bins on a strict improvement (DESIGN.md §5.2 contraction)
+  __device__ __forceinline__ void pl_update(int slot, bool claimed, bool strict, uint32_t old_hi, uint32_t new_hi) {
+    if (slot < 0) return;
+    if (claimed) {
+      red_add_s(saddr(&S.pl[pbin(float_of_ord(new_hi))]), 1);
+    } else if (strict) {
+      const int ob = pbin(float_of_ord(old_hi)), nb = pbin(float_of_ord(new_hi));
+      if (ob != nb) {
+        red_add_s(saddr(&S.pl[ob]), -1);
+        red_add_s(saddr(&S.pl[nb]), 1);
+      }
+    }
+  }
+
   __device__ __forceinline__ int insert(uint32_t q, u64 key, bool& claimed, bool& logit, bool& strict) {
-    int s = insert_s(tab_sa, (uint32_t)p.NBK, q, key, claimed, logit, strict);
-    if (s >= 0) return s;
-    s = insert_g(ovf, (uint32_t)(p.C_ovf / 4), q, key, claimed, logit, strict);
+    uint32_t old_hi = 0xFFFFFFFFu;
+    int s = insert_s(tab_sa, (uint32_t)p.NBK, q, key, claimed, logit, strict, old_hi);
+    if (s < 0) s = insert_g(ovf, (uint32_t)(p.C_ovf / 4), q, key, claimed, logit, strict, old_hi);
+    else {
+      pl_update(s, claimed, strict, old_hi, (uint32_t)(key >> 32));
+      return s;
+    }
     if (s < 0) {
       S.status = WFST_ERR_CAPACITY;
       return -1;
     }
     if (claimed) atomicAdd(&S.n_ovf, 1);
+    pl_update(s, claimed, strict, old_hi, (uint32_t)(key >> 32));
     return s + p.C;
   }
 
@@ -502,6 +529,12 @@ struct Frame {
         if (slot < 0) claimed = false;
       }
     }
+#ifdef WFST_COUNT
+    {
+      const unsigned mi = __ballot_sync(0xffffffffu, slot >= 0);
+      if (lane == 0) red_add_s64(saddr(&S.dbg[1]), __popc(mi));
+    }
+#endif
     if (add_claim(slot, claimed, flag, bin)) update_theta();
   }
 
@@ -651,6 +684,12 @@ struct Frame {
           const bool pass = v[u] && c < bound && bin < th;
           const int j = j0 + u * BS + tid;
           const int4 entry = make_int4(arc[u].x, (int)ord_of(c), f.z + j, bin | (int)(arc[u].w & 0x80000000));
+#ifdef WFST_COUNT
+          {
+            const unsigned mh = __ballot_sync(0xffffffffu, pass);
+            if (lane == 0) red_add_s64(saddr(&S.dbg[0]), __popc(mh));
+          }
+#endif
           stage(pass, entry, staged, beam, best_sa, theta_sa);
         }
       }
@@ -889,53 +928,34 @@ struct Frame {
   __device__ void contract() {
     const int tid = threadIdx.x, lane = tid & 31;
     const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
-    // bucket range [best, cutoff) for the cost order of the next frontier
-    const float bk_ref = float_of_ord(S.best_ord);
-    float span = __fsub_rn(S.use_alpha ? fminf(cut_b, cut_a) : cut_b, bk_ref);
-    if (!(span > 0.0f) || isinf(span)) span = 32.0f;
-    const float bk_inv = (float)kNBuck / span;
-    if (tid < kNBuck) S.bucket_base[tid] = 0;
+    // The placement histogram counts the table's live entries per coarse cost bin (kept exact
+    // by every insert).  pbin is monotone, so bins below bc = min(pbin(cut_b), pbin(cut_a)) hold
+    // only survivors and no survivor lies above bc: their counts give exact cursors, and the
+    // survivors of bin bc are appended after them.  One pass over the table, no counting pass.
+    const int bc = min(pbin(cut_b), pbin(cut_a));
     if (tid == 0) {
-      S.n_surv = 0;
-      S.min_surv = INFINITY;
-    }
-    __syncthreads();
-    float mn = INFINITY;
-    // pass 1: count the survivors of each cost bucket (the table is only read)
-    scan_entries<4>([&](int slot, u64 v) {
-      const float c = key_cost(v);
-      const bool k = v != kEmpty && c < cut_b && c <= cut_a;
-      const int bk = k ? (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1))
-                       : kNBuck;
-      const unsigned grp = __match_any_sync(0xffffffffu, bk);
-      if (bk < kNBuck && lane == __ffs(grp) - 1) red_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
-      if (k) mn = fminf(mn, c);
-    });
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    if ((tid & 31) == 0) S.warp_tmp[tid >> 5] = __float_as_int(mn);
-    __syncthreads();
-    if (tid == 0) {
-      float m = INFINITY;
-      for (int w = 0; w < NW; w++) m = fminf(m, __int_as_float(S.warp_tmp[w]));
-      S.min_surv = m;
       int acc = 0;
-      for (int b = 0; b < kNBuck; b++) {
-        const int n = S.bucket_base[b];
-        S.bucket_base[b] = acc;
-        acc += n;
+      for (int b = 0; b < bc; b++) {
+        S.pl_base[b] = acc;
+        acc += S.pl[b];
       }
-      S.n_surv = acc;
+      S.pl_base[bc] = acc;
+      S.n_surv = acc + S.pl[bc];   // upper bound until the appended count is known
+      S.n_app = 0;
+      S.min_surv = INFINITY;
+      S.warp_tmp[0] = -1;   // min survivor cost, orderable (0xFFFFFFFF: none)
     }
-    mark(6);   // counts done
     __syncthreads();
-    const int n_surv = S.n_surv;
+    mark(6);   // cursors ready
+    const int n_ub = S.n_surv;
     const int32_t rb = S.L.rec_used;
-    if (n_surv > p.FCAP || (long long)rb + n_surv > p.R_cap) {
+    if (n_ub > p.FCAP || (long long)rb + n_ub > p.R_cap) {
       if (tid == 0) S.status = WFST_ERR_CAPACITY;
       __syncthreads();
       return;
     }
+    const int app0 = S.pl_base[bc];
+    float mn = INFINITY;
     // pass 2: drain the tables and place each survivor at its bucket cursor: frontier entry
     // (with the state's emitting range, prepared for the next frame: P:78) and traceback record
     int4* Fout = F0 + (size_t)(S.L.cur ^ 1) * p.FCAP;
@@ -950,12 +970,13 @@ struct Frame {
         const bool live = v[u] != kEmpty;
         const float c = key_cost(v[u]);
         const bool k = live && c < cut_b && c <= cut_a;
-        const int bk = k ? (int)fminf(fmaxf(__fmul_rn(__fsub_rn(c, bk_ref), bk_inv), 0.0f), (float)(kNBuck - 1))
-                         : kNBuck;
+        if (k) mn = fminf(mn, c);
+        const int bk = k ? min(pbin(c), bc) : kPlace;   // bin bc: the append region
         const unsigned grp = __match_any_sync(0xffffffffu, bk);
         const int leader = __ffs(grp) - 1;
         int base = 0;
-        if (bk < kNBuck && lane == leader) base = atom_add_s(saddr(&S.bucket_base[bk]), __popc(grp));
+        if (bk < kPlace && lane == leader)
+          base = bk < bc ? atom_add_s(saddr(&S.pl_base[bk]), __popc(grp)) : app0 + atom_add_s(saddr(&S.n_app), __popc(grp));
         base = __shfl_sync(0xffffffffu, base, leader);
         pos[u] = k ? base + __popc(grp & ((1u << lane) - 1u)) : (live ? -1 : -2);
         if (live) clear_slot(sl[u]);
@@ -985,14 +1006,23 @@ struct Frame {
     {
       const unsigned long long wsum = warp_sum64(epsd);
       if (lane == 0 && wsum) red_add_s64(saddr(&S.eps_deg), wsum);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      if (lane == 0 && mn < INFINITY) atomicMin((unsigned int*)&S.warp_tmp[0], ord_of(mn));
     }
     __syncthreads();
+    if (tid == 0) {
+      S.n_surv = app0 + S.n_app;
+      const uint32_t o = (uint32_t)S.warp_tmp[0];
+      S.min_surv = o == 0xFFFFFFFFu ? INFINITY : float_of_ord(o);
+    }
     mark(8);   // placement done
   }
 
   __device__ void begin_frame(float beam_cut_fixed) {
     const int tid = threadIdx.x;
     for (int i = tid; i < kNB; i += BS) hist[i] = 0;
+    if (tid < kPlace) S.pl[tid] = 0;
     if (tid == 0) {
       S.best_ord = 0xFFFFFFFFu;
       S.theta = kNB;
@@ -1001,6 +1031,7 @@ struct Frame {
       S.n_ovf = 0;
       S.n_big = 0;
       S.next_group = 0;
+      S.dbg[0] = S.dbg[1] = 0;
       S.n_wl = 0;
       S.use_alpha = 0;
       S.kalpha = INFINITY;
@@ -1043,6 +1074,10 @@ struct Frame {
         L.cand += S.n_claim;
         L.surv += n_surv;
         L.ovf += S.n_ovf;
+#ifdef WFST_COUNT
+        L.phase[7] += S.dbg[0];
+        L.phase[9] += S.dbg[1];
+#endif
         if (emitting) {
           L.emit_arcs += S.emit_arcs;
           L.alpha_frames += S.use_alpha;
