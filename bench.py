@@ -214,6 +214,8 @@ def gpu_arm(args):
             ev[0].record()
         for t0 in range(0, T, chunk):
             D.decode_frames(ll[t0:t0 + chunk] if chunk < T else ll)
+            if args.partial:   # row f2: settled partial results of every stream after each chunk
+                D.partial_paths(cap=4 * T + 64)
         if ev is not None:
             ev[1].record()
         return D.best_paths(cap=cap, raise_on_error=False)
@@ -403,6 +405,8 @@ def main(argv=None):
     ap.add_argument("--chunk", type=int, default=25, help="frames per H2D chunk in the e2e leg")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch (from profiles/)")
     ap.add_argument("--threads", type=int, default=0, help="frame-kernel CTA size (default by variant)")
+    ap.add_argument("--partial", action="store_true",
+                    help="fetch settled partial results after every chunk (row f2; not the headline)")
     ap.add_argument("--lattice", type=float, default=None,
                     help="also build lattice segments with this lattice-beam (row f1; not the headline)")
     ap.add_argument("--ctas-per-sm", dest="ctas_per_sm", type=int, default=0)

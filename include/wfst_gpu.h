@@ -197,6 +197,22 @@ wfst_status wfst_decoder_frame_stats(wfst_decoder_t d, int32_t stream, float* fs
 wfst_status wfst_debug_layer(wfst_decoder_t d, int32_t stream, int32_t layer, int32_t* states,
                              int32_t* arcs, float* costs, int32_t cap, int32_t* n);
 
+/* ---- settled partial results (row f2 of SURVEY §8, NEXT; "return intermediate results
+ * during online decoding") --------------------------------------------------------------------
+ * The settled prefix of a stream is the longest arc sequence shared by the tracebacks of ALL
+ * current survivors, cut after its last emitting arc (reading R15): no later frame can change
+ * it.  Each call returns, per stream, only the arcs settled SINCE the previous call (or the
+ * reset), in order, with their non-zero olabels; concatenating a stream's outputs gives its
+ * settled prefix, which is always a prefix of the final wfst_get_best_path result.
+ *   arcs/olabels: host [n][cap] (nullable); n_arcs[i] / n_olabels[i] (nullable): counts;
+ *   settled_frames[i]: frames (= layer) covered by the settled prefix so far.
+ * Synchronises the decoder.  A stream whose new arcs exceed cap returns INVALID_ARG with the
+ * needed count in n_arcs[i] and keeps its settle point (call again with a larger cap).
+ * Layers of more than 16384 tokens return CAPACITY. */
+wfst_status wfst_get_partial_paths(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
+                                   int32_t* olabels, int32_t cap, int32_t* n_arcs, int32_t* n_olabels,
+                                   int32_t* settled_frames);
+
 /* ---- lattice (row f1 of SURVEY §8, NEXT) ----------------
  * With opts.lattice = 1 every reset and decode call also builds, per stream and frame, the lattice
  * segment of that frame (one extra launch after the frame kernel, same CUDA stream): every arc

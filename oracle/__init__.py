@@ -187,6 +187,39 @@ class OracleGraph:
         r.lattice_beam = float(lattice_beam)
         return r
 
+    def settled_prefix(self, ll: np.ndarray, beam: float, max_active: int = 0) -> np.ndarray:
+        """Row f2 (reading R15; "intermediate results during online decoding"): decode the
+        frames of ll, then take the traceback (canonical arc ids, start first) of EVERY survivor of
+        the last layer, their longest common prefix, cut after its last emitting arc.  Written as
+        the definition -- every path is traced in full -- not as the GPU's walk-back."""
+        r = self.decode(ll, beam, max_active, survivors=True)
+        perm = self.perm()
+        src_c = self.g.src[perm]
+        emit_c = self.g.ilabel[perm] != 0
+        maps = [dict(zip(L[0].tolist(), L[1].tolist())) for L in r.layers]   # state -> winning arc
+
+        def trace(k, q):
+            out = []
+            while True:
+                a = maps[k][q]
+                if a < 0:
+                    return out[::-1]
+                out.append(a)
+                if emit_c[a]:
+                    k -= 1
+                q = int(src_c[a])
+
+        T = len(r.layers) - 1
+        paths = [trace(T, int(q)) for q in r.layers[T][0]]
+        lcp = []
+        for col in zip(*paths):
+            if any(x != col[0] for x in col):
+                break
+            lcp.append(col[0])
+        while lcp and not emit_c[lcp[-1]]:
+            lcp.pop()
+        return np.array(lcp, np.int64)
+
     def decode_batch(self, ll: np.ndarray, beam: float, max_active: int, n_threads: int,
                      arcs_cap: int = 0):
         """ll: float32 [T][B][P] contiguous.  Returns (cost, reached, rc, arcs_count, arcs, n_arcs)."""

@@ -17,6 +17,7 @@
 
 #include "frame_kernel.cuh"
 #include "lattice_kernel.cuh"
+#include "partial_kernel.cuh"
 #include "wfst_internal.h"
 
 using namespace wfst;
@@ -203,6 +204,8 @@ struct wfst_decoder_s {
   size_t stage_bytes = 0;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_use[2] = {nullptr, nullptr};
+  int2* d_settled = nullptr;        // [lane] last settle point of the partial results (row f2)
+  size_t partial_smem = 0;
   // lattice (row f1)
   bool lattice = false;
   int64_t S_cap = 0;
@@ -266,6 +269,12 @@ __global__ void lat_reset_kernel(const int32_t* lanes, int32_t n, unsigned long 
     cursor[lanes[i]] = 0;
     status[lanes[i]] = WFST_OK;
   }
+}
+
+// row f2: a lane starts a new utterance: nothing is settled yet
+__global__ void settle_reset_kernel(const int32_t* lanes, int32_t n, int2* settled) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) settled[lanes[i]] = make_int2(-1, -1);
 }
 
 // row f1: the lattice segments of the layers the last frame-kernel launch produced
@@ -439,6 +448,8 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   if (e == cudaSuccess) e = cudaMalloc(&d->d_qhead, 4);
   if (e == cudaSuccess) e = cudaMalloc(&d->d_round, 4 * L);
   if (e == cudaSuccess) e = cudaMalloc(&d->d_lane_ids, 4 * L);
+  if (e == cudaSuccess) e = cudaMalloc(&d->d_settled, sizeof(int2) * L);
+  if (e == cudaSuccess) e = cudaMemset(d->d_settled, 0xFF, sizeof(int2) * L);
   if (e != cudaSuccess) {
     cudaFree(d->d_pool);
     cudaFree(d->d_lanes);
@@ -545,6 +556,7 @@ void wfst_decoder_destroy(wfst_decoder_t d) {
   cudaFree(d->d_path);
   cudaFree(d->d_host_stage[0]);
   cudaFree(d->d_host_stage[1]);
+  cudaFree(d->d_settled);
   cudaFree(d->d_lat_q);
   cudaFree(d->d_lat_lane);
   cudaFree(d->d_lat_out);
@@ -597,7 +609,9 @@ wfst_status wfst_decoder_reset(wfst_decoder_t d, const int32_t* streams, int32_t
   kp.mode = kModeInit;
   kp.K = 1;
   kp.n_items = B;
-  cudaError_t e = launch_frames(d, kp, st);
+  settle_reset_kernel<<<(B + 255) / 256, 256, 0, st>>>(d->d_lane_ids, B, d->d_settled);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = launch_frames(d, kp, st);
   if (e != cudaSuccess) return cuda_fail(e, "reset launch");
   if (d->lattice) {
     e = launch_lattice(d, nullptr, 0, B, 0, kModeInit, st);
@@ -1016,6 +1030,86 @@ wfst_status wfst_get_lattice(wfst_decoder_t d, int32_t stream, int32_t* seg_n, i
   }
   if (gamma && n_tok) memcpy(gamma, hb + o_gam, 4 * (size_t)n_tok);
   return WFST_OK;
+}
+
+wfst_status wfst_get_partial_paths(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
+                                   int32_t* olabels, int32_t cap, int32_t* n_arcs, int32_t* n_olabels,
+                                   int32_t* settled_frames) {
+  if (!d || n < 0 || !n_arcs || !settled_frames || cap < 0) return fail(WFST_ERR_INVALID_ARG, "bad argument");
+  if (n == 0) return WFST_OK;
+  DeviceGuard dg(d->device);
+  std::vector<int32_t> ids(n);
+  for (int i = 0; i < n; i++) {
+    int32_t s = streams ? streams[i] : i;
+    if (s < 0 || s >= d->n_lanes) return fail(WFST_ERR_INVALID_ARG, "stream id out of range");
+    if (!d->h_initialized[s]) return fail(WFST_ERR_STATE, "stream " + std::to_string(s) + " not reset");
+    ids[i] = s;
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "sync");
+  const int cp = std::max(cap, 1);
+  size_t need = (size_t)n * (6 + 2 * (size_t)cp);
+  if (need > d->path_cap) {
+    cudaFree(d->d_path);
+    d->d_path = nullptr;
+    e = cudaMalloc(&d->d_path, need * 4);
+    if (e != cudaSuccess) {
+      d->path_cap = 0;
+      return cuda_fail(e, "path buffer");
+    }
+    d->path_cap = need;
+  }
+  int32_t* p = d->d_path;
+  PartialParams pp{};
+  pp.arcs = d->kp.arcs;
+  pp.olabel = d->g->d_olabel;
+  pp.lanes = p;
+  pp.lanes_st = d->d_lanes;
+  pp.rec = d->kp.rec;
+  pp.R_cap = d->R_cap;
+  pp.layer_info = d->kp.layer_info;
+  pp.TMAX = d->TMAX;
+  pp.settled = d->d_settled;
+  pp.cap = cp;
+  pp.n_arcs_out = p + n;
+  pp.n_olab_out = p + 2 * n;
+  pp.layer_out = p + 3 * n;
+  pp.status_out = p + 4 * n;
+  pp.arcs_out = p + 6 * n;
+  pp.olab_out = pp.arcs_out + (size_t)n * cp;
+  // shared memory: a set of wanted source states (2 slots per token) + one flag per token
+  pp.wcap = 32768;
+  pp.fcap = 16384;
+  const size_t smem = (size_t)pp.wcap * 4 + (size_t)pp.fcap;
+  if (d->partial_smem != smem) {
+    e = cudaFuncSetAttribute(partial_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "partial kernel attribute");
+    d->partial_smem = smem;
+  }
+  e = cudaMemcpy(p, ids.data(), 4 * (size_t)n, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "ids");
+  partial_kernel<1024><<<n, 1024, smem>>>(pp);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "partial kernel");
+  std::vector<int32_t> head(5 * (size_t)n);
+  e = cudaMemcpy(head.data(), p, 4 * head.size(), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && arcs && cap > 0) e = cudaMemcpy(arcs, pp.arcs_out, 4 * (size_t)n * cp, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && olabels && cap > 0)
+    e = cudaMemcpy(olabels, pp.olab_out, 4 * (size_t)n * cp, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "partial D2H");
+  wfst_status first = WFST_OK;
+  for (int i = 0; i < n; i++) {
+    n_arcs[i] = head[n + i];
+    if (n_olabels) n_olabels[i] = head[2 * n + i];
+    settled_frames[i] = head[3 * n + i];
+    wfst_status s = (wfst_status)head[4 * n + i];
+    if (s != WFST_OK && first == WFST_OK) {
+      first = s;
+      set_error("stream " + std::to_string(ids[i]) + ": " + wfst_status_string(s));
+    }
+  }
+  return first;
 }
 
 }  // extern "C"

@@ -24,7 +24,7 @@ SYMBOLS = ["wfst_load_graph", "wfst_graph_from_arrays", "wfst_graph_info", "wfst
            "wfst_decode_frames_host", "wfst_decoder_sync", "wfst_decoder_status", "wfst_get_best_path",
            "wfst_get_best_paths", "wfst_decoder_stats", "wfst_decoder_reset_stats", "wfst_decoder_frame_stats",
            "wfst_debug_layer", "wfst_synth_loglikes", "wfst_last_error", "wfst_status_string",
-           "wfst_abi_version", "wfst_get_lattice"]
+           "wfst_abi_version", "wfst_get_lattice", "wfst_get_partial_paths"]
 
 
 class WfstError(RuntimeError):
@@ -99,6 +99,7 @@ def lib():
             "wfst_status_string": [C.c_int],
             "wfst_abi_version": [],
             "wfst_get_lattice": [P, I32, P, I32, P, P, P, P, P, P, I64, P, P, I64, P, P, P],
+            "wfst_get_partial_paths": [P, P, I32, P, P, I32, P, P, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -324,6 +325,19 @@ class Decoder:
         k = int(n[0])
         return st[:k].copy(), ar[:k].copy(), co[:k].copy()
 
+
+    def partial_paths(self, streams=None, cap: int = 4096) -> dict:
+        """Row f2: the arcs/olabels settled since the previous call, per stream
+        (wfst_get_partial_paths), and the frames the settled prefix covers."""
+        ids = np.arange(self.n_streams, dtype=np.int32) if streams is None else _np(streams, np.int32)
+        n = ids.size
+        arcs = np.zeros((n, cap), np.int32)
+        ols = np.zeros((n, cap), np.int32)
+        nar, nol, fr = np.zeros(n, np.int32), np.zeros(n, np.int32), np.zeros(n, np.int32)
+        _check(lib().wfst_get_partial_paths(self.h, _ptr(ids), n, _ptr(arcs), _ptr(ols), cap, _ptr(nar), _ptr(nol),
+                                            _ptr(fr)))
+        return dict(arcs=[arcs[i, :nar[i]].copy() for i in range(n)], olabels=[ols[i, :nol[i]].copy() for i in range(n)],
+                    settled_frames=fr)
 
     def lattice(self, stream: int, arcs_cap: int = 1 << 20, layers_cap: int = 1 << 14,
                 gamma_cap: int = 1 << 22) -> dict:

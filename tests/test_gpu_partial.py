@@ -1,0 +1,81 @@
+"""Row f2 (NEXT): settled partial results on the GPU vs the oracle's settled prefix (reading
+R15), and SPEC's prefix consistency of mid-utterance best paths: after k frames
+the best path equals the oracle's decode of the k-frame prefix."""
+import math
+
+import numpy as np
+import pytest
+
+import bruteforce as BF
+from paper_1910_10032_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def W():
+    from paper_1910_10032_b200 import build, wfst_gpu
+    build.build()
+    return wfst_gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+@pytest.mark.parametrize("chunk,beam,alpha", [(10, 10.0, 300), (7, 12.0, 2000), (1, 10.0, 50)])
+def test_partial_paths_match_oracle(W, torch, oracle_mod, chunk, beam, alpha):
+    g = I.hclg_graph(3000, 6, 200, seed=4)
+    og = oracle_mod.OracleGraph(g)
+    emit = g.ilabel[BF.canonical_order(g)] != 0
+    T, B, P = 40, 6, 200
+    pl = I.planted_walks(g, B, T, seed=9)
+    ll = I.loglikes(77, range(B), T, P, pl, 1.0, 4.0)
+    G = W.Graph.from_arrays(g)
+    D = W.Decoder(G, B, beam, alpha)
+    D.reset()
+    t = torch.from_numpy(ll).cuda()
+    acc = [[] for _ in range(B)]
+    olab = [[] for _ in range(B)]
+    grew = 0
+    for t0 in range(0, T, chunk):
+        D.decode_frames(t[t0:t0 + chunk].contiguous())
+        pp = D.partial_paths(cap=4 * T + 64)
+        bp = D.best_paths(cap=4 * T + 64)
+        for b in range(B):
+            acc[b] += pp["arcs"][b].tolist()
+            olab[b] += pp["olabels"][b].tolist()
+            grew += len(pp["arcs"][b]) > 0
+            L = min(t0 + chunk, T)
+            want = og.settled_prefix(ll[:L, b, :], beam, alpha)
+            assert acc[b] == want.tolist(), (b, L)
+            assert pp["settled_frames"][b] == int(emit[want].sum()), (b, L)
+            # SPEC prefix consistency: the mid-utterance best path is the prefix decode's
+            r = og.decode(ll[:L, b, :], beam, alpha)
+            n = bp["n_arcs"][b]
+            assert list(bp["arcs"][b, :n]) == list(r.arcs) and bp["cost"][b] == r.cost32, (b, L)
+            assert acc[b] == list(bp["arcs"][b, :len(acc[b])])
+    assert grew > B
+    olc = g.olabel[BF.canonical_order(g)]
+    for b in range(B):
+        assert olab[b] == [int(x) for x in olc[acc[b]] if x != 0]
+
+
+def test_partial_paths_reset_restarts(W, torch):
+    g = I.hclg_graph(2000, 3, 50, seed=3)
+    G = W.Graph.from_arrays(g)
+    D = W.Decoder(G, 2, 10.0, 100)
+    pl = I.planted_walks(g, 2, 20, seed=2)
+    ll = torch.from_numpy(I.loglikes(5, range(2), 20, 50, pl, 1.0, 4.0)).cuda()
+    D.reset()
+    D.decode_frames(ll)
+    first = D.partial_paths()
+    assert D.partial_paths()["arcs"][0].size == 0          # nothing new since the last call
+    D.reset()
+    D.decode_frames(ll)
+    again = D.partial_paths()
+    for b in range(2):
+        assert np.array_equal(first["arcs"][b], again["arcs"][b])
