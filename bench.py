@@ -174,6 +174,8 @@ def decoder_opts(args) -> dict:
         v = getattr(args, k, 0)
         if v:
             o[k] = v
+    if getattr(args, "hist", False):   # row f4: the paper's histogram max-active instead of the exact one
+        o["max_active_mode"] = 1
     if getattr(args, "lattice", None) is not None:   # row f1: segments built inside every decode call
         o["lattice"] = 1
         o["lattice_beam"] = args.lattice
@@ -405,6 +407,8 @@ def main(argv=None):
     ap.add_argument("--chunk", type=int, default=25, help="frames per H2D chunk in the e2e leg")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch (from profiles/)")
     ap.add_argument("--threads", type=int, default=0, help="frame-kernel CTA size (default by variant)")
+    ap.add_argument("--hist", action="store_true",
+                    help="histogram max-active (row f4; approximate, not the headline)")
     ap.add_argument("--partial", action="store_true",
                     help="fetch settled partial results after every chunk (row f2; not the headline)")
     ap.add_argument("--lattice", type=float, default=None,

@@ -89,6 +89,9 @@ typedef struct {
   int32_t lattice;           /* 1: build lattice segments every frame (row f1)    */
   float lattice_beam;        /* lattice-beam (P:146 uses 8) when lattice = 1; may be 0 or +INF     */
   int64_t lattice_arcs_per_stream; /* segment arena per stream (default 2 x records_per_stream)   */
+  int32_t max_active_mode;   /* 0: exact alpha-th smallest (R6, default); 1: the paper's histogram
+                                adaptive beam (row f4, R16: 1024 bins of beam/1024 from the best,
+                                keep below the bin where the count reaches alpha)                */
 } wfst_decoder_opts_t;
 
 typedef struct {

@@ -53,6 +53,7 @@ def lib():
         L.oracle_graph_max_pdf.restype = I32
         L.oracle_decode.argtypes = [P, P, I64, I32, I32, F32, I32, P, P, P, I32, P, P, I32, P,
                                     P, P, P, P, P, P, I64, P]
+        L.oracle_decode_mode.argtypes = [P, P, I64, I32, I32, F32, I32, I32, P, P, P, I32, P, P, I32, P, P]
         L.oracle_decode_batch.argtypes = [P, P, I32, I32, I32, F32, I32, I32, P, P, P, P, P, I32, P]
         L.oracle_lattice.argtypes = [P, P, I64, I32, F32, F32, P, P, P, P, P, P, P, P, P, I64, P]
         L.oracle_lattice_finalize.argtypes = [P, I32, P, P, P, P, P, P, P, P, P, P, P, P]
@@ -186,6 +187,28 @@ class OracleGraph:
         r.lattice_best = float(best[0])
         r.lattice_beam = float(lattice_beam)
         return r
+
+    def decode_hist(self, ll: np.ndarray, beam: float, max_active: int) -> OracleResult:
+        """Row f4: decode with the histogram max-active rule R16 instead of the exact R6."""
+        ll = np.ascontiguousarray(ll, dtype=np.float32)
+        T, P = ll.shape
+        cost = np.zeros(1, np.float32)
+        rf = np.zeros(1, np.int32)
+        cap = 4 * (T + 1) + 64
+        arcs = np.zeros(cap, np.int32)
+        n_arcs = np.zeros(1, np.int32)
+        ol = np.zeros(cap, np.int32)
+        n_ol = np.zeros(1, np.int32)
+        fst = np.zeros((max(T, 1), 3), np.float32)
+        fcn = np.zeros((max(T, 1), 5), np.int64)
+        rc = lib().oracle_decode_mode(self.h, _p(ll) if T else None, P, T, P, float(beam), int(max_active), 1,
+                                      _p(cost), _p(rf), _p(arcs), cap, _p(n_arcs), _p(ol), cap, _p(n_ol),
+                                      _p(fst), _p(fcn))
+        if rc:
+            raise OracleError(rc, "decode_hist")
+        return OracleResult(cost=float(cost[0]), cost32=cost[0], reached_final=int(rf[0]),
+                            arcs=arcs[: n_arcs[0]].copy(), olabels=ol[: n_ol[0]].copy(),
+                            frame_stats=fst[:T].copy(), frame_counts=fcn[:T].copy())
 
     def settled_prefix(self, ll: np.ndarray, beam: float, max_active: int = 0) -> np.ndarray:
         """Row f2 (reading R15; "intermediate results during online decoding"): decode the

@@ -251,12 +251,38 @@ static int32_t layer_find(const Layer *L, int32_t q) {
  *   surv_n[T+1]                 survivors per layer (layer 0 = after init)
  *   surv_state/arc/cost[surv_cap] concatenated layers, sorted by state
  */
-int oracle_decode(void *gp, const float *ll, int64_t ll_stride, int32_t T, int32_t P, float beam,
-                  int32_t max_active, float *cost, int32_t *reached_final, int32_t *arcs,
-                  int32_t arcs_cap, int32_t *n_arcs, int32_t *olabels, int32_t ol_cap,
-                  int32_t *n_ol, float *fstats, int64_t *fcounts, int32_t *surv_n,
-                  int32_t *surv_state, int32_t *surv_arc, float *surv_cost, int64_t surv_cap,
-                  int64_t *eps_relax_total) {
+/* R16 (row f4, opt-in, NEXT): the paper's histogram max-active -- "Set Beam via max-active"
+ * (Fig. 1) implemented with a histogram whose thresholds are "somewhat arbitrary".
+ * Written out deterministically: NB bins of width wd = beam/NB over [best, best + beam),
+ * bin(c) = (int) clamp((c - best) * (NB/beam), 0, NB-1); b = the smallest bin whose cumulative
+ * in-beam count reaches alpha; adaptive cutoff ca = best + (b+1)*wd; keep c < ca (stored as
+ * kalpha = the largest float below ca, so keep() stays c <= kalpha).  fp32, this order. */
+#define HIST_NB 1024
+static float hist_cutoff(const float *cand, int32_t n, float best, float beam, int32_t alpha) {
+  int32_t h[HIST_NB];
+  memset(h, 0, sizeof h);
+  const float inv = (float)HIST_NB / beam, wd = beam / (float)HIST_NB;
+  for (int32_t i = 0; i < n; i++) {
+    float x = (cand[i] - best) * inv;
+    if (x > (float)(HIST_NB - 1)) x = (float)(HIST_NB - 1);
+    if (x < 0.0f) x = 0.0f;
+    h[(int)x]++;
+  }
+  int32_t b = 0, cum = 0;
+  for (b = 0; b < HIST_NB; b++) {
+    cum += h[b];
+    if (cum >= alpha) break;
+  }
+  const float ca = best + (float)(b + 1) * wd;
+  return nextafterf(ca, -INFINITY);
+}
+
+static int decode_impl(void *gp, const float *ll, int64_t ll_stride, int32_t T, int32_t P, float beam,
+                       int32_t max_active, int alpha_mode, float *cost, int32_t *reached_final,
+                       int32_t *arcs, int32_t arcs_cap, int32_t *n_arcs, int32_t *olabels,
+                       int32_t ol_cap, int32_t *n_ol, float *fstats, int64_t *fcounts,
+                       int32_t *surv_n, int32_t *surv_state, int32_t *surv_arc, float *surv_cost,
+                       int64_t surv_cap, int64_t *eps_relax_total) {
   const OGraph *g = (const OGraph *)gp;
   if (!g || T < 0 || (T > 0 && (!ll || P <= 0)) || !cost || !reached_final) return O_INVALID;
   if (T > 0 && P <= g->max_pdf) return O_PDF_RANGE;
@@ -310,10 +336,14 @@ int oracle_decode(void *gp, const float *ll, int64_t ll_stride, int32_t T, int32
     int32_t n_in = 0;
     for (int32_t i = 0; i < w.n_touched; i++)
       if (w.dcost[w.touched[i]] < k.beam_cut) w.tmp[n_in++] = w.dcost[w.touched[i]];
-    /* R6: exact max-active (alpha-th smallest in-beam cost) */
+    /* R6: exact max-active (alpha-th smallest in-beam cost); R16: the histogram variant */
     if (max_active > 0 && n_in > max_active) {
-      qsort(w.tmp, (size_t)n_in, 4, cmp_float);
-      k.kalpha = w.tmp[max_active - 1];
+      if (alpha_mode == 1) {
+        k.kalpha = hist_cutoff(w.tmp, n_in, best, beam, max_active);
+      } else {
+        qsort(w.tmp, (size_t)n_in, 4, cmp_float);
+        k.kalpha = w.tmp[max_active - 1];
+      }
       k.use_alpha = 1;
     }
     int32_t n_cand = w.n_touched;
@@ -400,6 +430,27 @@ int oracle_decode(void *gp, const float *ll, int64_t ll_stride, int32_t T, int32
 done:
   work_free(&w);
   return rc;
+}
+
+int oracle_decode(void *gp, const float *ll, int64_t ll_stride, int32_t T, int32_t P, float beam,
+                  int32_t max_active, float *cost, int32_t *reached_final, int32_t *arcs,
+                  int32_t arcs_cap, int32_t *n_arcs, int32_t *olabels, int32_t ol_cap,
+                  int32_t *n_ol, float *fstats, int64_t *fcounts, int32_t *surv_n,
+                  int32_t *surv_state, int32_t *surv_arc, float *surv_cost, int64_t surv_cap,
+                  int64_t *eps_relax_total) {
+  return decode_impl(gp, ll, ll_stride, T, P, beam, max_active, 0, cost, reached_final, arcs, arcs_cap,
+                     n_arcs, olabels, ol_cap, n_ol, fstats, fcounts, surv_n, surv_state, surv_arc,
+                     surv_cost, surv_cap, eps_relax_total);
+}
+
+/* Same with the max-active rule selected: 0 exact (R6), 1 histogram (R16). */
+int oracle_decode_mode(void *gp, const float *ll, int64_t ll_stride, int32_t T, int32_t P, float beam,
+                       int32_t max_active, int32_t alpha_mode, float *cost, int32_t *reached_final,
+                       int32_t *arcs, int32_t arcs_cap, int32_t *n_arcs, int32_t *olabels,
+                       int32_t ol_cap, int32_t *n_ol, float *fstats, int64_t *fcounts) {
+  return decode_impl(gp, ll, ll_stride, T, P, beam, max_active, alpha_mode, cost, reached_final, arcs,
+                     arcs_cap, n_arcs, olabels, ol_cap, n_ol, fstats, fcounts, NULL, NULL, NULL, NULL,
+                     0, NULL);
 }
 
 /* ---- row f1 (NEXT): lattice segments and the end-of-utterance lattice ----

@@ -470,6 +470,11 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.n_states = g->Q;
   kp.beam = beam;
   kp.alpha = d->alpha;
+  kp.amode = d->o.max_active_mode;
+  if (kp.amode != 0 && kp.amode != 1) {
+    wfst_decoder_destroy(d);
+    return fail(WFST_ERR_INVALID_ARG, "max_active_mode must be 0 (exact) or 1 (histogram)");
+  }
   kp.C = d->C;
   kp.NBK = d->C / 4;
   kp.C_ovf = d->C_ovf;

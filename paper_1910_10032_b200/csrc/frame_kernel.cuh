@@ -59,6 +59,7 @@ struct KParams {
   int32_t* lane_round;
   float beam;
   int32_t alpha;
+  int32_t amode;          // max-active rule: 0 exact (R6), 1 histogram (R16, row f4)
   int32_t C, NBK, C_ovf, FCAP;
   int32_t row_floats;     // log-likelihood columns staged on chip per frame (max pdf + 1)
   int32_t row_bytes;      // shared bytes reserved for the staged row
@@ -478,7 +479,8 @@ struct Frame {
       if (bin >= 0) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
     }
     const int end = base + __popc(m);
-    return p.alpha > 0 && end >= p.alpha && (end >> 10) != (base >> 10);
+    // (the histogram rule keeps candidates above the exact k_alpha: no early rejection then)
+    return p.alpha > 0 && p.amode == 0 && end >= p.alpha && (end >> 10) != (base >> 10);
   }
 
   // theta = smallest b such that >= alpha distinct states have first-insert bin < b (warp-collective)
@@ -777,6 +779,10 @@ struct Frame {
       __syncthreads();
       return;
     }
+    if (p.amode == 1) {
+      select_hist();
+      return;
+    }
     // exact alpha-th smallest in-beam cost by radix select on rk = ord(c) - ord(best) (every
     // entry is >= best), 10-bit digits from the top set bit of ord(beam_cut) - ord(best); the
     // first pass also counts the in-beam entries.
@@ -844,6 +850,56 @@ struct Frame {
       }
       shift = max(shift - 10, 0);
     }
+    for (int i = tid; i < kNB; i += BS) hist[i] = 0;
+    __syncthreads();
+  }
+
+  // ---- row f4 (NEXT): the paper's histogram max-active (Fig. 1; reading R16):
+  // one pass counts the in-beam entries into kNB bins of width beam/kNB over [best, best+beam);
+  // b = the first bin whose cumulative count reaches alpha; keep c < best + (b+1)*beam/kNB.
+  // Same fp32 operations as the oracle's hist_cutoff.
+  __device__ void select_hist() {
+    const int tid = threadIdx.x;
+    const float beam_cut = S.beam_cut;
+    const float best = float_of_ord(S.best_ord);
+    const float inv = __fdiv_rn((float)kNB, p.beam), wd = __fdiv_rn(p.beam, (float)kNB);
+    for (int i = tid; i < kNB; i += BS) hist[i] = 0;
+    __syncthreads();
+    long long cnt = 0;
+    scan_entries<4>([&](int, u64 v) {
+      const float c = key_cost(v);
+      if (v == kEmpty || !(c < beam_cut)) return;
+      cnt++;
+      float x = __fmul_rn(__fsub_rn(c, best), inv);
+      x = fmaxf(fminf(x, (float)(kNB - 1)), 0.0f);
+      red_add_s(hist_sa + 4u * (uint32_t)(int)x, 1);
+    });
+    const long long n_in = block_sum64<BS>(cnt, S.warp_tmp64);   // includes a barrier
+    if (tid < 32) {
+      const int lane = tid;
+      if (n_in > p.alpha) {   // warp 0: the bin where the cumulative count reaches alpha
+        int sum = 0;
+        for (int i = 0; i < 32; i++) sum += hist[lane * 32 + i];
+        const int incl = warp_incl_scan(sum);
+        const unsigned m = __ballot_sync(0xffffffffu, incl >= p.alpha);
+        const int L = __ffs(m) - 1;
+        if (lane == L) {
+          int c = incl - sum, d = lane * 32;
+          for (; d < lane * 32 + 31; d++) {
+            if (c + hist[d] >= p.alpha) break;
+            c += hist[d];
+          }
+          const float ca = __fadd_rn(best, __fmul_rn((float)(d + 1), wd));
+          S.kalpha = nextafterf(ca, -INFINITY);
+          S.use_alpha = 1;
+        }
+      } else if (lane == 0) {
+        S.use_alpha = 0;
+        S.kalpha = INFINITY;
+      }
+      if (lane == 0) S.n_in = (int)n_in;
+    }
+    __syncthreads();
     for (int i = tid; i < kNB; i += BS) hist[i] = 0;
     __syncthreads();
   }

@@ -44,7 +44,8 @@ class DecoderOpts(C.Structure):
     _fields_ = [("table_slots", C.c_int32), ("overflow_slots", C.c_int32), ("records_per_stream", C.c_int64),
                 ("max_frames", C.c_int32), ("threads", C.c_int32), ("frames_per_item", C.c_int32),
                 ("max_ctas", C.c_int32), ("debug_costs", C.c_int32), ("ctas_per_sm", C.c_int32),
-                ("lattice", C.c_int32), ("lattice_beam", C.c_float), ("lattice_arcs_per_stream", C.c_int64)]
+                ("lattice", C.c_int32), ("lattice_beam", C.c_float), ("lattice_arcs_per_stream", C.c_int64),
+                ("max_active_mode", C.c_int32)]
 
 
 class Stats(C.Structure):
