@@ -479,9 +479,13 @@ struct Frame {
       if (bin >= 0) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
     }
     const int end = base + __popc(m);
-    // (the histogram rule keeps candidates above the exact k_alpha: no early rejection then)
-    return p.alpha > 0 && p.amode == 0 && end >= p.alpha && (end >> 10) != (base >> 10);
+    return p.alpha > 0 && end >= p.alpha && (end >> 10) != (base >> 10);
   }
+
+  // Candidates in bins >= theta are provably above the exact k_alpha (R6).  The histogram rule
+  // (R16) cuts at most one histogram bin (beam/1024) above k_alpha, less than one max-active bin
+  // (2*beam/1024): its candidates are rejected two bins later, which keeps the test exact.
+  __device__ __forceinline__ int th_margin() const { return p.amode == 1 ? 2 : 0; }
 
   // theta = smallest b such that >= alpha distinct states have first-insert bin < b (warp-collective)
   __device__ void update_theta() {
@@ -522,7 +526,7 @@ struct Frame {
       // re-check against the bounds as they are now (both only tighten)
       const uint32_t bo = (uint32_t)lds32(best_sa);
       const bool ok = (bo == 0xFFFFFFFFu || float_of_ord(o) < __fadd_rn(float_of_ord(bo), beam)) &&
-                      bin < lds32(theta_sa);
+                      bin < lds32(theta_sa) + th_margin();
       if (ok) {
         if (o < bo) red_min_s32(best_sa, o);
         const uint32_t qf = (uint32_t)e.x | (flag << 31);   // state | has-epsilon flag
@@ -646,7 +650,7 @@ struct Frame {
           const float co = __shfl_sync(0xffffffffu, cost, own[u]);
           const float c = __fadd_rn(__fsub_rn(__fadd_rn(co, __int_as_float(arc[u].y)), L[u]), 0.0f);
           const int bin = bin_of(c, ref, inv_w);
-          const bool pass = v[u] && c < bound && bin < th;
+          const bool pass = v[u] && c < bound && bin < th + th_margin();
           const int4 entry = make_int4(arc[u].x, (int)ord_of(c), a[u], bin | (int)(arc[u].w & 0x80000000));
           stage(pass, entry, staged, beam, best_sa, theta_sa);
         }
@@ -683,7 +687,7 @@ struct Frame {
         for (int u = 0; u < R; u++) {
           const float c = __fadd_rn(__fsub_rn(__fadd_rn(cost, __int_as_float(arc[u].y)), L[u]), 0.0f);
           const int bin = bin_of(c, ref, inv_w);
-          const bool pass = v[u] && c < bound && bin < th;
+          const bool pass = v[u] && c < bound && bin < th + th_margin();
           const int j = j0 + u * BS + tid;
           const int4 entry = make_int4(arc[u].x, (int)ord_of(c), f.z + j, bin | (int)(arc[u].w & 0x80000000));
 #ifdef WFST_COUNT
