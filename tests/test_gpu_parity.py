@@ -324,3 +324,52 @@ def test_c4_large_graph_memory_and_chunks(W, torch, oracle_mod):
         assert res["reached_final"][b] == r.reached_final
         assert list(res["arcs"][b, :n]) == list(r.arcs)
         assert res["cost"][b] == r.cost32
+
+
+def test_c3_other_full_size_sampled(W, torch, oracle_mod):
+    """C3's alpha-saturated "other" preset (max-active binds every frame, 10k survivors) at full
+    size in the bench's launch configuration; sampled streams against the oracle, including the
+    per-frame cutoffs."""
+    import bench
+    res, ctx = bench.run_gpu_once("c3", "other", with_paths=True)
+    og = oracle_mod.OracleGraph(ctx["graph"])
+    c = I.CONFIGS["c3"]
+    for b in (3, 300):
+        ll = I.loglikes_stream(c["ll_seed"], b, c["frames"], c["n_pdfs"], ctx["planted"][:, b], **I.preset("other"))
+        r = og.decode(ll, c["beam"], c["max_active"])
+        n = res["n_arcs"][b]
+        assert list(res["arcs"][b, :n]) == list(r.arcs)
+        assert res["cost"][b] == r.cost32 and res["reached_final"][b] == r.reached_final
+
+
+def test_c5_online_chunks_full_size(W, torch, oracle_mod):
+    """C5 (BASELINE configs[4]) on one GPU: 4096 concurrent streams on C3's graph, 500 frames in
+    50-frame chunks, settled partial results fetched after every chunk (row f2); sampled streams
+    checked against the oracle (final path, and the settled prefix after each chunk)."""
+    import bench
+    wl = bench.make_workload("c5", "clean")
+    T, B, P = wl["T"], wl["B"], wl["P"]
+    G = W.Graph.from_arrays(wl["graph"])
+    D = W.Decoder(G, B, wl["beam"], wl["alpha"])
+    ll = bench.device_loglikes(W, torch, wl, "cuda:0")
+    og = oracle_mod.OracleGraph(wl["graph"])
+    c = wl["c"]
+    sample = (0, 2047, 4095)
+    llh = {b: I.loglikes_stream(c["ll_seed"], b, T, P, wl["planted"][:, b], **wl["preset"]) for b in sample}
+    D.reset()
+    acc = {b: [] for b in sample}
+    for t0 in range(0, T, c["chunk"]):
+        D.decode_frames(ll[t0:t0 + c["chunk"]])
+        pp = D.partial_paths(streams=list(sample), cap=4 * T + 64)
+        for i, b in enumerate(sample):
+            acc[b] += pp["arcs"][i].tolist()
+            if t0 in (0, 200, 450):
+                want = og.settled_prefix(llh[b][:t0 + c["chunk"]], wl["beam"], wl["alpha"])
+                assert acc[b] == want.tolist(), (b, t0)
+    res = D.best_paths(cap=4 * T + 64)
+    assert res["rc"] == 0
+    for b in sample:
+        r = og.decode(llh[b], wl["beam"], wl["alpha"])
+        n = res["n_arcs"][b]
+        assert list(res["arcs"][b, :n]) == list(r.arcs) and res["cost"][b] == r.cost32
+        assert acc[b] == list(r.arcs[:len(acc[b])]) and len(acc[b]) > 100
