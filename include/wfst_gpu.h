@@ -79,7 +79,7 @@ typedef struct {
   int32_t table_slots;       /* per-stream on-chip token table slots (default: all free smem)     */
   int32_t overflow_slots;    /* per-stream global overflow table slots (default max(32768, 4*alpha)) */
   int64_t records_per_stream;/* traceback records per stream (default sized from max_frames)      */
-  int32_t max_frames;        /* frames per utterance kept in per-frame stats (default 2048)       */
+  int32_t max_frames;        /* layers kept per stream (default 4096; a ring with opts.reclaim)   */
   int32_t threads;           /* CTA size of the frame kernel (256/512/1024; default 512 or 256)   */
   int32_t frames_per_item;   /* frames a CTA runs on one stream before re-queueing (default 16)  */
   int32_t max_ctas;          /* cap on persistent CTAs (default: #SMs)                            */
@@ -92,6 +92,11 @@ typedef struct {
   int32_t max_active_mode;   /* 0: exact alpha-th smallest (R6, default); 1: the paper's histogram
                                 adaptive beam (row f4, R16: 1024 bins of beam/1024 from the best,
                                 keep below the bin where the count reaches alpha)                */
+  int32_t reclaim;           /* 1: traceback GC (row f2): every wfst_get_partial_paths call releases
+                                the records and layers below the new settle point, so an unbounded
+                                stream needs only records_per_stream / max_frames for the frames
+                                since its paths last converged; wfst_get_best_path then returns the
+                                arcs AFTER the settled prefix.  Exclusive with lattice.             */
 } wfst_decoder_opts_t;
 
 typedef struct {

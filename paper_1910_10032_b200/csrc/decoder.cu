@@ -55,13 +55,15 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, 
     return;
   }
   const int4* Fc = p.front + (size_t)lane * 2 * p.FCAP + (size_t)L.cur * p.FCAP;
+  const int64_t lb0 = (uint32_t)L.layer_base % (uint32_t)p.R_cap;   // the last layer's first record (ring)
+  auto rix = [&](int i) { const int64_t x = lb0 + i; return x >= p.R_cap ? x - p.R_cap : x; };
   const int2* rec = p.rec + (size_t)lane * p.R_cap;
   const int2* linfo = p.layer_info + (size_t)lane * (p.TMAX + 1);
   u64 kf = kEmpty, ka = kEmpty;
   for (int i = tid; i < L.n_front; i += blockDim.x) {
     const int4 f = __ldcg(Fc + i);
     const float c = __int_as_float(f.y);
-    const u64 arc = (uint32_t)__ldcg(&rec[L.layer_base + i].x);  // -1 -> 0xFFFFFFFF sorts last (R9)
+    const u64 arc = (uint32_t)__ldcg(&rec[rix(i)].x);  // -1 -> 0xFFFFFFFF sorts last (R9)
     const float F = __int_as_float(__ldg(&p.state_info[f.x].w));
     if (F < INFINITY) kf = min(kf, ((u64)ord_of(__fadd_rn(c, F)) << 32) | arc);
     ka = min(ka, ((u64)ord_of(c) << 32) | arc);
@@ -90,7 +92,7 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, 
   const u64 kb = reached ? kf : ka;
   // the arc identifies the survivor uniquely within a layer
   for (int i = tid; i < L.n_front && kb != kEmpty; i += blockDim.x)
-    if ((uint32_t)__ldcg(&rec[L.layer_base + i].x) == (uint32_t)kb) s_idx = i;
+    if ((uint32_t)__ldcg(&rec[rix(i)].x) == (uint32_t)kb) s_idx = i;
   __syncthreads();
   if (kb == kEmpty || s_idx < 0) {
     if (tid == 0) {
@@ -105,7 +107,7 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, 
   if (tid == 0) {
     cost_out[li] = float_of_ord((uint32_t)(kb >> 32));
     reached_out[li] = reached ? 1 : 0;
-    s_arc = __ldcg(&rec[L.layer_base + s_idx].x);
+    s_arc = __ldcg(&rec[rix(s_idx)].x);
     s_layer = L.frames;
   }
   __syncthreads();
@@ -115,6 +117,9 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, 
   for (long long step = 0; step < max_steps; step++) {
     const int arc = s_arc;
     if (arc < 0) break;
+    // traceback GC (row f2): below the settle point the path was already handed out by
+    // wfst_get_partial_paths -- stop at the settled root (entered by an emitting arc)
+    if (s_layer == L.layer_floor && L.layer_floor > 0 && __ldg(&p.arcs[arc].z) >= 0) break;
     int src = 0, layer = 0;
     if (tid == 0) {
       const int4 a = __ldg(p.arcs + arc);
@@ -129,10 +134,12 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, 
     __syncthreads();
     const int want = s_arc;
     layer = s_layer;
-    const int2 info = __ldcg(&linfo[layer]);
+    const int2 info = __ldcg(&linfo[layer % (p.TMAX + 1)]);
     __syncthreads();
+    const int64_t r0 = (uint32_t)info.x % (uint32_t)p.R_cap;   // record ring (row f2 GC)
     for (int i = tid; i < info.y; i += blockDim.x) {
-      const int2 r = __ldcg(rec + info.x + i);
+      const int64_t ri = r0 + i;
+      const int2 r = __ldcg(rec + (ri >= p.R_cap ? ri - p.R_cap : ri));
       if (r.y == want) {
         s_idx = info.x + i;
         s_arc = r.x;
@@ -172,7 +179,7 @@ __global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, 
 // ---------------- host side ----------------
 // kernel variants: (threads per CTA, arcs in flight per lane, resident CTAs per SM)
 struct WfstVariant {
-  int bs, ctas;
+  int bs, ctas, am;
   void* fn;
   void (*launch)(int grid, size_t smem, cudaStream_t st, const KParams& kp);
 };
@@ -236,18 +243,19 @@ struct DeviceGuard {
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
-template <int BS, int R, int MINB>
+template <int BS, int R, int MINB, int AM>
 void launch_v(int grid, size_t smem, cudaStream_t st, const KParams& kp) {
-  frame_kernel<BS, R, MINB><<<grid, BS, smem, st>>>(kp);
+  frame_kernel<BS, R, MINB, AM><<<grid, BS, smem, st>>>(kp);
 }
-#define WFST_VARIANT(BS, R, MINB) {BS, MINB, (void*)frame_kernel<BS, R, MINB>, launch_v<BS, R, MINB>}
+#define WFST_VARIANT(BS, R, MINB, AM) {BS, MINB, AM, (void*)frame_kernel<BS, R, MINB, AM>, launch_v<BS, R, MINB, AM>}
 const WfstVariant kVariants[] = {
-    WFST_VARIANT(512, 4, 1), WFST_VARIANT(256, 4, 1), WFST_VARIANT(1024, 2, 1), WFST_VARIANT(256, 4, 2),
-    WFST_VARIANT(512, 2, 2), WFST_VARIANT(256, 2, 3), WFST_VARIANT(256, 2, 4),
+    WFST_VARIANT(512, 4, 1, 0), WFST_VARIANT(256, 4, 1, 0), WFST_VARIANT(1024, 2, 1, 0), WFST_VARIANT(256, 4, 2, 0),
+    WFST_VARIANT(512, 2, 2, 0), WFST_VARIANT(256, 2, 3, 0), WFST_VARIANT(256, 2, 4, 0),
+    WFST_VARIANT(1024, 2, 1, 1),   // histogram max-active (row f4): default launch shape only
 };
-const WfstVariant* find_variant(int bs, int ctas) {
+const WfstVariant* find_variant(int bs, int ctas, int am) {
   for (const WfstVariant& v : kVariants)
-    if (v.bs == bs && v.ctas == ctas) return &v;
+    if (v.bs == bs && v.ctas == ctas && v.am == am) return &v;
   return nullptr;
 }
 
@@ -337,10 +345,14 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   d->ctas_per_sm = d->o.ctas_per_sm > 0 ? d->o.ctas_per_sm : 1;
   d->n_scratch = d->o.max_ctas > 0 ? d->o.max_ctas : d->n_sm * d->ctas_per_sm;
   d->threads = d->o.threads > 0 ? d->o.threads : (d->ctas_per_sm == 1 ? 1024 : 256);
-  d->variant = find_variant(d->threads, d->ctas_per_sm);
+  if (d->o.max_active_mode != 0 && d->o.max_active_mode != 1) {
+    delete d;
+    return fail(WFST_ERR_INVALID_ARG, "max_active_mode must be 0 (exact) or 1 (histogram)");
+  }
+  d->variant = find_variant(d->threads, d->ctas_per_sm, d->o.max_active_mode);
   if (!d->variant) {
     delete d;
-    return fail(WFST_ERR_INVALID_ARG, "unsupported (threads, ctas_per_sm) combination");
+    return fail(WFST_ERR_INVALID_ARG, "unsupported (threads, ctas_per_sm, max_active_mode) combination");
   }
   // on-chip table: what is left of the SM's shared memory per resident CTA
   const size_t static_smem = sizeof(SmemCtl) + 4 * (size_t)d->threads + (size_t)(d->threads / 32) * kStage * 16 + 1024;
@@ -418,6 +430,10 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   size_t i_wl = add(NS * 2 * FC * 4);
   size_t i_rec = add(L * (size_t)d->R_cap * sizeof(int2));
   d->lattice = d->o.lattice != 0;
+  if (d->lattice && d->o.reclaim) {
+    delete d;
+    return fail(WFST_ERR_INVALID_ARG, "opts.lattice and opts.reclaim are exclusive (the lattice needs every layer)");
+  }
   if (d->lattice) {
     d->S_cap = d->o.lattice_arcs_per_stream > 0 ? d->o.lattice_arcs_per_stream : 2 * d->R_cap;
     if (!(d->o.lattice_beam >= 0.0f)) {
@@ -470,11 +486,6 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.n_states = g->Q;
   kp.beam = beam;
   kp.alpha = d->alpha;
-  kp.amode = d->o.max_active_mode;
-  if (kp.amode != 0 && kp.amode != 1) {
-    wfst_decoder_destroy(d);
-    return fail(WFST_ERR_INVALID_ARG, "max_active_mode must be 0 (exact) or 1 (histogram)");
-  }
   kp.C = d->C;
   kp.NBK = d->C / 4;
   kp.C_ovf = d->C_ovf;
@@ -897,19 +908,26 @@ wfst_status wfst_debug_layer(wfst_decoder_t d, int32_t stream, int32_t layer, in
   if (e == cudaSuccess) e = cudaMemcpy(&L, d->d_lanes + stream, sizeof L, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "debug layer");
   if (layer > L.frames) return fail(WFST_ERR_INVALID_ARG, "layer not decoded yet");
+  if (layer < L.layer_floor || L.frames - layer > d->TMAX) return fail(WFST_ERR_INVALID_ARG, "layer reclaimed");
   int2 info;
-  e = cudaMemcpy(&info, d->kp.layer_info + (size_t)stream * (d->TMAX + 1) + layer, sizeof info, cudaMemcpyDeviceToHost);
+  e = cudaMemcpy(&info, d->kp.layer_info + (size_t)stream * (d->TMAX + 1) + layer % (d->TMAX + 1), sizeof info,
+                 cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "debug layer");
   *n = info.y;
   if (info.y > cap) return fail(WFST_ERR_INVALID_ARG, "capacity too small");
   std::vector<int2> r(info.y);
   std::vector<float> c(info.y, NAN);
   if (info.y > 0) {
-    e = cudaMemcpy(r.data(), d->kp.rec + (size_t)stream * d->R_cap + info.x, sizeof(int2) * info.y,
-                   cudaMemcpyDeviceToHost);
+    // the layer's records may wrap around the end of the record ring
+    const int64_t r0 = (int64_t)info.x % d->R_cap, n1 = std::min<int64_t>(info.y, d->R_cap - r0);
+    const size_t lb = (size_t)stream * d->R_cap;
+    e = cudaMemcpy(r.data(), d->kp.rec + lb + r0, sizeof(int2) * n1, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && n1 < info.y)
+      e = cudaMemcpy(r.data() + n1, d->kp.rec + lb, sizeof(int2) * (info.y - n1), cudaMemcpyDeviceToHost);
     if (e == cudaSuccess && d->kp.rec_cost)
-      e = cudaMemcpy(c.data(), d->kp.rec_cost + (size_t)stream * d->R_cap + info.x, 4 * (size_t)info.y,
-                     cudaMemcpyDeviceToHost);
+      e = cudaMemcpy(c.data(), d->kp.rec_cost + lb + r0, 4 * (size_t)n1, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && d->kp.rec_cost && n1 < info.y)
+      e = cudaMemcpy(c.data() + n1, d->kp.rec_cost + lb, 4 * (size_t)(info.y - n1), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(e, "debug layer");
   }
   for (int i = 0; i < info.y; i++) {
@@ -1075,6 +1093,8 @@ wfst_status wfst_get_partial_paths(wfst_decoder_t d, const int32_t* streams, int
   pp.layer_info = d->kp.layer_info;
   pp.TMAX = d->TMAX;
   pp.settled = d->d_settled;
+  pp.reclaim = d->o.reclaim;
+  pp.lanes_rw = d->d_lanes;
   pp.cap = cp;
   pp.n_arcs_out = p + n;
   pp.n_olab_out = p + 2 * n;

@@ -40,11 +40,14 @@ struct LaneState {
   int32_t n_front;      // survivors in the current frontier (cost-bucketed order)
   int32_t cur;          // frontier buffer holding them
   int32_t frames;       // frames decoded in this utterance
-  int32_t layer_base;   // record index of the current layer's first survivor
-  int32_t rec_used;
+  int32_t layer_base;   // record index of the current layer's first survivor (logical)
+  int32_t rec_used;     // records written in this utterance (logical; physical = index % R_cap)
   float front_best;     // min cost of the current survivors
   u64 emit_arcs, eps_arcs, eps_relax, cand, surv, ovf, alpha_frames, frames_total;
   u64 phase[12];        // clock64 cycles per phase (see wfst_stats_t.phase_cycles)
+  int32_t rec_phys;     // rec_used % R_cap: the record ring slot of the next record
+  int32_t rec_floor;    // records below this are reclaimed (row f2 traceback GC; 0 otherwise)
+  int32_t layer_floor;  // layers below this are reclaimed (layer index ring of TMAX+1 entries)
 };
 
 struct KParams {
@@ -59,7 +62,6 @@ struct KParams {
   int32_t* lane_round;
   float beam;
   int32_t alpha;
-  int32_t amode;          // max-active rule: 0 exact (R6), 1 histogram (R16, row f4)
   int32_t C, NBK, C_ovf, FCAP;
   int32_t row_floats;     // log-likelihood columns staged on chip per frame (max pdf + 1)
   int32_t row_bytes;      // shared bytes reserved for the staged row
@@ -336,8 +338,9 @@ __device__ __forceinline__ long long block_sum64(long long v, long long* s_tmp) 
 }
 
 // ---------------- one lane's frames ----------------
-template <int BS, int R>
-struct Frame {
+template <int BS, int R, int AM>
+struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a template parameter so
+                 // the default kernel carries no code of the other mode
   static constexpr int NW = BS / 32;
   const KParams& p;
   SmemCtl& S;
@@ -485,7 +488,7 @@ struct Frame {
   // Candidates in bins >= theta are provably above the exact k_alpha (R6).  The histogram rule
   // (R16) cuts at most one histogram bin (beam/1024) above k_alpha, less than one max-active bin
   // (2*beam/1024): its candidates are rejected two bins later, which keeps the test exact.
-  __device__ __forceinline__ int th_margin() const { return p.amode == 1 ? 2 : 0; }
+  static constexpr int kThMargin = AM == 1 ? 2 : 0;
 
   // theta = smallest b such that >= alpha distinct states have first-insert bin < b (warp-collective)
   __device__ void update_theta() {
@@ -503,7 +506,7 @@ struct Frame {
         for (int i = 0; i < kNB / 32; i++) {
           c += lds32(hist_sa + 4u * (base + i));
           if (c >= p.alpha) {
-            atomicMin(&S.theta, base + i + 1);
+            atomicMin(&S.theta, base + i + 1 + kThMargin);
             break;
           }
         }
@@ -526,7 +529,7 @@ struct Frame {
       // re-check against the bounds as they are now (both only tighten)
       const uint32_t bo = (uint32_t)lds32(best_sa);
       const bool ok = (bo == 0xFFFFFFFFu || float_of_ord(o) < __fadd_rn(float_of_ord(bo), beam)) &&
-                      bin < lds32(theta_sa) + th_margin();
+                      bin < lds32(theta_sa);
       if (ok) {
         if (o < bo) red_min_s32(best_sa, o);
         const uint32_t qf = (uint32_t)e.x | (flag << 31);   // state | has-epsilon flag
@@ -650,7 +653,7 @@ struct Frame {
           const float co = __shfl_sync(0xffffffffu, cost, own[u]);
           const float c = __fadd_rn(__fsub_rn(__fadd_rn(co, __int_as_float(arc[u].y)), L[u]), 0.0f);
           const int bin = bin_of(c, ref, inv_w);
-          const bool pass = v[u] && c < bound && bin < th + th_margin();
+          const bool pass = v[u] && c < bound && bin < th;
           const int4 entry = make_int4(arc[u].x, (int)ord_of(c), a[u], bin | (int)(arc[u].w & 0x80000000));
           stage(pass, entry, staged, beam, best_sa, theta_sa);
         }
@@ -687,7 +690,7 @@ struct Frame {
         for (int u = 0; u < R; u++) {
           const float c = __fadd_rn(__fsub_rn(__fadd_rn(cost, __int_as_float(arc[u].y)), L[u]), 0.0f);
           const int bin = bin_of(c, ref, inv_w);
-          const bool pass = v[u] && c < bound && bin < th + th_margin();
+          const bool pass = v[u] && c < bound && bin < th;
           const int j = j0 + u * BS + tid;
           const int4 entry = make_int4(arc[u].x, (int)ord_of(c), f.z + j, bin | (int)(arc[u].w & 0x80000000));
 #ifdef WFST_COUNT
@@ -783,7 +786,7 @@ struct Frame {
       __syncthreads();
       return;
     }
-    if (p.amode == 1) {
+    if constexpr (AM == 1) {
       select_hist();
       return;
     }
@@ -1009,12 +1012,13 @@ struct Frame {
     mark(6);   // cursors ready
     const int n_ub = S.n_surv;
     const int32_t rb = S.L.rec_used;
-    if (n_ub > p.FCAP || (long long)rb + n_ub > p.R_cap) {
+    if (n_ub > p.FCAP || (long long)rb + n_ub - S.L.rec_floor > p.R_cap || (long long)rb + n_ub > INT32_MAX) {
       if (tid == 0) S.status = WFST_ERR_CAPACITY;
       __syncthreads();
       return;
     }
     const int app0 = S.pl_base[bc];
+    const int32_t rp = S.L.rec_phys;   // ring slot of the layer's first record
     float mn = INFINITY;
     // pass 2: drain the tables and place each survivor at its bucket cursor: frontier entry
     // (with the state's emitting range, prepared for the next frame: P:78) and traceback record
@@ -1058,8 +1062,9 @@ struct Frame {
         const int32_t arc = (uint32_t)(w[u] >> 32) == (uint32_t)(v[u] >> 32) ? (int32_t)(uint32_t)w[u] : -2;
         if (arc == -2) S.status = WFST_ERR_STATE;
         Fout[pos[u]] = make_int4((int)q, __float_as_int(c), si[u].x, si[u].y - si[u].x);
-        rec[rb + pos[u]] = make_int2(arc, (int)q);
-        if (rec_cost) rec_cost[rb + pos[u]] = c;
+        const int64_t r = (int64_t)rp + pos[u] - (rp + pos[u] >= p.R_cap ? p.R_cap : 0);   // record ring
+        rec[r] = make_int2(arc, (int)q);
+        if (rec_cost) rec_cost[r] = c;
         epsd += (unsigned long long)(si[u].z - si[u].y);
       }
     });
@@ -1124,6 +1129,8 @@ struct Frame {
       if (L.status == WFST_OK) {
         L.layer_base = L.rec_used;
         L.rec_used += n_surv;
+        L.rec_phys += n_surv;
+        if (L.rec_phys >= p.R_cap) L.rec_phys -= (int32_t)p.R_cap;
         L.n_front = n_surv;
         L.cur ^= 1;
         L.front_best = S.min_surv;
@@ -1144,9 +1151,9 @@ struct Frame {
           L.frames_total++;
         }
         const size_t lane = (size_t)S.lane;
-        if (layer <= p.TMAX) p.layer_info[lane * (p.TMAX + 1) + layer] = make_int2(L.layer_base, n_surv);
-        if (emitting && t >= 0 && L.frames - 1 < p.TMAX) {
-          const size_t fi = lane * p.TMAX + (L.frames - 1);
+        p.layer_info[lane * (p.TMAX + 1) + layer % (p.TMAX + 1)] = make_int2(L.layer_base, n_surv);
+        if (emitting && t >= 0) {
+          const size_t fi = lane * p.TMAX + (L.frames - 1) % p.TMAX;
           p.fstats[fi * 3 + 0] = float_of_ord(S.best_ord);
           p.fstats[fi * 3 + 1] = S.beam_cut;
           p.fstats[fi * 3 + 2] = S.use_alpha ? S.kalpha : INFINITY;
@@ -1172,6 +1179,9 @@ struct Frame {
       L.frames = 0;
       L.layer_base = 0;
       L.rec_used = 0;
+      L.rec_phys = 0;
+      L.rec_floor = 0;
+      L.layer_floor = 0;
       L.status = WFST_OK;
       L.initialized = 1;
       L.front_best = 0.0f;
@@ -1231,7 +1241,7 @@ struct Frame {
   // t_next < 0: no prefetch of the next frame's row
   __device__ void run_frame(int t, int t_next) {
     const int tid = threadIdx.x;
-    if (S.L.frames >= p.TMAX) {   // layer boundaries of longer utterances are not kept
+    if (S.L.frames - S.L.layer_floor >= p.TMAX) {   // the layer index ring is full
       if (tid == 0) S.L.status = WFST_ERR_CAPACITY;
       __syncthreads();
       return;
@@ -1278,7 +1288,7 @@ struct Frame {
   }
 };
 
-template <int BS, int R, int MINB>
+template <int BS, int R, int MINB, int AM>
 __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SmemCtl S;
@@ -1299,7 +1309,7 @@ __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
     mbar_init(saddr(&S.row_mbar), 1);
   }
   __syncthreads();
-  Frame<BS, R> fr(p, S, tab_sa, hist, s_wbuf + (tid & ~31), saddr(s_stage + (tid >> 5) * kStage), saddr(rowmem));
+  Frame<BS, R, AM> fr(p, S, tab_sa, hist, s_wbuf + (tid & ~31), saddr(s_stage + (tid >> 5) * kStage), saddr(rowmem));
   fr.bind_scratch();
   while (true) {
     if (tid == 0) S.item = atomicAdd(p.q_head, 1);

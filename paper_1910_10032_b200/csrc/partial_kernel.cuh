@@ -39,6 +39,8 @@ struct PartialParams {
   int32_t* status_out;      // [n]
   int32_t wcap;             // shared set capacity (slots)
   int32_t fcap;             // shared flag capacity (tokens of one layer)
+  int32_t reclaim;          // 1: records and layers below the new settle point are released
+  LaneState* lanes_rw;      // (same array as lanes_st; written only to move the floors)
 };
 
 __device__ __forceinline__ void pset_put(uint32_t* set, uint32_t cap, uint32_t q) {
@@ -70,12 +72,14 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
   const LaneState* Lp = p.lanes_st + ln;
   const int Lcur = __ldcg(&Lp->frames);
   const int2* rec = p.rec + (size_t)ln * p.R_cap;
-  const int2* linfo = p.layer_info + (size_t)ln * (p.TMAX + 1);
+  const int2* linfo_base = p.layer_info + (size_t)ln * (p.TMAX + 1);
+  auto linfo_at = [&](int k) { return linfo_base[k % (p.TMAX + 1)]; };   // layer index ring
+  auto R = [&](int64_t i) { return (uint32_t)i % (uint32_t)p.R_cap; };   // record ring (32-bit: R_cap < 2^31)
   const int2 prev = p.settled[ln];
   if (tid == 0) {
     s_status = __ldcg(&Lp->status) != WFST_OK ? __ldcg(&Lp->status)
                : !__ldcg(&Lp->initialized)    ? WFST_ERR_STATE
-               : Lcur > p.TMAX                ? WFST_ERR_CAPACITY
+               : Lcur - __ldcg(&Lp->layer_floor) > p.TMAX ? WFST_ERR_CAPACITY
                                               : WFST_OK;
     s_len = 0;
   }
@@ -94,7 +98,7 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
   }
   // ---- walk back from the current layer to the deepest single root
   int k = Lcur;
-  int2 Lk = linfo[k];
+  int2 Lk = linfo_at(k);
   if (Lk.y > p.fcap) {
     if (tid == 0) {
       s_status = WFST_ERR_CAPACITY;
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
       __syncthreads();
       for (int i = tid; i < Lk.y; i += BS) {
         if (!flag[i]) continue;
-        const int a = __ldcg(&rec[Lk.x + i].x);
+        const int a = __ldcg(&rec[R((int64_t)Lk.x + i)].x);
         if (a >= 0 && __ldg(&p.arcs[a].z) < 0) {
           pset_put(set, (uint32_t)p.wcap, (uint32_t)(__ldg(&p.arcs[a].w) & 0x7FFFFFFF));
           s_nw = 1;
@@ -127,7 +131,7 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
       __syncthreads();
       if (!s_nw) break;
       for (int i = tid; i < Lk.y; i += BS)
-        if (!flag[i] && pset_has(set, (uint32_t)p.wcap, (uint32_t)__ldcg(&rec[Lk.x + i].y))) {
+        if (!flag[i] && pset_has(set, (uint32_t)p.wcap, (uint32_t)__ldcg(&rec[R((int64_t)Lk.x + i)].y))) {
           flag[i] = 1;
           s_changed = 1;
         }
@@ -142,7 +146,7 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
     __syncthreads();
     for (int i = tid; i < Lk.y; i += BS) {
       if (!flag[i]) continue;
-      const int a = __ldcg(&rec[Lk.x + i].x);
+      const int a = __ldcg(&rec[R((int64_t)Lk.x + i)].x);
       if (a < 0 || __ldg(&p.arcs[a].z) >= 0) {
         atomicAdd(&s_roots, 1);
         s_root = Lk.x + i;
@@ -158,18 +162,18 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
     __syncthreads();
     for (int i = tid; i < Lk.y; i += BS) {
       if (!flag[i]) continue;
-      const int a = __ldcg(&rec[Lk.x + i].x);
+      const int a = __ldcg(&rec[R((int64_t)Lk.x + i)].x);
       if (a >= 0 && __ldg(&p.arcs[a].z) >= 0)
         pset_put(set, (uint32_t)p.wcap, (uint32_t)(__ldg(&p.arcs[a].w) & 0x7FFFFFFF));
     }
     __syncthreads();
     k--;
-    Lk = linfo[k];
+    Lk = linfo_at(k);
     if (Lk.y > p.fcap) {
       if (tid == 0) s_status = WFST_ERR_CAPACITY;
       break;
     }
-    for (int i = tid; i < Lk.y; i += BS) flag[i] = pset_has(set, (uint32_t)p.wcap, (uint32_t)__ldcg(&rec[Lk.x + i].y));
+    for (int i = tid; i < Lk.y; i += BS) flag[i] = pset_has(set, (uint32_t)p.wcap, (uint32_t)__ldcg(&rec[R((int64_t)Lk.x + i)].y));
     __syncthreads();
   }
   __syncthreads();
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
   while (true) {
     const int idx = s_idx;
     if (idx == stop) break;
-    const int arc = __ldcg(&rec[idx].x);
+    const int arc = __ldcg(&rec[R(idx)].x);
     if (arc < 0) break;   // the start token
     __syncthreads();
     if (tid == 0) {
@@ -204,10 +208,10 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
       s_idx = -1;
     }
     __syncthreads();
-    const int2 info = linfo[s_layer];
+    const int2 info = linfo_at(s_layer);
     const int want = s_arc;
     for (int i = tid; i < info.y; i += BS)
-      if (__ldcg(&rec[info.x + i].y) == want) s_idx = info.x + i;
+      if (__ldcg(&rec[R((int64_t)info.x + i)].y) == want) s_idx = info.x + i;
     __syncthreads();
     if (s_idx < 0) {
       if (tid == 0) s_status = WFST_ERR_STATE;
@@ -228,7 +232,13 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
       if (ol != 0) p.olab_out[(size_t)blockIdx.x * p.cap + nol++] = ol;
     }
     p.n_olab_out[blockIdx.x] = nol;
-    if (s_status == WFST_OK && s_len <= p.cap) p.settled[ln] = make_int2(k, root);
+    if (s_status == WFST_OK && s_len <= p.cap) {
+      p.settled[ln] = make_int2(k, root);
+      if (p.reclaim) {   // traceback GC: everything below the settle point is handed out
+        p.lanes_rw[ln].rec_floor = linfo_at(k).x;
+        p.lanes_rw[ln].layer_floor = k;
+      }
+    }
     if (s_status == WFST_OK && s_len > p.cap) s_status = WFST_ERR_INVALID_ARG;
   }
   __syncthreads();

@@ -79,3 +79,45 @@ def test_partial_paths_reset_restarts(W, torch):
     again = D.partial_paths()
     for b in range(2):
         assert np.array_equal(first["arcs"][b], again["arcs"][b])
+
+
+def test_reclaim_unbounded_stream(W, torch, oracle_mod):
+    """Traceback GC (second half of row f2): 600 frames through a 64-layer index ring and a
+    record ring of ~60 frames, partial results every 20 frames.  The partial outputs followed by
+    the final best path (which then starts at the settle point) equal the oracle's one-best
+    path; the same decoder without reclaim runs out of layers."""
+    g = I.hclg_graph(3000, 6, 200, seed=4)
+    og = oracle_mod.OracleGraph(g)
+    T, B, P, beam, alpha = 600, 4, 200, 10.0, 300
+    pl = I.planted_walks(g, B, T, seed=9)
+    ll = I.loglikes(77, range(B), T, P, pl, 1.0, 4.0)
+    G = W.Graph.from_arrays(g)
+    t = torch.from_numpy(ll).cuda()
+    opts = dict(max_frames=64, records_per_stream=60 * 1200)
+    D = W.Decoder(G, B, beam, alpha, reclaim=1, **opts)
+    D.reset()
+    acc = [[] for _ in range(B)]
+    for t0 in range(0, T, 20):
+        D.decode_frames(t[t0:t0 + 20].contiguous())
+        pp = D.partial_paths(cap=4 * T)
+        for b in range(B):
+            acc[b] += pp["arcs"][b].tolist()
+    res = D.best_paths(cap=4 * T + 64)
+    assert res["rc"] == 0
+    for b in range(B):
+        r = og.decode(ll[:, b, :], beam, alpha)
+        tail = list(res["arcs"][b, :res["n_arcs"][b]])
+        assert acc[b] + tail == list(r.arcs), b
+        assert res["cost"][b] == r.cost32 and len(tail) < len(r.arcs) // 4
+    D2 = W.Decoder(G, B, beam, alpha, **opts)
+    D2.reset()
+    for t0 in range(0, T, 20):
+        D2.decode_frames(t[t0:t0 + 20].contiguous())
+    assert D2.best_paths(cap=4 * T + 64, raise_on_error=False)["rc"] == 6   # CAPACITY
+
+
+def test_reclaim_excludes_lattice(W):
+    g = I.hclg_graph(2000, 3, 50, seed=1)
+    G = W.Graph.from_arrays(g)
+    with pytest.raises(W.WfstError):
+        W.Decoder(G, 2, 10.0, 100, reclaim=1, lattice=1, lattice_beam=8.0)
