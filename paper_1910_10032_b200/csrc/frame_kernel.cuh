@@ -85,7 +85,8 @@ struct SmemCtl {
   int32_t item, lane, b, status;
   uint32_t best_ord;
   int32_t theta;
-  int32_t n_claim, n_claim_emit, n_ovf, n_oclaim, n_surv, n_in, n_wl, n_wl_next, n_big, next_group;
+  int32_t n_claim, n_claim_emit, n_ovf, n_oclaim, n_surv, n_in, n_wl, n_big, next_group;
+  int32_t wlc[3];   // epsilon worklist counters (rotating)
   int32_t pl[kPlace];        // placement histogram: live entries per coarse cost bin
   int32_t pl_base[kPlace];   // placement cursors
   int32_t n_app;             // survivors appended in the cutoff's bin
@@ -917,15 +918,21 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
     // seed: the emitting phase listed every claimed state with epsilon arcs (flag in bit 31 of
     // the state word) in worklist 0; the ones the cutoff drops are skipped below
+    // Worklist counters rotate over three words: iteration i reads wlc[i%3], appends to
+    // wlc[(i+1)%3] and clears wlc[(i+2)%3] (read in iteration i-1, appended to in i+1), so one
+    // barrier per iteration suffices.
+    if (tid == 0) {
+      S.wlc[0] = S.n_wl;
+      S.wlc[1] = S.wlc[2] = 0;
+    }
     __syncthreads();
-    int cur = 0;
+    int cur = 0, r = 0;
     long long relax = 0;
     while (true) {
-      const int n_wl = S.n_wl;
+      const int n_wl = min(S.wlc[r], p.FCAP);
       if (n_wl == 0) break;
-      __syncthreads();
-      if (tid == 0) S.n_wl_next = 0;
-      __syncthreads();
+      const int rn = r == 2 ? 0 : r + 1;
+      if (tid == 0) S.wlc[rn == 2 ? 0 : rn + 1] = 0;
       const uint32_t* W = wl0 + (size_t)cur * p.FCAP;
       uint32_t* Wn = wl0 + (size_t)(cur ^ 1) * p.FCAP;
       for (int i0 = 0; i0 < n_wl; i0 += BS) {
@@ -966,7 +973,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
           const uint32_t has_eps = (uint32_t)arc.w >> 31;
           add_claim(slot, claimed, has_eps, -1, false);
           const bool push = strict && has_eps;
-          const int wi = warp_append(push, saddr(&S.n_wl_next));
+          const int wi = warp_append(push, saddr(&S.wlc[rn]));
           if (push) {
             if (wi < p.FCAP) Wn[wi] = (uint32_t)slot;
             else S.status = WFST_ERR_CAPACITY;
@@ -974,9 +981,8 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         }
       }
       __syncthreads();
-      if (tid == 0) S.n_wl = min(S.n_wl_next, p.FCAP);
       cur ^= 1;
-      __syncthreads();
+      r = rn;
     }
     {
       const unsigned long long wsum = warp_sum64((unsigned long long)relax);
@@ -996,17 +1002,22 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     // only survivors and no survivor lies above bc: their counts give exact cursors, and the
     // survivors of bin bc are appended after them.  One pass over the table, no counting pass.
     const int bc = min(pbin(cut_b), pbin(cut_a));
-    if (tid == 0) {
-      int acc = 0;
-      for (int b = 0; b < bc; b++) {
-        S.pl_base[b] = acc;
-        acc += S.pl[b];
+    static_assert(kPlace == 64, "warp 0 scans two placement bins per lane");
+    if (tid < 32) {   // exclusive scan of the bins below bc (per-frame critical path: no serial loop)
+      const int b0 = 2 * lane, b1 = b0 + 1;
+      const int c0 = b0 < bc ? S.pl[b0] : 0, c1 = b1 < bc ? S.pl[b1] : 0;
+      const int incl = warp_incl_scan(c0 + c1);
+      const int excl = incl - c0 - c1;
+      if (b0 < bc) S.pl_base[b0] = excl;
+      if (b1 < bc) S.pl_base[b1] = excl + c0;
+      const int acc = __shfl_sync(0xffffffffu, incl, 31);
+      if (lane == 0) {
+        S.pl_base[bc] = acc;
+        S.n_surv = acc + S.pl[bc];   // upper bound until the appended count is known
+        S.n_app = 0;
+        S.min_surv = INFINITY;
+        S.warp_tmp[0] = -1;   // min survivor cost, orderable (0xFFFFFFFF: none)
       }
-      S.pl_base[bc] = acc;
-      S.n_surv = acc + S.pl[bc];   // upper bound until the appended count is known
-      S.n_app = 0;
-      S.min_surv = INFINITY;
-      S.warp_tmp[0] = -1;   // min survivor cost, orderable (0xFFFFFFFF: none)
     }
     __syncthreads();
     mark(6);   // cursors ready
