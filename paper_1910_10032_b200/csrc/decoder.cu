@@ -204,7 +204,17 @@ struct wfst_decoder_s {
   size_t pool_bytes = 0;
   int32_t* d_qhead = nullptr;
   int32_t* d_round = nullptr;
-  int32_t* d_lane_ids = nullptr;   // batch -> lane (n_lanes capacity)
+  int32_t* d_lane_ids = nullptr;   // batch -> lane of the work being enqueued (a slot of the ring)
+  // channel -> lane mappings (row f3): a ring of kIdRing device buffers filled from pinned host
+  // memory by stream-ordered copies, so a call on a different subset of streams does not
+  // synchronise the device; a slot is reused only after the work that read it has finished
+  static constexpr int kIdRing = 8;
+  int32_t* d_id_ring = nullptr;
+  int32_t* h_id_ring = nullptr;
+  cudaEvent_t ev_ids[kIdRing] = {};   // after the last work that read the slot
+  cudaEvent_t ev_up[kIdRing] = {};    // after the slot's upload
+  cudaStream_t ids_stream = nullptr;  // stream of the last call
+  int id_slot = 0;
   int32_t* d_path = nullptr;       // best-path scratch
   size_t path_cap = 0;
   float* d_host_stage[2] = {nullptr, nullptr};
@@ -463,7 +473,13 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   if (e == cudaSuccess) e = cudaMalloc(&d->d_lanes, sizeof(LaneState) * L);
   if (e == cudaSuccess) e = cudaMalloc(&d->d_qhead, 4);
   if (e == cudaSuccess) e = cudaMalloc(&d->d_round, 4 * L);
-  if (e == cudaSuccess) e = cudaMalloc(&d->d_lane_ids, 4 * L);
+  if (e == cudaSuccess) e = cudaMalloc(&d->d_id_ring, 4 * L * wfst_decoder_s::kIdRing);
+  if (e == cudaSuccess) e = cudaMallocHost(&d->h_id_ring, 4 * L * wfst_decoder_s::kIdRing);
+  for (int k = 0; k < wfst_decoder_s::kIdRing && e == cudaSuccess; k++)
+    e = cudaEventCreateWithFlags(&d->ev_ids[k], cudaEventDisableTiming);
+  for (int k = 0; k < wfst_decoder_s::kIdRing && e == cudaSuccess; k++)
+    e = cudaEventCreateWithFlags(&d->ev_up[k], cudaEventDisableTiming);
+  if (e == cudaSuccess) d->d_lane_ids = d->d_id_ring;
   if (e == cudaSuccess) e = cudaMalloc(&d->d_settled, sizeof(int2) * L);
   if (e == cudaSuccess) e = cudaMemset(d->d_settled, 0xFF, sizeof(int2) * L);
   if (e != cudaSuccess) {
@@ -471,7 +487,8 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     cudaFree(d->d_lanes);
     cudaFree(d->d_qhead);
     cudaFree(d->d_round);
-    cudaFree(d->d_lane_ids);
+    cudaFree(d->d_id_ring);
+    cudaFreeHost(d->h_id_ring);
     delete d;
     return cuda_fail(e, "decoder allocation");
   }
@@ -568,7 +585,12 @@ void wfst_decoder_destroy(wfst_decoder_t d) {
   cudaFree(d->d_lanes);
   cudaFree(d->d_qhead);
   cudaFree(d->d_round);
-  cudaFree(d->d_lane_ids);
+  cudaFree(d->d_id_ring);
+  if (d->h_id_ring) cudaFreeHost(d->h_id_ring);
+  for (int k = 0; k < wfst_decoder_s::kIdRing; k++)
+    if (d->ev_ids[k]) cudaEventDestroy(d->ev_ids[k]);
+  for (int k = 0; k < wfst_decoder_s::kIdRing; k++)
+    if (d->ev_up[k]) cudaEventDestroy(d->ev_up[k]);
   cudaFree(d->d_path);
   cudaFree(d->d_host_stage[0]);
   cudaFree(d->d_host_stage[1]);
@@ -598,13 +620,29 @@ static wfst_status set_lanes(wfst_decoder_t d, const int32_t* streams, int32_t B
     if (require_init && !d->h_initialized[s]) return fail(WFST_ERR_STATE, "stream " + std::to_string(s) + " not reset");
     ids[i] = s;
   }
-  if (ids == d->cur_ids) return WFST_OK;  // same mapping as the work already queued
-  // the buffer may be in use by queued kernels: wait for them before replacing it
-  cudaError_t e = cudaDeviceSynchronize();
-  if (e == cudaSuccess) e = cudaMemcpy(d->d_lane_ids, ids.data(), 4 * (size_t)B, cudaMemcpyHostToDevice);
+  if (ids == d->cur_ids) {   // same mapping as the work already queued
+    if (st != d->ids_stream) {   // another stream: order it after the slot's upload
+      cudaError_t e = cudaStreamWaitEvent(st, d->ev_up[d->id_slot], 0);
+      if (e != cudaSuccess) return cuda_fail(e, "lane ids event");
+      d->ids_stream = st;
+    }
+    return WFST_OK;
+  }
+  // next ring slot: wait only for the (old) work that read it, then a stream-ordered upload
+  const int k = (d->id_slot + 1) % wfst_decoder_s::kIdRing;
+  cudaError_t e = cudaEventSynchronize(d->ev_ids[k]);
+  int32_t* h = d->h_id_ring + (size_t)k * d->n_lanes;
+  int32_t* dv = d->d_id_ring + (size_t)k * d->n_lanes;
+  if (e == cudaSuccess) {
+    memcpy(h, ids.data(), 4 * (size_t)B);
+    e = cudaMemcpyAsync(dv, h, 4 * (size_t)B, cudaMemcpyHostToDevice, st);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(d->ev_up[k], st);
   if (e != cudaSuccess) return cuda_fail(e, "lane ids upload");
+  d->id_slot = k;
+  d->d_lane_ids = dv;
   d->cur_ids = ids;
-  (void)st;
+  d->ids_stream = st;
   return WFST_OK;
 }
 
@@ -634,7 +672,8 @@ wfst_status wfst_decoder_reset(wfst_decoder_t d, const int32_t* streams, int32_t
     if (e != cudaSuccess) return cuda_fail(e, "lattice launch");
   }
   for (int32_t i = 0; i < B; i++) d->h_initialized[streams ? streams[i] : i] = 1;
-  return WFST_OK;
+  e = cudaEventRecord(d->ev_ids[d->id_slot], st);   // the slot is free once this work is done
+  return e == cudaSuccess ? WFST_OK : cuda_fail(e, "event");
 }
 
 wfst_status wfst_decode_frames(wfst_decoder_t d, const float* d_loglikes, int32_t T, int32_t B, int32_t P,
@@ -670,7 +709,8 @@ wfst_status wfst_decode_frames(wfst_decoder_t d, const float* d_loglikes, int32_
     e = launch_lattice(d, d_loglikes, T, B, P, kModeFrames, st);
     if (e != cudaSuccess) return cuda_fail(e, "lattice launch");
   }
-  return WFST_OK;
+  e = cudaEventRecord(d->ev_ids[d->id_slot], st);   // the slot is free once this work is done
+  return e == cudaSuccess ? WFST_OK : cuda_fail(e, "event");
 }
 
 static cudaError_t ensure_copy_stream(wfst_decoder_t d) {
