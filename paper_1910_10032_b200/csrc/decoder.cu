@@ -314,7 +314,7 @@ cudaError_t launch_lattice(wfst_decoder_t d, const float* ll, int32_t T, int32_t
   }
   if (e == cudaSuccess) e = cudaMemsetAsync(d->d_lat_q, 0, 4, st);
   if (e != cudaSuccess) return e;
-  lattice_kernel<1024><<<std::min(d->lat_grid, lp.n_items), 1024, d->lat_smem, st>>>(lp);
+  lattice_kernel<kLatBS, kLatCtas><<<std::min(d->lat_grid, lp.n_items), kLatBS, d->lat_smem, st>>>(lp);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaEventRecord(d->ev_lat, st);
   return e;
@@ -454,7 +454,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   size_t i_rcost = (d->o.debug_costs || d->lattice) ? add(L * (size_t)d->R_cap * 4) : (size_t)-1;
   // lattice: arena {arc, src, dst, slack} + path slack per entry, cursor, segment index, status,
   // gamma per record; fallback token maps of the lattice CTAs for layers beyond shared memory
-  const size_t NLAT = d->lattice ? (size_t)d->n_sm : 0;
+  const size_t NLAT = d->lattice ? (size_t)d->n_sm * kLatCtas : 0;
   const int64_t lat_gcap = 2 * (int64_t)d->FCAP + 32;
   size_t i_seg = d->lattice ? add(L * (size_t)d->S_cap * sizeof(int4)) : 0;
   size_t i_psl = d->lattice ? add(L * (size_t)d->S_cap * 4) : 0;
@@ -547,11 +547,12 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     lp.stage_cap = (int32_t)lat_stage;
     lp.FCAP = d->FCAP;
     d->lat_grid = (int)NLAT;
-    d->lat_smem = std::min((size_t)prop.sharedMemPerBlockOptin, (size_t)220 * 1024);
+    d->lat_smem = std::min((size_t)prop.sharedMemPerBlockOptin, (size_t)(220 / kLatCtas) * 1024);
     lp.smem_bytes = (int32_t)d->lat_smem;
     d->kp_pslack = (float*)(base + parts[i_psl].off);
     d->kp_gamma = (uint32_t*)(base + parts[i_gam].off);
-    e = cudaFuncSetAttribute(lattice_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d->lat_smem);
+    e = cudaFuncSetAttribute(lattice_kernel<kLatBS, kLatCtas>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)d->lat_smem);
     if (e == cudaSuccess) e = cudaMalloc(&d->d_lat_q, 4);
     if (e == cudaSuccess) e = cudaMalloc(&d->d_lat_lane, 4);
     if (e == cudaSuccess) e = cudaMalloc(&d->d_lat_out, 16);

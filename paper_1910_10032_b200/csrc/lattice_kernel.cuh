@@ -86,9 +86,18 @@ __device__ int block_excl_scan(int x, int* s_tmp /* 33 ints */, int& total) {
 }
 
 constexpr int kLatBig = 64, kLatBigCap = 64;   // tokens with more arcs are expanded CTA-wide
+constexpr int kLatU = 4;                        // arcs in flight per thread
 
-template <int BS>
-__global__ void __launch_bounds__(BS, 1) lattice_kernel(LatParams p) {
+#ifndef WFST_LAT_BS
+#define WFST_LAT_BS 1024
+#endif
+#ifndef WFST_LAT_CTAS
+#define WFST_LAT_CTAS 1
+#endif
+constexpr int kLatBS = WFST_LAT_BS, kLatCtas = WFST_LAT_CTAS;   // lattice CTA size, CTAs per SM
+
+template <int BS, int MINB>
+__global__ void __launch_bounds__(BS, MINB) lattice_kernel(LatParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_item, s_skip, s_err, s_scan[33], s_nbig, s_nst, s_big[kLatBigCap];
   __shared__ long long s_base;
@@ -165,12 +174,11 @@ __global__ void __launch_bounds__(BS, 1) lattice_kernel(LatParams p) {
     const int n_src = n_e + n_k;
     // one arc: R1 cost, keep(), destination token, extra cost; staged with its group count
     // (warp-collective: every lane calls it, v = the lane has an arc)
-    auto proc = [&](bool v, int a, float co, int u) {
+    auto proc = [&](bool v, int a, const int4& arc, float co, int u) {   // arc preloaded (MLP)
       bool ok = false;
       int jt = -1;
       float s = 0.f;
       if (v) {
-        const int4 arc = __ldg(p.arcs + a);
         const bool em = arc.z >= 0;
         const float c = em ? __fadd_rn(__fsub_rn(__fadd_rn(co, __int_as_float(arc.y)), rowp[arc.z]), 0.0f)
                            : __fadd_rn(__fadd_rn(co, __int_as_float(arc.y)), 0.0f);
@@ -214,20 +222,29 @@ __global__ void __launch_bounds__(BS, 1) lattice_kernel(LatParams p) {
       }
       const int incl = warp_incl_scan(deg);
       const int total = __shfl_sync(0xffffffffu, incl, 31);
-      for (int j0 = 0; j0 < total; j0 += 32) {
-        const int j = j0 + lane;
-        // owner = first lane whose inclusive prefix exceeds j (binary search over the warp)
-        int lo_l = 0;
+      for (int j0 = 0; j0 < total; j0 += 32 * kLatU) {
+        int a[kLatU], own[kLatU];
+        float co_o[kLatU];
+        int4 arc[kLatU];
 #pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const int v = __shfl_sync(0xffffffffu, incl, lo_l + step - 1);
-          if (v <= j) lo_l += step;
+        for (int x = 0; x < kLatU; x++) {
+          const int j = j0 + x * 32 + lane;
+          // owner = first lane whose inclusive prefix exceeds j (binary search over the warp)
+          int lo_l = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int v = __shfl_sync(0xffffffffu, incl, lo_l + step - 1);
+            if (v <= j) lo_l += step;
+          }
+          own[x] = min(lo_l, 31);
+          const int ex_o = __shfl_sync(0xffffffffu, incl - deg, own[x]);
+          const int eb_o = __shfl_sync(0xffffffffu, e0, own[x]);
+          co_o[x] = __shfl_sync(0xffffffffu, co, own[x]);
+          a[x] = eb_o + (j - ex_o);
+          arc[x] = j < total ? __ldg(p.arcs + a[x]) : make_int4(0, 0, 0, 0);   // all loads first
         }
-        const int own = min(lo_l, 31);
-        const int ex_o = __shfl_sync(0xffffffffu, incl - deg, own);
-        const int eb_o = __shfl_sync(0xffffffffu, e0, own);
-        const float co_o = __shfl_sync(0xffffffffu, co, own);
-        proc(j < total, eb_o + (j - ex_o), co_o, u0 + own);
+#pragma unroll
+        for (int x = 0; x < kLatU; x++) proc(j0 + x * 32 + lane < total, a[x], arc[x], co_o[x], u0 + own[x]);
       }
     }
     __syncthreads();
@@ -237,7 +254,16 @@ __global__ void __launch_bounds__(BS, 1) lattice_kernel(LatParams p) {
       int e0, deg;
       float co;
       src_of(u, e0, deg, co);
-      for (int j0 = 0; j0 < deg; j0 += BS) proc(j0 + tid < deg, e0 + j0 + tid, co, u);
+      for (int j0 = 0; j0 < deg; j0 += BS * kLatU) {
+        int4 arc[kLatU];
+#pragma unroll
+        for (int y = 0; y < kLatU; y++) {
+          const int j = j0 + y * BS + tid;
+          arc[y] = j < deg ? __ldg(p.arcs + e0 + j) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int y = 0; y < kLatU; y++) proc(j0 + y * BS + tid < deg, e0 + j0 + y * BS + tid, arc[y], co, u);
+      }
     }
     __syncthreads();
     // counts -> CSR offsets; reserve the segment in the stream's arena; scatter the staged arcs
