@@ -314,7 +314,10 @@ def gpu_arm(args):
         "arcs_per_s": round(arcs_all * 1e3 / (ms_max), 1) if ms_max else None,
         "frames_per_s": round(args.steps * frames_per_step * world / (ms_max / 1e3), 1),
         "e2e": e2e,
-        "gpu_launches": (2 + (T + chunk - 1) // chunk) * args.steps,
+        # per step: reset = settle-point reset + init frame kernel, one frame-kernel launch per
+        # chunk (+ one lattice launch each with --lattice, + one on reset), best paths
+        "gpu_launches": (3 + (T + chunk - 1) // chunk * (2 if args.lattice is not None else 1)
+                         + (2 if args.lattice is not None else 0)) * args.steps,
         "decoder_opts": decoder_opts(args),
         "roofline": {"bound": "hbm", "kernel": "frame_kernel", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
