@@ -363,10 +363,12 @@ def cpu_baseline(wl, args):
     n = min(wl["B"], max(16, cores))
     dt, arcs, rc = _oracle_time(wl, n, cores)
     audio = n * wl["T"] * FRAME_S
+    dt1, _, _ = _oracle_time(wl, 2, 1)   # the single-core rate, 2 streams
     return {"value": round(audio / dt, 2), "unit": UNIT, "cores": min(cores, n), "kind": "oracle",
             "sample": f"{n} of {wl['B']} streams x {wl['T']} frames of {args.config}/{args.preset} "
                       f"(oracle/wfst_oracle.c, pthreads), {dt:.2f} s wall",
-            "arcs_per_s": round(arcs / dt, 1), "errors": int((rc != 0).sum())}
+            "arcs_per_s": round(arcs / dt, 1), "errors": int((rc != 0).sum()),
+            "single_core": {"value": round(2 * wl["T"] * FRAME_S / dt1, 2), "sample": "2 streams, 1 thread"}}
 
 
 def reference_arm(args):
