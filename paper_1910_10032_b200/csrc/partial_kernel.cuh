@@ -66,7 +66,10 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* set = (uint32_t*)smem_raw;                       // wanted source states
   unsigned char* flag = (unsigned char*)(set + p.wcap);      // tokens of the current layer in S
-  __shared__ int s_changed, s_roots, s_root, s_status, s_len, s_idx, s_arc, s_layer, s_nw;
+  __shared__ int s_changed, s_roots, s_root, s_status, s_len, s_idx, s_arc, s_layer, s_nw, s_nflag;
+  // the wanted-state set is sized to what can be wanted (twice the tokens flagged), so that
+  // clearing it costs O(flagged tokens), not O(capacity), per step
+  auto set_cap = [&](int n) { return (uint32_t)min(p.wcap, max(64, 2 * n)); };
   const int tid = threadIdx.x;
   const int ln = p.lanes[blockIdx.x];
   const LaneState* Lp = p.lanes_st + ln;
@@ -109,12 +112,14 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
     return;
   }
   for (int i = tid; i < Lk.y; i += BS) flag[i] = 1;
+  if (tid == 0) s_nflag = Lk.y;
   __syncthreads();
   int root = -1;   // record index of the settle point
   while (true) {
     // epsilon predecessors inside layer k (chains are short; repeat until nothing new)
     while (true) {
-      for (uint32_t i = tid; i < (uint32_t)p.wcap; i += BS) set[i] = 0xFFFFFFFFu;
+      const uint32_t wc = set_cap(s_nflag);
+      for (uint32_t i = tid; i < wc; i += BS) set[i] = 0xFFFFFFFFu;
       if (tid == 0) {
         s_changed = 0;
         s_nw = 0;
@@ -124,16 +129,17 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
         if (!flag[i]) continue;
         const int a = __ldcg(&rec[R((int64_t)Lk.x + i)].x);
         if (a >= 0 && __ldg(&p.arcs[a].z) < 0) {
-          pset_put(set, (uint32_t)p.wcap, (uint32_t)(__ldg(&p.arcs[a].w) & 0x7FFFFFFF));
+          pset_put(set, wc, (uint32_t)(__ldg(&p.arcs[a].w) & 0x7FFFFFFF));
           s_nw = 1;
         }
       }
       __syncthreads();
       if (!s_nw) break;
       for (int i = tid; i < Lk.y; i += BS)
-        if (!flag[i] && pset_has(set, (uint32_t)p.wcap, (uint32_t)__ldcg(&rec[R((int64_t)Lk.x + i)].y))) {
+        if (!flag[i] && pset_has(set, wc, (uint32_t)__ldcg(&rec[R((int64_t)Lk.x + i)].y))) {
           flag[i] = 1;
           s_changed = 1;
+          atomicAdd(&s_nflag, 1);
         }
       __syncthreads();
       if (!s_changed) break;
@@ -158,13 +164,15 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
       break;
     }
     // predecessors of the roots in layer k-1
-    for (uint32_t i = tid; i < (uint32_t)p.wcap; i += BS) set[i] = 0xFFFFFFFFu;
+    const uint32_t wc = set_cap(s_roots);
+    for (uint32_t i = tid; i < wc; i += BS) set[i] = 0xFFFFFFFFu;
+    if (tid == 0) s_nflag = 0;
     __syncthreads();
     for (int i = tid; i < Lk.y; i += BS) {
       if (!flag[i]) continue;
       const int a = __ldcg(&rec[R((int64_t)Lk.x + i)].x);
       if (a >= 0 && __ldg(&p.arcs[a].z) >= 0)
-        pset_put(set, (uint32_t)p.wcap, (uint32_t)(__ldg(&p.arcs[a].w) & 0x7FFFFFFF));
+        pset_put(set, wc, (uint32_t)(__ldg(&p.arcs[a].w) & 0x7FFFFFFF));
     }
     __syncthreads();
     k--;
@@ -173,7 +181,11 @@ __global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
       if (tid == 0) s_status = WFST_ERR_CAPACITY;
       break;
     }
-    for (int i = tid; i < Lk.y; i += BS) flag[i] = pset_has(set, (uint32_t)p.wcap, (uint32_t)__ldcg(&rec[R((int64_t)Lk.x + i)].y));
+    for (int i = tid; i < Lk.y; i += BS) {
+      const bool f = pset_has(set, wc, (uint32_t)__ldcg(&rec[R((int64_t)Lk.x + i)].y));
+      flag[i] = f;
+      if (f) atomicAdd(&s_nflag, 1);
+    }
     __syncthreads();
   }
   __syncthreads();
