@@ -217,7 +217,7 @@ def gpu_arm(args):
         for t0 in range(0, T, chunk):
             D.decode_frames(ll[t0:t0 + chunk] if chunk < T else ll)
             if args.partial:   # row f2: settled partial results of every stream after each chunk
-                D.partial_paths(cap=4 * T + 64)
+                D.partial_paths()
         if ev is not None:
             ev[1].record()
         return D.best_paths(cap=cap, raise_on_error=False)

@@ -1160,9 +1160,17 @@ wfst_status wfst_get_partial_paths(wfst_decoder_t d, const int32_t* streams, int
   if (e != cudaSuccess) return cuda_fail(e, "partial kernel");
   std::vector<int32_t> head(5 * (size_t)n);
   e = cudaMemcpy(head.data(), p, 4 * head.size(), cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && arcs && cap > 0) e = cudaMemcpy(arcs, pp.arcs_out, 4 * (size_t)n * cp, cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && olabels && cap > 0)
-    e = cudaMemcpy(olabels, pp.olab_out, 4 * (size_t)n * cp, cudaMemcpyDeviceToHost);
+  // copy only the columns some stream used (a few frames' worth of arcs per call, not cap)
+  int mx_a = 0, mx_o = 0;
+  for (int i = 0; i < n && e == cudaSuccess; i++) {
+    mx_a = std::max(mx_a, std::min(head[n + i], cp));
+    mx_o = std::max(mx_o, std::min(head[2 * n + i], cp));
+  }
+  const size_t pitch = 4 * (size_t)cp;
+  if (e == cudaSuccess && arcs && cap > 0 && mx_a > 0)
+    e = cudaMemcpy2D(arcs, pitch, pp.arcs_out, pitch, 4 * (size_t)mx_a, n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && olabels && cap > 0 && mx_o > 0)
+    e = cudaMemcpy2D(olabels, pitch, pp.olab_out, pitch, 4 * (size_t)mx_o, n, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "partial D2H");
   wfst_status first = WFST_OK;
   for (int i = 0; i < n; i++) {

@@ -329,18 +329,32 @@ class Decoder:
         return st[:k].copy(), ar[:k].copy(), co[:k].copy()
 
 
-    def partial_paths(self, streams=None, cap: int = 4096) -> dict:
+    def partial_paths(self, streams=None, cap: int = 512) -> dict:
         """Row f2: the arcs/olabels settled since the previous call, per stream
-        (wfst_get_partial_paths), and the frames the settled prefix covers."""
+        (wfst_get_partial_paths), and the frames the settled prefix covers.  cap grows on demand
+        (a stream that does not fit keeps its settle point, so the call is simply repeated)."""
         ids = np.arange(self.n_streams, dtype=np.int32) if streams is None else _np(streams, np.int32)
         n = ids.size
-        arcs = np.zeros((n, cap), np.int32)
-        ols = np.zeros((n, cap), np.int32)
+        arcs = np.empty((n, cap), np.int32)
+        ols = np.empty((n, cap), np.int32)
         nar, nol, fr = np.zeros(n, np.int32), np.zeros(n, np.int32), np.zeros(n, np.int32)
-        _check(lib().wfst_get_partial_paths(self.h, _ptr(ids), n, _ptr(arcs), _ptr(ols), cap, _ptr(nar), _ptr(nol),
-                                            _ptr(fr)))
+        rc = lib().wfst_get_partial_paths(self.h, _ptr(ids), n, _ptr(arcs), _ptr(ols), cap, _ptr(nar), _ptr(nol),
+                                          _ptr(fr))
+        if rc == 1 and int(nar.max(initial=0)) > cap:
+            return self._partial_merge(ids, arcs, ols, nar, nol, fr, cap)
+        _check(rc)
         return dict(arcs=[arcs[i, :nar[i]].copy() for i in range(n)], olabels=[ols[i, :nol[i]].copy() for i in range(n)],
                     settled_frames=fr)
+
+    def _partial_merge(self, ids, arcs, ols, nar, nol, fr, cap):
+        """Streams whose new arcs exceeded cap kept their settle point: fetch them again."""
+        big = nar > cap
+        out_a = [arcs[i, :nar[i]].copy() if not big[i] else None for i in range(ids.size)]
+        out_o = [ols[i, :nol[i]].copy() if not big[i] else None for i in range(ids.size)]
+        again = self.partial_paths(ids[big], cap=int(nar.max()) + 64)
+        for k, i in enumerate(np.nonzero(big)[0]):
+            out_a[i], out_o[i], fr[i] = again["arcs"][k], again["olabels"][k], again["settled_frames"][k]
+        return dict(arcs=out_a, olabels=out_o, settled_frames=fr)
 
     def lattice(self, stream: int, arcs_cap: int = 1 << 20, layers_cap: int = 1 << 14,
                 gamma_cap: int = 1 << 22) -> dict:
