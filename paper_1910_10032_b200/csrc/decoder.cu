@@ -217,10 +217,11 @@ struct wfst_decoder_s {
   int id_slot = 0;
   int32_t* d_path = nullptr;       // best-path scratch
   size_t path_cap = 0;
-  float* d_host_stage[2] = {nullptr, nullptr};
+  static constexpr int kStages = 3;   // host-input staging buffers (copies run ahead of decoding)
+  float* d_host_stage[kStages] = {};
   size_t stage_bytes = 0;
   cudaStream_t copy_stream = nullptr;
-  cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_use[2] = {nullptr, nullptr};
+  cudaEvent_t ev_copy[kStages] = {}, ev_use[kStages] = {};
   int2* d_settled = nullptr;        // [lane] last settle point of the partial results (row f2)
   size_t partial_smem = 0;
   // lattice (row f1)
@@ -253,15 +254,18 @@ struct DeviceGuard {
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
+#ifndef WFST_R1024
+#define WFST_R1024 2   // arcs in flight per thread in the default 1024-thread kernel
+#endif
 template <int BS, int R, int MINB, int AM>
 void launch_v(int grid, size_t smem, cudaStream_t st, const KParams& kp) {
   frame_kernel<BS, R, MINB, AM><<<grid, BS, smem, st>>>(kp);
 }
 #define WFST_VARIANT(BS, R, MINB, AM) {BS, MINB, AM, (void*)frame_kernel<BS, R, MINB, AM>, launch_v<BS, R, MINB, AM>}
 const WfstVariant kVariants[] = {
-    WFST_VARIANT(512, 4, 1, 0), WFST_VARIANT(256, 4, 1, 0), WFST_VARIANT(1024, 2, 1, 0), WFST_VARIANT(256, 4, 2, 0),
+    WFST_VARIANT(512, 4, 1, 0), WFST_VARIANT(256, 4, 1, 0), WFST_VARIANT(1024, WFST_R1024, 1, 0), WFST_VARIANT(256, 4, 2, 0),
     WFST_VARIANT(512, 2, 2, 0), WFST_VARIANT(256, 2, 3, 0), WFST_VARIANT(256, 2, 4, 0),
-    WFST_VARIANT(1024, 2, 1, 1),   // histogram max-active (row f4): default launch shape only
+    WFST_VARIANT(1024, WFST_R1024, 1, 1),   // histogram max-active (row f4): default launch shape only
 };
 const WfstVariant* find_variant(int bs, int ctas, int am) {
   for (const WfstVariant& v : kVariants)
@@ -602,7 +606,7 @@ void wfst_decoder_destroy(wfst_decoder_t d) {
   if (d->ev_lat) cudaEventDestroy(d->ev_lat);
   if (d->h_lat_stage) cudaFreeHost(d->h_lat_stage);
   if (d->copy_stream) cudaStreamDestroy(d->copy_stream);
-  for (int i = 0; i < 2; i++) {
+  for (int i = 0; i < wfst_decoder_s::kStages; i++) {
     if (d->ev_copy[i]) cudaEventDestroy(d->ev_copy[i]);
     if (d->ev_use[i]) cudaEventDestroy(d->ev_use[i]);
   }
@@ -718,7 +722,7 @@ static cudaError_t ensure_copy_stream(wfst_decoder_t d) {
   cudaError_t e = cudaSuccess;
   if (!d->copy_stream) {
     e = cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking);
-    for (int i = 0; i < 2 && e == cudaSuccess; i++) {
+    for (int i = 0; i < wfst_decoder_s::kStages && e == cudaSuccess; i++) {
       e = cudaEventCreateWithFlags(&d->ev_copy[i], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_use[i], cudaEventDisableTiming);
     }
@@ -740,23 +744,22 @@ wfst_status wfst_decode_frames_host(wfst_decoder_t d, const float* h_loglikes, i
   if (need > d->stage_bytes) {
     cudaStreamSynchronize(st);
     if (d->copy_stream) cudaStreamSynchronize(d->copy_stream);
-    cudaFree(d->d_host_stage[0]);
-    cudaFree(d->d_host_stage[1]);
-    d->d_host_stage[0] = d->d_host_stage[1] = nullptr;
+    for (int i = 0; i < wfst_decoder_s::kStages; i++) {
+      cudaFree(d->d_host_stage[i]);
+      d->d_host_stage[i] = nullptr;
+    }
     d->stage_bytes = 0;
-    e = cudaMalloc(&d->d_host_stage[0], need);
-    if (e == cudaSuccess) e = cudaMalloc(&d->d_host_stage[1], need);
+    for (int i = 0; i < wfst_decoder_s::kStages && e == cudaSuccess; i++) e = cudaMalloc(&d->d_host_stage[i], need);
     if (e != cudaSuccess) return cuda_fail(e, "staging allocation");
     d->stage_bytes = need;
   }
   e = ensure_copy_stream(d);
   if (e != cudaSuccess) return cuda_fail(e, "copy stream");
   // the staging buffers may still be read by earlier work on st
-  e = cudaEventRecord(d->ev_use[0], st);
-  if (e == cudaSuccess) e = cudaEventRecord(d->ev_use[1], st);
+  for (int i = 0; i < wfst_decoder_s::kStages && e == cudaSuccess; i++) e = cudaEventRecord(d->ev_use[i], st);
   if (e != cudaSuccess) return cuda_fail(e, "event");
   int k = 0;
-  for (int32_t t0 = 0; t0 < T; t0 += CF, k ^= 1) {
+  for (int32_t t0 = 0; t0 < T; t0 += CF, k = (k + 1) % wfst_decoder_s::kStages) {
     int32_t n = std::min(CF, T - t0);
     size_t bytes = (size_t)n * B * P * 4;
     e = cudaStreamWaitEvent(d->copy_stream, d->ev_use[k], 0);

@@ -28,7 +28,10 @@ constexpr int kNB = 1024;          // cost bins of the max-active bound (DESIGN.
 constexpr int kMaxProbeS = WFST_MAXPROBE;   // buckets probed in the on-chip table before overflowing
 constexpr int kMaxProbeG = 512;    // buckets probed in the global overflow table
 constexpr int kModeFrames = 0, kModeInit = 1;
-constexpr int kBig = 64;           // tokens with more emitting arcs are expanded CTA-wide
+#ifndef WFST_KBIG
+#define WFST_KBIG 64
+#endif
+constexpr int kBig = WFST_KBIG;    // tokens with more emitting arcs are expanded CTA-wide
 constexpr int kBigCap = 256;
 constexpr int kStage = 32;         // per-warp staging buffer (candidates awaiting insertion)
 constexpr int kPlace = 64;         // coarse cost bins ordering the next frontier (kNB / 16 each)
