@@ -1187,6 +1187,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   __device__ void init_lane() {
     const int tid = threadIdx.x;
     if (tid == 0) {
+      S.t_mark = clock64();   // the contraction's phase marks measure from here
       LaneState& L = S.L;   // a new utterance: keep the lifetime counters
       L.n_front = 0;
       L.cur = 0;
