@@ -32,6 +32,10 @@ constexpr int kModeFrames = 0, kModeInit = 1;
 #define WFST_KBIG 64
 #endif
 constexpr int kBig = WFST_KBIG;    // tokens with more emitting arcs are expanded CTA-wide
+#ifndef WFST_THSHIFT
+#define WFST_THSHIFT 10
+#endif
+constexpr int kThShift = WFST_THSHIFT;   // the max-active bound is refreshed every 2^kThShift claims
 constexpr int kBigCap = 256;
 constexpr int kStage = 32;         // per-warp staging buffer (candidates awaiting insertion)
 constexpr int kPlace = 64;         // coarse cost bins ordering the next frontier (kNB / 16 each)
@@ -486,7 +490,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       if (bin >= 0) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
     }
     const int end = base + __popc(m);
-    return p.alpha > 0 && end >= p.alpha && (end >> 10) != (base >> 10);
+    return p.alpha > 0 && end >= p.alpha && (end >> kThShift) != (base >> kThShift);
   }
 
   // Candidates in bins >= theta are provably above the exact k_alpha (R6).  The histogram rule
