@@ -409,7 +409,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
       // bytes per record: {arc, state} (+ cost with debug_costs or lattice, + gamma and 4 arena
       // entries of 20 B with lattice)
       int64_t per_rec = (int64_t)sizeof(int2) + (d->o.debug_costs || d->o.lattice ? 4 : 0) +
-                        (d->o.lattice ? 4 + 2 * 20 : 0);
+                        (d->o.lattice ? 4 + 16 + 2 * 20 : 0);
       int64_t cap = budget / per_rec;
       if (cap < d->R_cap) d->R_cap = std::max<int64_t>(cap, per_frame);
     }
@@ -456,6 +456,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     }
   }
   size_t i_rcost = (d->o.debug_costs || d->lattice) ? add(L * (size_t)d->R_cap * 4) : (size_t)-1;
+  size_t i_rsi = d->lattice ? add(L * (size_t)d->R_cap * sizeof(int4)) : (size_t)-1;
   // lattice: arena {arc, src, dst, slack} + path slack per entry, cursor, segment index, status,
   // gamma per record; fallback token maps of the lattice CTAs for layers beyond shared memory
   const size_t NLAT = d->lattice ? (size_t)d->n_sm * kLatCtas : 0;
@@ -521,6 +522,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.wl = (uint32_t*)(base + parts[i_wl].off);
   kp.rec = (int2*)(base + parts[i_rec].off);
   kp.rec_cost = i_rcost != (size_t)-1 ? (float*)(base + parts[i_rcost].off) : nullptr;
+  kp.rec_si = i_rsi != (size_t)-1 ? (int4*)(base + parts[i_rsi].off) : nullptr;
   kp.fstats = (float*)(base + parts[i_fst].off);
   kp.fcounts = (long long*)(base + parts[i_fcn].off);
   kp.layer_info = (int2*)(base + parts[i_linfo].off);
@@ -535,6 +537,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     lp.lanes_st = d->d_lanes;
     lp.rec = kp.rec;
     lp.rec_cost = kp.rec_cost;
+    lp.rec_si = kp.rec_si;
     lp.R_cap = d->R_cap;
     lp.layer_info = kp.layer_info;
     lp.TMAX = d->TMAX;

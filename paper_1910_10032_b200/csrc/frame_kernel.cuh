@@ -82,7 +82,8 @@ struct KParams {
   u64* ovf;           // [cta][C_ovf]     global overflow token table
   uint32_t* wl;       // [cta][2][FCAP]   epsilon worklists (slots)
   int2* rec;          // [lane][R_cap]    traceback records {winning arc (-1: start), state}
-  float* rec_cost;    // [lane][R_cap]    (debug) survivor cost
+  float* rec_cost;    // [lane][R_cap]    survivor cost (debug_costs or lattice)
+  int4* rec_si;       // [lane][R_cap]    survivor's {e_begin, e_end, eps_end, state} (lattice only)
   float* fstats;      // [lane][TMAX][3]
   long long* fcounts; // [lane][TMAX][5]
   int2* layer_info;   // [lane][TMAX+1]   {record base, survivors}
@@ -366,6 +367,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   uint32_t* wl0;      // epsilon worklist 0; worklist 1 follows at +FCAP
   int2* rec;
   float* rec_cost;
+  int4* rec_si;
 
   __device__ Frame(const KParams& p_, SmemCtl& S_, uint32_t tab_sa_, int* hist_, int* wbuf_, uint32_t stage_sa_,
                    uint32_t row_sa_)
@@ -418,6 +420,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     F0 = p.front + L * 2 * FC;
     rec = p.rec + L * (size_t)p.R_cap;
     rec_cost = p.rec_cost ? p.rec_cost + L * (size_t)p.R_cap : nullptr;
+    rec_si = p.rec_si ? p.rec_si + L * (size_t)p.R_cap : nullptr;
   }
 
   __device__ __forceinline__ u64 slot_key(int i) const { return lds64(tab_sa + 8u * (uint32_t)i); }
@@ -1083,6 +1086,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         const int64_t r = (int64_t)rp + pos[u] - (rp + pos[u] >= p.R_cap ? p.R_cap : 0);   // record ring
         rec[r] = make_int2(arc, (int)q);
         if (rec_cost) rec_cost[r] = c;
+        if (rec_si) rec_si[r] = make_int4(si[u].x, si[u].y, si[u].z, (int)q);   // for the lattice pass
         epsd += (unsigned long long)(si[u].z - si[u].y);
       }
     });

@@ -30,6 +30,7 @@ struct LatParams {
   const LaneState* lanes_st;
   const int2* rec;          // [lane][R_cap] {arc, state}
   const float* rec_cost;    // [lane][R_cap]
+  const int4* rec_si;       // [lane][R_cap] {e_begin, e_end, eps_end, state}, written by the frame kernel
   int64_t R_cap;
   const int2* layer_info;   // [lane][TMAX+1] {record base, n}
   int32_t TMAX;
@@ -99,10 +100,9 @@ constexpr int kLatBS = WFST_LAT_BS, kLatCtas = WFST_LAT_CTAS;   // lattice CTA s
 template <int BS, int MINB>
 __global__ void __launch_bounds__(BS, MINB) lattice_kernel(LatParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int s_item, s_skip, s_err, s_scan[33], s_nbig, s_nst, s_big[kLatBigCap];
+  __shared__ int s_item, s_skip, s_err, s_scan[33], s_nbig, s_nst, s_next, s_big[kLatBigCap];
   __shared__ long long s_base;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = BS / 32;
+  const int tid = threadIdx.x, lane = tid & 31;
   while (true) {
     if (tid == 0) s_item = atomicAdd(p.q_head, 1);
     __syncthreads();
@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(BS, MINB) lattice_kernel(LatParams p) {
       s_err = WFST_OK;
       s_nbig = 0;
       s_nst = 0;
+      s_next = 0;
     }
     __syncthreads();
     for (int i = tid; i < n_k; i += BS) {
@@ -198,17 +199,22 @@ __global__ void __launch_bounds__(BS, MINB) lattice_kernel(LatParams p) {
         if (x < p.stage_cap) stg[x] = make_int4(a, u < n_e ? u : u - n_e, jt, __float_as_int(s));
       }
     };
-    auto src_of = [&](int u, int& e0, int& deg, float& co) {
+    const int4* rsi = p.rec_si + (size_t)ln * p.R_cap;
+    auto src_of = [&](int u, int& e0, int& deg, float& co) {   // contiguous loads, no gathers
       const bool em = u < n_e;
       const int r = em ? Lp1.x + u : Lk.x + (u - n_e);
-      const int q = __ldcg(&rec[r].y);
       co = __ldcg(rco + r);
-      const int4 si = __ldg(p.state_info + q);
+      const int4 si = __ldcg(rsi + r);
       e0 = em ? si.x : si.y;
       deg = em ? si.y - si.x : si.z - si.y;
     };
-    // tokens of small out-degree: 32 per warp, arcs flattened over the warp
-    for (int u0 = warp * 32; u0 < n_src; u0 += NW * 32) {
+    // tokens of small out-degree: groups of 32 handed to warps dynamically, arcs flattened over
+    // the warp
+    while (true) {
+      int u0 = 0;
+      if (lane == 0) u0 = atomicAdd(&s_next, 32);
+      u0 = __shfl_sync(0xffffffffu, u0, 0);
+      if (u0 >= n_src) break;
       const int u = u0 + lane;
       int e0 = 0, deg = 0;
       float co = 0.f;
