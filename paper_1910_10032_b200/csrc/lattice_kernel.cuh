@@ -275,13 +275,17 @@ __global__ void __launch_bounds__(BS, MINB) lattice_kernel(LatParams p) {
     // counts -> CSR offsets; reserve the segment in the stream's arena; scatter the staged arcs
     const int n_st = s_nst;
     int run = 0;
-    for (int i0 = 0; i0 < n_k; i0 += BS) {
-      const int i = i0 + tid;
-      const int x = i < n_k ? cnt[i] : 0;
-      int tot;
-      const int ex = block_excl_scan<BS>(x, s_scan, tot);
-      if (i < n_k) cnt[i] = run + ex;
-      run += tot;
+    {   // one block scan: each thread owns a contiguous range of tokens
+      const int per = (n_k + BS - 1) / BS, i0 = min(n_k, tid * per), i1 = min(n_k, i0 + per);
+      int loc = 0;
+      for (int i = i0; i < i1; i++) loc += cnt[i];
+      const int ex = block_excl_scan<BS>(loc, s_scan, run);
+      int acc = ex;
+      for (int i = i0; i < i1; i++) {
+        const int c = cnt[i];
+        cnt[i] = acc;
+        acc += c;
+      }
     }
     if (tid == 0) {
       const int err = s_err != WFST_OK ? s_err : n_st > p.stage_cap ? WFST_ERR_CAPACITY : WFST_OK;
