@@ -122,3 +122,24 @@ def test_reclaim_excludes_lattice(W):
     G = W.Graph.from_arrays(g)
     with pytest.raises(W.WfstError):
         W.Decoder(G, 2, 10.0, 100, reclaim=1, lattice=1, lattice_beam=8.0)
+
+
+def test_partial_and_lattice_before_any_frame(W, torch, oracle_mod):
+    """Edge case T = 0: right after reset nothing is settled, the lattice is layer 0 alone (the
+    initial epsilon closure, reading R3) and equals the oracle's."""
+    g = I.hclg_graph(3000, 6, 200, seed=4)
+    G = W.Graph.from_arrays(g)
+    D = W.Decoder(G, 2, 10.0, 300)
+    D.reset()
+    pp = D.partial_paths()
+    assert all(a.size == 0 for a in pp["arcs"]) and list(pp["settled_frames"]) == [0, 0]
+    DL = W.Decoder(G, 1, 10.0, 300, lattice=1, lattice_beam=8.0)
+    DL.reset()
+    L = DL.lattice(0)
+    og = oracle_mod.OracleGraph(g)
+    r = og.lattice(np.zeros((0, 200), np.float32), 10.0, 300, 8.0)
+    assert L["n_layers"] == 1 == len(r.segments)
+    st = DL.debug_layer(0, 0)[0]
+    got = sorted((int(a), int(st[j])) for a, j in zip(L["segments"][0][0], L["segments"][0][2]))
+    want = sorted((int(a), int(r.layers[0][0][j])) for a, j in zip(r.segments[0][0], r.segments[0][2]))
+    assert got == want
