@@ -30,7 +30,11 @@ namespace {
 // else of (c, arc); then the traceback: the predecessor of a record {arc, state} is the record
 // of src(arc) in the previous layer (emitting arc) or the same layer (epsilon arc), found by a
 // CTA-wide scan of that layer's records.  Arcs are written back to front into arcs_out.
-__global__ void best_path_kernel(KParams p, const int32_t* __restrict__ olabel, const int32_t* __restrict__ lanes,
+#ifndef WFST_BP_THREADS
+#define WFST_BP_THREADS 512
+#endif
+constexpr int kBestPathThreads = WFST_BP_THREADS;   // (<= 1024: s_fin / s_any hold one entry per warp)
+__global__ void __launch_bounds__(kBestPathThreads) best_path_kernel(KParams p, const int32_t* __restrict__ olabel, const int32_t* __restrict__ lanes,
                                  int32_t n, int32_t cap, float* cost_out, int32_t* reached_out, int32_t* n_arcs_out,
                                  int32_t* arcs_out, int32_t* olab_out, int32_t* n_olab_out, int32_t* status_out) {
   __shared__ u64 s_fin[32], s_any[32];
@@ -844,7 +848,7 @@ wfst_status wfst_get_best_paths(wfst_decoder_t d, const int32_t* streams, int32_
   for (int i = 0; i < n; i++) ids[i] = streams ? streams[i] : i;
   e = cudaMemcpy(d_ids, ids.data(), 4 * (size_t)n, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "ids");
-  best_path_kernel<<<n, 256>>>(d->kp, d->g->d_olabel, d_ids, n, cap, d_cost, d_reached, d_nar, d_arcs, d_ol, d_nol,
+  best_path_kernel<<<n, kBestPathThreads>>>(d->kp, d->g->d_olabel, d_ids, n, cap, d_cost, d_reached, d_nar, d_arcs, d_ol, d_nol,
                                d_st);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
