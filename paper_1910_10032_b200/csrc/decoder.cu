@@ -766,8 +766,29 @@ wfst_status wfst_decode_frames_host(wfst_decoder_t d, const float* h_loglikes, i
   for (int i = 0; i < wfst_decoder_s::kStages && e == cudaSuccess; i++) e = cudaEventRecord(d->ev_use[i], st);
   if (e != cudaSuccess) return cuda_fail(e, "event");
   int k = 0;
-  for (int32_t t0 = 0; t0 < T; t0 += CF, k = (k + 1) % wfst_decoder_s::kStages) {
-    int32_t n = std::min(CF, T - t0);
+  // chunk schedule: a short first chunk (decoding starts after a fifth of a chunk's copy) and a
+  // short last one (little decoding left once the last copy lands); full chunks in between
+  std::vector<int32_t> sizes;
+  {
+    const int32_t small = std::max(1, CF / 5);
+    int32_t rem = T;
+    if (rem > CF + small) {
+      sizes.push_back(small);
+      rem -= small;
+    }
+    while (rem > CF + small) {
+      sizes.push_back(CF);
+      rem -= CF;
+    }
+    if (rem > CF) {
+      sizes.push_back(rem - small);
+      rem = small;
+    }
+    if (rem > 0) sizes.push_back(rem);
+  }
+  int32_t t0 = 0;
+  for (size_t ci = 0; ci < sizes.size(); t0 += sizes[ci], ci++, k = (k + 1) % wfst_decoder_s::kStages) {
+    int32_t n = sizes[ci];
     size_t bytes = (size_t)n * B * P * 4;
     e = cudaStreamWaitEvent(d->copy_stream, d->ev_use[k], 0);
     if (e == cudaSuccess)
