@@ -105,7 +105,7 @@ struct SmemCtl {
   int32_t use_alpha;
   int32_t radix_prefix, radix_k;
   unsigned long long emit_arcs, eps_deg, eps_relax;
-  unsigned long long dbg[2];   // WFST_COUNT instrumentation: hub candidates staged, table inserts
+  unsigned long long dbg[2];   // WFST_COUNT instrumentation: entries dropped by the beam / by max-active
   uint32_t sclaim[kSmallClaims];   // claimed slots while the frame is small
   int32_t warp_tmp[32];
   long long warp_tmp64[32];
@@ -549,12 +549,6 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         if (slot < 0) claimed = false;
       }
     }
-#ifdef WFST_COUNT
-    {
-      const unsigned mi = __ballot_sync(0xffffffffu, slot >= 0);
-      if (lane == 0) red_add_s64(saddr(&S.dbg[1]), __popc(mi));
-    }
-#endif
     if (add_claim(slot, claimed, flag, bin)) update_theta();
   }
 
@@ -704,12 +698,6 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
           const bool pass = v[u] && c < bound && bin < th;
           const int j = j0 + u * BS + tid;
           const int4 entry = make_int4(arc[u].x, (int)ord_of(c), f.z + j, bin | (int)(arc[u].w & 0x80000000));
-#ifdef WFST_COUNT
-          {
-            const unsigned mh = __ballot_sync(0xffffffffu, pass);
-            if (lane == 0) red_add_s64(saddr(&S.dbg[0]), __popc(mh));
-          }
-#endif
           stage(pass, entry, staged, beam, best_sa, theta_sa);
         }
       }
@@ -1065,6 +1053,9 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         base = __shfl_sync(0xffffffffu, base, leader);
         pos[u] = k ? base + __popc(grp & ((1u << lane) - 1u)) : (live ? -1 : -2);
         if (live) clear_slot(sl[u]);
+#ifdef WFST_COUNT
+        if (live && !k) red_add_s64(saddr(&S.dbg[c < cut_b ? 1 : 0]), 1ull);
+#endif
         w[u] = kEmpty;
         si[u] = make_int4(0, 0, 0, 0);
         if (k) {
