@@ -191,10 +191,20 @@ def gpu_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; WFST_DIST_BACKEND=gloo lets a multi-rank run share fewer GPUs (used to
+    # exercise the multi-rank path on a one-GPU box -- the only collectives are a barrier and a
+    # two-number reduction, never on the data path)
+    backend = os.environ.get("WFST_DIST_BACKEND", "nccl")
+    if backend == "gloo":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     if rank == 0:
         build.build()
     if world > 1:
@@ -242,7 +252,7 @@ def gpu_arm(args):
     kern_ms = [a.elapsed_time(b) for a, b in kev]
     st = D.stats()
     if world > 1:
-        ms_max, arcs_all = reduce_over_ranks(dist, dev, ms, float(st["emit_arcs"] + st["eps_arcs"]))
+        ms_max, arcs_all = reduce_over_ranks(dist, red_dev, ms, float(st["emit_arcs"] + st["eps_arcs"]))
     else:
         ms_max = ms
         arcs_all = float(st["emit_arcs"] + st["eps_arcs"])
@@ -276,7 +286,7 @@ def gpu_arm(args):
         torch.cuda.synchronize(dev)
         ems = e0.elapsed_time(e1)
         if world > 1:
-            ems, _ = reduce_over_ranks(dist, dev, ems, 0.0)
+            ems, _ = reduce_over_ranks(dist, red_dev, ems, 0.0)
         d2h = B * (4 + 4 + 4 + 4 + 4 + 2 * cap * 4)
         e2e = {"value": e2e_steps * B * T * FRAME_S * world / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": T * B * P * 4 * world, "d2h_bytes_per_step": d2h * world,
