@@ -6,9 +6,14 @@ Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s `cpu_baseline` /
 
 `wfst_oracle.c` is the serial token-passing Viterbi beam search of PAPER.md §3
 (Fig. 1) under the readings R1-R12 listed in
-DESIGN.md §3; this module only builds it with gcc and marshals arguments.
+DESIGN.md §3, plus the NEXT rows: lattice segments and the end-of-utterance
+sweep (R13-R14, row f1) and the histogram max-active rule (R16, row f4); this
+module builds it with gcc and marshals arguments.  `OracleGraph.settled_prefix`
+(R15, row f2) is written here in Python as its definition (every survivor's
+traceback, longest common prefix).
 Pins (tests/test_oracle_*.py): fp64 trellis Bellman-Ford and exhaustive path
-enumeration (tests/bruteforce.py), SPEC worked examples, invariants.
+enumeration (tests/bruteforce.py), SPEC worked examples, closed forms,
+invariants.
 """
 from __future__ import annotations
 

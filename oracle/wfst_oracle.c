@@ -30,6 +30,9 @@
  *   R10 finals: argmin c + F over final survivors; else argmin c, flag 0.
  *   R11 traceback by back-pointers: emitting arc -> previous layer,
  *       eps arc -> same layer.
+ * NEXT rows: oracle_lattice / oracle_lattice_finalize (R13-R14,
+ * lattice segments and the final backward sweep) and the histogram max-active
+ * rule of oracle_decode_mode (R16).
  * Canonical arc ids: arcs stably bucketed by (src, emitting-first) in input
  * order ("within a span, emitting arcs precede non-emitting").
  */
