@@ -143,3 +143,35 @@ def test_partial_and_lattice_before_any_frame(W, torch, oracle_mod):
     got = sorted((int(a), int(st[j])) for a, j in zip(L["segments"][0][0], L["segments"][0][2]))
     want = sorted((int(a), int(r.layers[0][0][j])) for a, j in zip(r.segments[0][0], r.segments[0][2]))
     assert got == want
+
+
+def test_reclaim_long_streams_c3_graph(W, torch, oracle_mod):
+    """Traceback GC at C3's scale: 64 streams x 3000 frames (30 s of audio each) on the 5M-state
+    graph through a 256-layer ring and ~100 frames' worth of records per stream, settled results
+    every 50 frames; sampled streams equal the oracle's one-best path end to end."""
+    c = I.CONFIGS["c3"]
+    g = I.config_graph("c3")
+    T, B, P, chunk = 3000, 64, c["n_pdfs"], 50
+    G = W.Graph.from_arrays(g)
+    D = W.Decoder(G, B, c["beam"], c["max_active"], reclaim=1, max_frames=256, records_per_stream=100 * 12000)
+    pl = I.planted_walks(g, B, T, seed=123)
+    ids = torch.arange(0, B, dtype=torch.int32, device="cuda")
+    plt = torch.from_numpy(np.ascontiguousarray(pl)).cuda()
+    D.reset()
+    acc = [[] for _ in range(B)]
+    for t0 in range(0, T, chunk):
+        x = torch.empty((chunk, B, P), dtype=torch.float32, device="cuda")
+        W.synth_loglikes(x, ids, t0, 60006, plt[t0:t0 + chunk].contiguous(), **I.preset("clean"))
+        D.decode_frames(x)
+        pp = D.partial_paths()
+        for b in range(B):
+            acc[b] += pp["arcs"][b].tolist()
+    res = D.best_paths(cap=4 * T + 64)
+    assert res["rc"] == 0
+    og = oracle_mod.OracleGraph(g)
+    for b in (0, 37):
+        ll = I.loglikes_stream(60006, b, T, P, pl[:, b], **I.preset("clean"))
+        r = og.decode(ll, c["beam"], c["max_active"])
+        tail = list(res["arcs"][b, :res["n_arcs"][b]])
+        assert acc[b] + tail == list(r.arcs), b
+        assert res["cost"][b] == r.cost32
