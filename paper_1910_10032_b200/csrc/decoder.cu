@@ -454,6 +454,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   }
   if (d->lattice) {
     d->S_cap = d->o.lattice_arcs_per_stream > 0 ? d->o.lattice_arcs_per_stream : 2 * d->R_cap;
+    d->S_cap = std::min<int64_t>(d->S_cap, INT32_MAX - 1);   // segment offsets are int32
     if (!(d->o.lattice_beam >= 0.0f)) {
       delete d;
       return fail(WFST_ERR_INVALID_ARG, "lattice_beam must be >= 0 (may be +inf)");
