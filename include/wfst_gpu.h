@@ -96,7 +96,9 @@ typedef struct {
                                 the records and layers below the new settle point, so an unbounded
                                 stream needs only records_per_stream / max_frames for the frames
                                 since its paths last converged; wfst_get_best_path then returns the
-                                arcs AFTER the settled prefix.  Exclusive with lattice.             */
+                                arcs AFTER the settled prefix.  Exclusive with lattice.  Record
+                                numbers are int32: an utterance may write up to 2^31 records
+                                (~650k frames at 3.3k survivors), beyond that CAPACITY.            */
 } wfst_decoder_opts_t;
 
 typedef struct {
