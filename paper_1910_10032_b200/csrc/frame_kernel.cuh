@@ -105,7 +105,6 @@ struct SmemCtl {
   int32_t use_alpha;
   int32_t radix_prefix, radix_k;
   unsigned long long emit_arcs, eps_deg, eps_relax;
-  unsigned long long dbg[2];   // WFST_COUNT instrumentation: entries dropped by the beam / by max-active
   uint32_t sclaim[kSmallClaims];   // claimed slots while the frame is small
   int32_t warp_tmp[32];
   long long warp_tmp64[32];
@@ -1053,9 +1052,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         base = __shfl_sync(0xffffffffu, base, leader);
         pos[u] = k ? base + __popc(grp & ((1u << lane) - 1u)) : (live ? -1 : -2);
         if (live) clear_slot(sl[u]);
-#ifdef WFST_COUNT
-        if (live && !k) red_add_s64(saddr(&S.dbg[c < cut_b ? 1 : 0]), 1ull);
-#endif
+
         w[u] = kEmpty;
         si[u] = make_int4(0, 0, 0, 0);
         if (k) {
@@ -1109,7 +1106,6 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       S.n_ovf = 0;
       S.n_big = 0;
       S.next_group = 0;
-      S.dbg[0] = S.dbg[1] = 0;
       S.n_wl = 0;
       S.use_alpha = 0;
       S.kalpha = INFINITY;
@@ -1154,10 +1150,6 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         L.cand += S.n_claim;
         L.surv += n_surv;
         L.ovf += S.n_ovf;
-#ifdef WFST_COUNT
-        L.phase[7] += S.dbg[0];
-        L.phase[9] += S.dbg[1];
-#endif
         if (emitting) {
           L.emit_arcs += S.emit_arcs;
           L.alpha_frames += S.use_alpha;
@@ -1261,6 +1253,9 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       return;
     }
     long long t0 = clock64();
+#ifdef WFST_COUNT
+    const long long t_frame0 = t0;
+#endif
     if (tid == 0) S.t_cur = t;
 #if WFST_ROWSMEM
     if (tid == 0 && !S.row_pending) row_issue(row_ptr(t));   // first frame of a work item
@@ -1297,6 +1292,9 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     if (tid == 0) S.t_mark = clock64();
     contract();
     tick_contract(t0);
+#ifdef WFST_COUNT   // frame cycles split by frame kind: phase[7] alpha-bound frames, phase[9] others
+    if (tid == 0) S.L.phase[S.use_alpha ? 7 : 9] += (u64)(clock64() - t_frame0);
+#endif
     finish_frame(t, true);
     tick(t0, 5);
   }

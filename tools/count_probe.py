@@ -1,5 +1,5 @@
 """Instrumented run (library built with -DWFST_COUNT): per stream-frame averages of arcs,
-claims, survivors and the claimed entries the cutoff drops (beam / max-active)."""
+claims, survivors, and the share of frame cycles spent in frames where max-active binds."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -17,6 +17,6 @@ st = D.stats()
 f = st["frames"]
 ph = st["phase_cycles"]
 print(json.dumps({"config": cfg, "preset": preset, "frames": f,
-                  "arcs": st["emit_arcs"] / f, "dropped_by_beam": ph["map_build"] / f, "dropped_by_alpha": ph["eps_backptr"] / f,
+                  "arcs": st["emit_arcs"] / f, "cycle_share_alpha_frames": ph["map_build"] / max(1, ph["map_build"] + ph["eps_backptr"]),
                   "claims": st["candidates"] / f, "survivors": st["survivors"] / f,
                   "ovf": st["overflow_inserts"] / f, "alpha_frames": st["alpha_frames"] / f}))
