@@ -95,6 +95,9 @@ struct SmemCtl {
   int32_t theta;
   int32_t n_claim, n_claim_emit, n_ovf, n_oclaim, n_surv, n_in, n_wl, n_big, next_group;
   int32_t wlc[3];   // epsilon worklist counters (rotating)
+#ifdef WFST_COUNT
+  unsigned long long dbgc[4];   // alpha-bound frames: claims above k_alpha by (0,0.5], (0.5,2], (2,5], >5
+#endif
   int32_t pl[kPlace];        // placement histogram: live entries per coarse cost bin
   int32_t pl_base[kPlace];   // placement cursors
   int32_t n_app;             // survivors appended in the cutoff's bin
@@ -1052,6 +1055,12 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         base = __shfl_sync(0xffffffffu, base, leader);
         pos[u] = k ? base + __popc(grp & ((1u << lane) - 1u)) : (live ? -1 : -2);
         if (live) clear_slot(sl[u]);
+#ifdef WFST_COUNT
+        if (live && !k && S.use_alpha && c < cut_b) {
+          const float d = __fsub_rn(c, cut_a);
+          red_add_s64(saddr(&S.dbgc[d <= 0.5f ? 0 : d <= 2.0f ? 1 : d <= 5.0f ? 2 : 3]), 1ull);
+        }
+#endif
 
         w[u] = kEmpty;
         si[u] = make_int4(0, 0, 0, 0);
@@ -1106,6 +1115,9 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       S.n_ovf = 0;
       S.n_big = 0;
       S.next_group = 0;
+#ifdef WFST_COUNT
+      S.dbgc[0] = S.dbgc[1] = S.dbgc[2] = S.dbgc[3] = 0;
+#endif
       S.n_wl = 0;
       S.use_alpha = 0;
       S.kalpha = INFINITY;
@@ -1293,7 +1305,11 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     contract();
     tick_contract(t0);
 #ifdef WFST_COUNT   // frame cycles split by frame kind: phase[7] alpha-bound frames, phase[9] others
-    if (tid == 0) S.L.phase[S.use_alpha ? 7 : 9] += (u64)(clock64() - t_frame0);
+    if (tid == 0) {
+      (void)t_frame0;
+      S.L.phase[7] += S.dbgc[0] + S.dbgc[1];   // (slots reused by this instrumentation build)
+      S.L.phase[9] += S.dbgc[2] + S.dbgc[3];
+    }
 #endif
     finish_frame(t, true);
     tick(t0, 5);

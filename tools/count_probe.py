@@ -17,6 +17,7 @@ st = D.stats()
 f = st["frames"]
 ph = st["phase_cycles"]
 print(json.dumps({"config": cfg, "preset": preset, "frames": f,
-                  "arcs": st["emit_arcs"] / f, "cycle_share_alpha_frames": ph["map_build"] / max(1, ph["map_build"] + ph["eps_backptr"]),
+                  "arcs": st["emit_arcs"] / f, "alpha_frame_claims_above_kalpha_le2": ph["map_build"] / max(1, st["alpha_frames"]),
+                  "alpha_frame_claims_above_kalpha_gt2": ph["eps_backptr"] / max(1, st["alpha_frames"]),
                   "claims": st["candidates"] / f, "survivors": st["survivors"] / f,
                   "ovf": st["overflow_inserts"] / f, "alpha_frames": st["alpha_frames"] / f}))
