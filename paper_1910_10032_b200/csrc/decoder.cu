@@ -514,7 +514,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.beam = beam;
   kp.alpha = d->alpha;
   kp.C = d->C;
-  kp.NBK = d->C / 4;
+  kp.NBK = d->C / kBucket;
   kp.C_ovf = d->C_ovf;
   kp.FCAP = d->FCAP;
   kp.R_cap = d->R_cap;

@@ -223,6 +223,10 @@ __device__ __forceinline__ int bin_of(float c, float ref, float inv_w) {
 // Insert (state q, key = ord(cost) << 32 | q) into a table of nb buckets of 4 slots.
 // Returns the slot, or -1 when the probe limit is reached.  claimed: the slot was empty;
 // logit: the cost is <= the slot's (an improvement or a tie); strict: <.
+#ifndef WFST_BUCKET
+#define WFST_BUCKET 4
+#endif
+constexpr int kBucket = WFST_BUCKET;   // slots per bucket of the on-chip table
 __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q, u64 key, bool& claimed,
                                         bool& logit, bool& strict, uint32_t& old_hi) {
   uint32_t b = bucket_of(q, nb);
@@ -230,14 +234,17 @@ __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q
   claimed = logit = strict = false;
 #pragma unroll 1
   for (int p = 0; p < kMaxProbeS;) {
-    const uint32_t ba = tab_sa + b * 32u;
-    u64 x0, x1, x2, x3;
-    lds64x2(ba, x0, x1);
-    lds64x2(ba + 16, x2, x3);
+    const uint32_t ba = tab_sa + b * (8u * kBucket);
+    u64 x[kBucket];
+#pragma unroll
+    for (int j = 0; j < kBucket; j += 2) lds64x2(ba + 8 * j, x[j], x[j + 1]);
     // bit j: slot j holds q / slot j is empty
-    const uint32_t mq = ((uint32_t)x0 == q) | (((uint32_t)x1 == q) << 1) | (((uint32_t)x2 == q) << 2) |
-                        (((uint32_t)x3 == q) << 3);
-    const uint32_t me = (x0 == kEmpty) | ((x1 == kEmpty) << 1) | ((x2 == kEmpty) << 2) | ((x3 == kEmpty) << 3);
+    uint32_t mq = 0, me = 0;
+#pragma unroll
+    for (int j = 0; j < kBucket; j++) {
+      mq |= (uint32_t)((uint32_t)x[j] == q) << j;
+      me |= (uint32_t)(x[j] == kEmpty) << j;
+    }
     int j;
     if (mq) {
       j = __ffs(mq) - 1;
@@ -247,7 +254,7 @@ __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q
       if (old == kEmpty) {
         claimed = logit = strict = true;
         old_hi = 0xFFFFFFFFu;
-        return (int)(b * 4 + j);
+        return (int)(b * kBucket + j);
       }
       if ((uint32_t)old != q) continue;   // lost the slot to another state: re-read this bucket
     } else {
@@ -261,7 +268,7 @@ __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q
     logit = hi <= old;
     strict = hi < old;
     old_hi = old;
-    return (int)(b * 4 + j);
+    return (int)(b * kBucket + j);
   }
   return -1;
 }
