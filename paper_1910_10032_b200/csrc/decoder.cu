@@ -410,8 +410,8 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
       int64_t per_lane_other = (int64_t)d->FCAP * 32 + (int64_t)d->TMAX * 60 +
                                ((int64_t)d->FCAP * (4 + 8 + 8) + (int64_t)d->C_ovf * 8) * d->n_scratch / n_streams;
       int64_t budget = (int64_t)(free_b / 2) / n_streams - per_lane_other;
-      // bytes per record: {arc, state} (+ cost with debug_costs or lattice, + gamma and 4 arena
-      // entries of 20 B with lattice)
+      // bytes per record: {arc, state} (+ cost with debug_costs or lattice; with lattice also
+      // gamma, the state record {e_begin, e_end, eps_end, state} and 2 arena entries of 20 B)
       int64_t per_rec = (int64_t)sizeof(int2) + (d->o.debug_costs || d->o.lattice ? 4 : 0) +
                         (d->o.lattice ? 4 + 16 + 2 * 20 : 0);
       int64_t cap = budget / per_rec;
