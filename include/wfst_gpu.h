@@ -134,6 +134,9 @@ wfst_status wfst_graph_from_arrays(int32_t n_states, int32_t start, int64_t n_ar
 wfst_status wfst_graph_info(wfst_graph_t g, wfst_graph_info_t* info);
 /* canonical arc id -> input arc index (n_arcs int64 entries, host). */
 wfst_status wfst_graph_canonical_perm(wfst_graph_t g, int64_t* perm, int64_t cap);
+/* A copy of graph g on CUDA device `device` (row e: one replica per GPU), copied device to device
+ * (over NVLink/NVSwitch when the devices are peers).  Free it with wfst_graph_free. */
+wfst_status wfst_graph_replicate(wfst_graph_t g, int device, wfst_graph_t* out);
 void wfst_graph_free(wfst_graph_t g);
 
 /* Eq. 1 and Eq. 2 of the paper, host arithmetic only (no device needed). */

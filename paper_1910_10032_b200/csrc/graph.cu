@@ -316,6 +316,46 @@ wfst_status wfst_graph_canonical_perm(wfst_graph_t g, int64_t* perm, int64_t cap
   return WFST_OK;
 }
 
+wfst_status wfst_graph_replicate(wfst_graph_t g, int device, wfst_graph_t* out) {
+  if (!g || !out) return fail(WFST_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  int n_dev = 0;
+  cudaError_t e = cudaGetDeviceCount(&n_dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= n_dev) return fail(WFST_ERR_INVALID_ARG, "device out of range");
+  auto* r = new wfst_graph_s();
+  r->device = device;
+  r->Q = g->Q;
+  r->start = g->start;
+  r->E = g->E;
+  r->EE = g->EE;
+  r->max_pdf = g->max_pdf;
+  r->perm = g->perm;
+  r->h_dst = g->h_dst;
+  r->h_olabel = g->h_olabel;
+  r->device_bytes = g->device_bytes;
+  const size_t bs = sizeof(int4) * (size_t)g->Q, ba = sizeof(int4) * (size_t)(g->E > 0 ? g->E : 1),
+               bo = sizeof(int32_t) * (size_t)(g->E > 0 ? g->E : 1);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaMalloc(&r->d_state, bs);
+  if (e == cudaSuccess) e = cudaMalloc(&r->d_arcs, ba);
+  if (e == cudaSuccess) e = cudaMalloc(&r->d_olabel, bo);
+  // device-to-device (over NVLink when the devices are peers; staged by the driver otherwise)
+  if (e == cudaSuccess) e = cudaMemcpyPeer(r->d_state, device, g->d_state, g->device, bs);
+  if (e == cudaSuccess) e = cudaMemcpyPeer(r->d_arcs, device, g->d_arcs, g->device, ba);
+  if (e == cudaSuccess) e = cudaMemcpyPeer(r->d_olabel, device, g->d_olabel, g->device, bo);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    wfst_graph_free(r);
+    return cuda_fail(e, "graph replicate");
+  }
+  *out = r;
+  return WFST_OK;
+}
+
 void wfst_graph_free(wfst_graph_t g) {
   if (!g) return;
   int prev = 0;

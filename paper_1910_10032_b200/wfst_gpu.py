@@ -24,7 +24,7 @@ SYMBOLS = ["wfst_load_graph", "wfst_graph_from_arrays", "wfst_graph_info", "wfst
            "wfst_decode_frames_host", "wfst_decoder_sync", "wfst_decoder_status", "wfst_get_best_path",
            "wfst_get_best_paths", "wfst_decoder_stats", "wfst_decoder_reset_stats", "wfst_decoder_frame_stats",
            "wfst_debug_layer", "wfst_synth_loglikes", "wfst_last_error", "wfst_status_string",
-           "wfst_abi_version", "wfst_get_lattice", "wfst_get_partial_paths"]
+           "wfst_abi_version", "wfst_get_lattice", "wfst_get_partial_paths", "wfst_graph_replicate"]
 
 
 class WfstError(RuntimeError):
@@ -101,6 +101,7 @@ def lib():
             "wfst_abi_version": [],
             "wfst_get_lattice": [P, I32, P, I32, P, P, P, P, P, P, I64, P, P, I64, P, P, P],
             "wfst_get_partial_paths": [P, P, I32, P, P, I32, P, P, P],
+            "wfst_graph_replicate": [P, C.c_int, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name, None)
@@ -191,6 +192,12 @@ class Graph:
         _check(lib().wfst_graph_from_arrays(int(g.n_states), int(g.start), int(arrs[0].size),
                                             *[_ptr(a) for a in arrs], device, C.byref(h)))
         return cls(h, device)
+
+    def replicate(self, device: int) -> "Graph":
+        """Row e: a copy of this graph on another CUDA device (wfst_graph_replicate)."""
+        h = C.c_void_p()
+        _check(lib().wfst_graph_replicate(self.h, device, C.byref(h)))
+        return Graph(h, device)
 
     def info(self) -> GraphInfo:
         if self._info is None:

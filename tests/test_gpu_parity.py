@@ -373,3 +373,29 @@ def test_c5_online_chunks_full_size(W, torch, oracle_mod):
         n = res["n_arcs"][b]
         assert list(res["arcs"][b, :n]) == list(r.arcs) and res["cost"][b] == r.cost32
         assert acc[b] == list(r.arcs[:len(acc[b])]) and len(acc[b]) > 100
+
+
+def test_graph_replicate(W, torch, oracle_mod):
+    """Row e: a graph replica (device-to-device copy; onto every visible device) decodes like the
+    original."""
+    g = I.hclg_graph(3000, 6, 200, seed=4)
+    G = W.Graph.from_arrays(g)
+    T, B = 20, 4
+    pl = I.planted_walks(g, B, T, seed=9)
+    ll = I.loglikes(77, range(B), T, 200, pl, 1.0, 4.0)
+    outs = []
+    for dev in range(torch.cuda.device_count()):
+        Gr = G.replicate(dev)
+        info, info0 = Gr.info(), G.info()
+        assert (info.n_states, info.n_arcs, info.device) == (info0.n_states, info0.n_arcs, dev)
+        with torch.cuda.device(dev):
+            D = W.Decoder(Gr, B, 10.0, 300)
+            D.reset()
+            D.decode_frames(torch.from_numpy(ll).to(f"cuda:{dev}"))
+            outs.append(D.best_paths(cap=4 * T + 64))
+    og = oracle_mod.OracleGraph(g)
+    for b in range(B):
+        r = og.decode(ll[:, b, :], 10.0, 300)
+        for res in outs:
+            n = res["n_arcs"][b]
+            assert list(res["arcs"][b, :n]) == list(r.arcs) and res["cost"][b] == r.cost32
