@@ -1175,18 +1175,18 @@ wfst_status wfst_get_partial_paths(wfst_decoder_t d, const int32_t* streams, int
   pp.status_out = p + 4 * n;
   pp.arcs_out = p + 6 * n;
   pp.olab_out = pp.arcs_out + (size_t)n * cp;
-  // shared memory: a set of wanted source states (2 slots per token) + one flag per token
-  pp.wcap = 32768;
+  // shared memory: a set of wanted source states (1.5 slots per token) + one flag per token
+  pp.wcap = 24576;   // 1.5 x fcap: two 512-thread CTAs per SM fit in shared memory
   pp.fcap = 16384;
   const size_t smem = (size_t)pp.wcap * 4 + (size_t)pp.fcap;
   if (d->partial_smem != smem) {
-    e = cudaFuncSetAttribute(partial_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(partial_kernel<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "partial kernel attribute");
     d->partial_smem = smem;
   }
   e = cudaMemcpy(p, ids.data(), 4 * (size_t)n, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "ids");
-  partial_kernel<1024><<<n, 1024, smem>>>(pp);
+  partial_kernel<512, 2><<<n, 512, smem>>>(pp);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cuda_fail(e, "partial kernel");

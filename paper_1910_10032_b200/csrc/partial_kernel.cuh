@@ -61,15 +61,15 @@ __device__ __forceinline__ bool pset_has(const uint32_t* set, uint32_t cap, uint
   }
 }
 
-template <int BS>
-__global__ void __launch_bounds__(BS, 1) partial_kernel(PartialParams p) {
+template <int BS, int MINB>
+__global__ void __launch_bounds__(BS, MINB) partial_kernel(PartialParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* set = (uint32_t*)smem_raw;                       // wanted source states
   unsigned char* flag = (unsigned char*)(set + p.wcap);      // tokens of the current layer in S
   __shared__ int s_changed, s_roots, s_root, s_status, s_len, s_idx, s_arc, s_layer, s_nw, s_nflag;
-  // the wanted-state set is sized to what can be wanted (twice the tokens flagged), so that
+  // the wanted-state set is sized to what can be wanted (1.5x the tokens flagged), so that
   // clearing it costs O(flagged tokens), not O(capacity), per step
-  auto set_cap = [&](int n) { return (uint32_t)min(p.wcap, max(64, 2 * n)); };
+  auto set_cap = [&](int n) { return (uint32_t)min(p.wcap, max(64, n + n / 2 + 1)); };   // load <= 2/3
   const int tid = threadIdx.x;
   const int ln = p.lanes[blockIdx.x];
   const LaneState* Lp = p.lanes_st + ln;
