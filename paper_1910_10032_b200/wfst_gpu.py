@@ -350,7 +350,8 @@ class Decoder:
         if rc == 1 and int(nar.max(initial=0)) > cap:
             return self._partial_merge(ids, arcs, ols, nar, nol, fr, cap)
         _check(rc)
-        return dict(arcs=[arcs[i, :nar[i]].copy() for i in range(n)], olabels=[ols[i, :nol[i]].copy() for i in range(n)],
+        # views into this call's fresh buffers (no per-stream copies: this runs every chunk)
+        return dict(arcs=[arcs[i, :nar[i]] for i in range(n)], olabels=[ols[i, :nol[i]] for i in range(n)],
                     settled_frames=fr)
 
     def _partial_merge(self, ids, arcs, ols, nar, nol, fr, cap):
