@@ -76,13 +76,14 @@ typedef struct {
 
 /* Decoder tuning; zero fields mean "default".  See DESIGN.md §5. */
 typedef struct {
-  int32_t table_slots;       /* per-stream on-chip token table slots (default: all free smem)     */
-  int32_t overflow_slots;    /* per-stream global overflow table slots (default max(32768, 4*alpha)) */
+  int32_t table_slots;       /* on-chip token table slots per CTA (default: all free shared memory) */
+  int32_t overflow_slots;    /* global overflow table slots per CTA (default max(C, 32768, 4*alpha)) */
   int64_t records_per_stream;/* traceback records per stream (default sized from max_frames)      */
   int32_t max_frames;        /* layers kept per stream (default 4096; a ring with opts.reclaim)   */
-  int32_t threads;           /* CTA size of the frame kernel (256/512/1024; default 512 or 256)   */
+  int32_t threads;           /* CTA size of the frame kernel (256/512/1024; default 1024 with one
+                                CTA per SM, else 256); the lattice and histogram modes use 1024   */
   int32_t frames_per_item;   /* frames a CTA runs on one stream before re-queueing (default 16)  */
-  int32_t max_ctas;          /* cap on persistent CTAs (default: #SMs)                            */
+  int32_t max_ctas;          /* cap on persistent CTAs (default: #SMs x ctas_per_sm)              */
   int32_t debug_costs;       /* 1: also keep each survivor's cost (wfst_debug_layer)              */
   int32_t ctas_per_sm;       /* resident lanes per SM (1-4; default 1); the on-chip table is sized
                                 from the SM's shared memory divided by this                       */
