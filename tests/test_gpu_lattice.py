@@ -166,3 +166,33 @@ def test_lattice_requires_option(W, torch):
     D.reset()
     with pytest.raises(W.WfstError):
         D.lattice(0)
+
+
+def test_lattice_with_stream_subsets(W, torch, oracle_mod):
+    """Decode calls on changing subsets of the streams (row f3) with lattices on: each call's
+    segments land in the right streams' arenas and layers."""
+    g = I.hclg_graph(3000, 6, 200, seed=4)
+    og = oracle_mod.OracleGraph(g)
+    emit = _emit_set(g)
+    T, B = 24, 4
+    pl = I.planted_walks(g, B, T, seed=9)
+    ll = I.loglikes(77, range(B), T, 200, pl, 1.0, 4.0)
+    G = W.Graph.from_arrays(g)
+    D = W.Decoder(G, B, 10.0, 300, lattice=1, lattice_beam=6.0)
+    D.reset()
+    t = torch.from_numpy(ll).cuda()
+    pos = [0] * B
+    schedule = [([0, 1], 5), ([2, 3], 7), ([3, 0], 6), ([1], 9), ([2], 10), ([0, 1, 3], 8), ([3, 2, 1, 0], 2), ([2], 7),
+                ([0], 5), ([1], 10), ([3], 10)]
+    for ids, n in schedule:
+        n = min(n, *(T - pos[b] for b in ids))
+        if n <= 0:
+            continue
+        x = torch.stack([t[pos[b]:pos[b] + n, b] for b in ids], dim=1).contiguous()
+        D.decode_frames(x, streams=np.array(ids, np.int32))
+        for b in ids:
+            pos[b] += n
+    assert pos == [T] * B
+    torch.cuda.synchronize()
+    for b in range(B):
+        _check_stream(D, og, ll[:, b, :], 10.0, 300, 6.0, b, emit)
