@@ -26,6 +26,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "wfst_oracle.c")
 _LIB = os.path.join(_HERE, "libwfst_oracle.so")
+# tests/test_oracle_mutations.py loads deliberately broken copies of the oracle (built from a
+# mutated scratch copy of wfst_oracle.c) to prove that the convention pins catch each mutation
+_LIB_OVERRIDE = os.environ.get("WFST_ORACLE_LIB")
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-pthread"]
 
 RC = {0: "OK", 1: "INVALID", 5: "PDF_RANGE", 6: "CAPACITY", 7: "NO_SURVIVOR", 9: "OOM"}
@@ -38,6 +41,8 @@ class OracleError(RuntimeError):
 
 
 def build(force: bool = False) -> str:
+    if _LIB_OVERRIDE:
+        return _LIB_OVERRIDE
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
     return _LIB
