@@ -8,21 +8,31 @@ A step = one pass of the whole hot path over one batch: 
 stream (start token + epsilon closure), decode all T frames of all B streams (one frame-kernel
 launch), final-cost argmin + traceback for every stream (one launch, paths copied to host).
 Log-likelihoods are device-resident for `value`; `e2e` repeats the step through the C ABI with
-pinned HOST log-likelihoods copied inside the timed region.  Multi-GPU: one process per GPU,
-each decoding its own B streams (global ids rank*B + b; weak scaling, no collective on the
-data path -- P:328-330).  Prints ONE JSON line on rank 0.
+pinned HOST log-likelihoods copied inside the timed region.  Prints ONE JSON line on rank 0.
+
+Multi-GPU (row e): one process per GPU, streams partitioned over the ranks, each rank
+with its own graph replica and decoder, no collective on the data path.  `--gpus N` launches
+the N ranks itself (torch.distributed.run) unless it already runs under a launcher (WORLD_SIZE
+set).  C3 (the headline) is weak-scaled (512 streams per GPU, global ids rank*512 + b); C5 is
+strong-scaled (4096 streams in total, contiguous blocks of 4096/N per rank).  After the timed
+region rank 0 gathers every global stream's result (host-side gather, the only data that moves
+between ranks) and re-decodes a sample of the other ranks' streams on its own GPU: the results
+must be identical (partition independence).
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import threading
 import time
+import zlib
 
 import numpy as np
 
@@ -46,11 +56,45 @@ def _peaks():
 
 
 def algorithmic_bytes(st: dict, frames: int, P: int) -> int:
-    """DESIGN.md §6 byte model per stream-frame, summed: 4P (log-likelihood row, read once)
-    + 12 per emitting arc (Eq. 1: dst, weight, pdf) + 8 per epsilon arc of a survivor (dst,
-    weight) + 36 per survivor (12 B state record (Eq. 1), 8 B traceback record, 8 B frontier
-    write + 8 B frontier read next frame)."""
-    return int(4 * P * frames + 12 * st["emit_arcs"] + 8 * st["eps_arcs"] + 36 * st["survivors"])
+    """SURVEY §8.5 byte model (what the method itself must move), summed over stream-frames:
+      16 n_src      frontier read (state + cost + 8 B of CSR row offsets)
+    + 12 n_arc_e    emitting arcs (Eq. 1: dst, weight, pdf)
+    + 4 P           the frame's log-likelihood row, read once
+    + 8 n_cand      u64 dedup update per distinct candidate
+    + 16 n_surv     frontier write 8 B + traceback record 8 B
+    + 16 n_arc_eps  epsilon arc read + update (epsilon out-degree of the kept tokens)
+    + 4 n_select    max-active selection: entries x passes, only when alpha binds
+    n_src and n_surv are both the survivor count (every survivor is written once and expanded
+    once in the next frame; the last layer of a step is written but not expanded -- 1/T of the
+    term)."""
+    return int(16 * st["survivors"] + 12 * st["emit_arcs"] + 4 * P * frames + 8 * st["candidates"]
+               + 16 * st["survivors"] + 16 * st["eps_arcs"] + 4 * st.get("select_entries", 0))
+
+
+def kernel_source_sha() -> str:
+    """Hash of the CUDA sources: an ncu traffic capture is valid only for the build it measured."""
+    d = os.path.join(ROOT, "paper_1910_10032_b200", "csrc")
+    h = hashlib.sha256()
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh", ".h")):
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(f.encode() + b"\0" + fh.read())
+    return h.hexdigest()[:16]
+
+
+def measured_traffic(cfg: str, preset: str):
+    """DRAM bytes per decode launch from a committed `ncu --set full` capture of THIS build
+    (profiles/*_traffic.json, tagged with kernel_source_sha); None when no capture matches."""
+    sha = kernel_source_sha()
+    d = os.path.join(ROOT, "profiles")
+    for f in sorted(os.listdir(d), reverse=True):
+        if not f.endswith("_traffic.json"):
+            continue
+        with open(os.path.join(d, f)) as fh:
+            t = json.load(fh)
+        if t.get("kernel_src_sha") == sha and t.get("config") == f"{cfg}/{preset}":
+            return float(t["dram_bytes_per_launch"]), f"profiles/{f} (ncu --set full of this build, sha {sha})"
+    return None, f"no ncu capture of this build (kernel sources sha {sha}) in profiles/"
 
 
 class ClockSampler:
@@ -118,6 +162,63 @@ def rank_streams(rank: int, world: int, per_rank: int) -> range:
     return range(rank * per_rank, (rank + 1) * per_rank)
 
 
+def partition(total: int, world: int, rank: int) -> range:
+    """Strong scaling: `total` global streams split into `world` contiguous near-equal blocks."""
+    assert 0 <= rank < world and total >= world
+    q, r = divmod(total, world)
+    start = rank * q + min(rank, r)
+    return range(start, start + q + (1 if rank < r else 0))
+
+
+def config_streams(c: dict, rank: int, world: int) -> range:
+    return partition(c["streams"], world, rank) if c.get("scaling") == "strong" else rank_streams(rank, world, c["streams"])
+
+
+def launcher_cmd(argv: list, n: int, port: int) -> list:
+    """`bench.py --gpus N` outside a launcher: one process per GPU via torch.distributed.run."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def result_digest(res: dict, i: int) -> tuple:
+    """(cost bits, reached_final, n_arcs, crc32 of the arc ids) of row i of a best_paths result."""
+    n = int(res["n_arcs"][i])
+    return (int(np.asarray(res["cost"][i], np.float32).view(np.uint32)), int(res["reached_final"][i]), n,
+            zlib.crc32(np.ascontiguousarray(res["arcs"][i, :n], np.int32).tobytes()))
+
+
+def gather_results(dist, world: int, ids, digests: list):
+    """Host-side gather of every rank's per-stream results to rank 0 (the only exchange of the
+    multi-GPU path, after the timed region).  Returns {global stream id: digest} on rank 0
+    (None elsewhere); asserts the partition covered every stream exactly once."""
+    local = (list(ids), list(digests))
+    if world == 1:
+        parts = [local]
+    else:
+        parts = [None] * world
+        dist.all_gather_object(parts, local)
+        if dist.get_rank() != 0:
+            return None
+    out = {}
+    for sid, dg in parts:
+        for s_, d_ in zip(sid, dg):
+            assert s_ not in out, f"stream {s_} decoded by two ranks"
+            out[s_] = d_
+    return out
+
+
+def distinct_devices(dist, world: int, local: int) -> int:
+    """GPUs actually used: distinct (host, device uuid) over the ranks (ranks sharing a device
+    under WFST_DIST_BACKEND=gloo count once)."""
+    import torch
+    me = (socket.gethostname(), str(torch.cuda.get_device_properties(local).uuid))
+    if world == 1:
+        return 1
+    allv = [None] * world
+    dist.all_gather_object(allv, me)
+    return len(set(allv))
+
+
 def reduce_over_ranks(dist, device, ms: float, arcs: float):
     """Max of the timed region and sum of arcs over ranks (the only collective, off the data path)."""
     import torch
@@ -129,17 +230,19 @@ def reduce_over_ranks(dist, device, ms: float, arcs: float):
 
 
 # ------------------------------------------------------------------------- workload
-def make_workload(cfg: str, preset: str, rank: int = 0, world: int = 1, beam=None, max_active=None):
+def make_workload(cfg: str, preset: str, rank: int = 0, world: int = 1, beam=None, max_active=None, graph=None,
+                  ids=None):
     c = dict(I.CONFIGS[cfg])
     if beam:
         c["beam"] = beam
     if max_active:
         c["max_active"] = max_active
-    g = I.config_graph(cfg)
-    B, T, P = c["streams"], c["frames"], c["n_pdfs"]
-    stream0 = rank_streams(rank, world, B).start
+    g = graph if graph is not None else I.config_graph(cfg)
+    ids = ids if ids is not None else config_streams(c, rank, world)
+    B, T, P = len(ids), c["frames"], c["n_pdfs"]
+    stream0 = ids.start
     planted = I.planted_walks(g, B, T, seed=c["ll_seed"], stream0=stream0)
-    return dict(cfg=cfg, c=c, graph=g, B=B, T=T, P=P, stream0=stream0, planted=planted,
+    return dict(cfg=cfg, c=c, graph=g, B=B, T=T, P=P, stream0=stream0, ids=ids, planted=planted,
                 preset=I.preset(preset), preset_name=preset, beam=c["beam"], alpha=c["max_active"])
 
 
@@ -183,6 +286,32 @@ def decoder_opts(args) -> dict:
 
 
 # ------------------------------------------------------------------------- GPU arm
+def cross_check(W, torch, wl_cfg, preset, graph, G, gathered: dict, world: int, dev, args, per_rank: int = 4):
+    """Rank 0 re-decodes the first `per_rank` streams of every OTHER rank's block on its own GPU
+    (global ids, inputs regenerated from them) and compares with the gathered results: a stream's
+    result must not depend on which GPU decoded it or how the streams were split."""
+    c = I.CONFIGS[wl_cfg]
+    ids = []
+    for r in range(1, world):
+        blk = config_streams(c, r, world)
+        ids.append(range(blk.start, blk.start + min(per_rank, len(blk))))
+    n_checked = n_bad = 0
+    for blk in ids:
+        wl = make_workload(wl_cfg, preset, beam=args.beam, max_active=args.max_active, graph=graph, ids=blk)
+        D = W.Decoder(G, wl["B"], wl["beam"], wl["alpha"], **decoder_opts(args))
+        ll = device_loglikes(W, torch, wl, dev)
+        chunk = wl["c"].get("chunk") or wl["T"]
+        D.reset()
+        for t0 in range(0, wl["T"], chunk):
+            D.decode_frames(ll[t0:t0 + chunk].contiguous() if chunk < wl["T"] else ll)
+        res = D.best_paths(cap=4 * wl["T"] + 64, raise_on_error=False)
+        for i, sid in enumerate(blk):
+            n_checked += 1
+            n_bad += int(result_digest(res, i) != gathered[sid])
+        del D, ll
+    return n_checked, n_bad
+
+
 def gpu_arm(args):
     import torch
     import torch.distributed as dist
@@ -192,8 +321,8 @@ def gpu_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # one process per GPU; WFST_DIST_BACKEND=gloo lets a multi-rank run share fewer GPUs (used to
-    # exercise the multi-rank path on a one-GPU box -- the only collectives are a barrier and a
-    # two-number reduction, never on the data path)
+    # exercise the multi-rank path on a one-GPU box -- the only collectives are a barrier, a
+    # two-number reduction and the final result gather, never on the data path)
     backend = os.environ.get("WFST_DIST_BACKEND", "nccl")
     if backend == "gloo":
         local = local % max(1, torch.cuda.device_count())
@@ -212,6 +341,7 @@ def gpu_arm(args):
 
     wl = make_workload(args.config, args.preset, rank, world, args.beam, args.max_active)
     T, B, P = wl["T"], wl["B"], wl["P"]
+    strong = wl["c"].get("scaling") == "strong"
     G = W.Graph.from_arrays(wl["graph"], device=local)
     ginfo = G.info()
     D = W.Decoder(G, B, wl["beam"], wl["alpha"], **decoder_opts(args))
@@ -234,7 +364,7 @@ def gpu_arm(args):
 
     for _ in range(args.warmup):
         res = step()
-    assert res["rc"] == 0, W.STATUS.get(res["rc"])
+        assert res["rc"] == 0, W.STATUS.get(res["rc"])
     D.reset_stats()
     torch.cuda.synchronize(dev)
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -242,12 +372,17 @@ def gpu_arm(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    rcs = []
     with ClockSampler(local) as clk:
         t0.record()
         for k in range(args.steps):
             res = step(kev[k])
+            rcs.append(int(res["rc"]))
         t1.record()
         torch.cuda.synchronize(dev)
+    # a lane that hit CAPACITY stops decoding and would make a step look faster: every timed
+    # step must have decoded every stream
+    assert all(r == 0 for r in rcs), f"timed steps with errors: {[W.STATUS.get(r, r) for r in rcs]}"
     ms = t0.elapsed_time(t1)
     kern_ms = [a.elapsed_time(b) for a, b in kev]
     st = D.stats()
@@ -256,8 +391,23 @@ def gpu_arm(args):
     else:
         ms_max = ms
         arcs_all = float(st["emit_arcs"] + st["eps_arcs"])
-    audio_s = args.steps * B * T * FRAME_S * world
+    total_streams = wl["c"]["streams"] if strong else B * world
+    audio_s = args.steps * total_streams * T * FRAME_S
     value = audio_s / (ms_max / 1e3)
+
+    # ---- host-side gather of every global stream's result (after the timed region) + a
+    # partition-independence check on rank 0
+    digests = [result_digest(res, i) for i in range(B)]
+    gathered = gather_results(dist, world, wl["ids"], digests)
+    n_dev = distinct_devices(dist, world, local)
+    gather = None
+    if rank == 0:
+        assert sorted(gathered) == list(range(total_streams)), "streams missing from the gather"
+        n_chk, n_bad = cross_check(W, torch, args.config, args.preset, wl["graph"], G, gathered, world, dev, args) \
+            if world > 1 else (0, 0)
+        assert n_bad == 0, f"{n_bad} of {n_chk} streams decoded differently on rank 0"
+        gather = {"streams": len(gathered), "rechecked_on_rank0": n_chk, "mismatches": n_bad,
+                  "digest": "%08x" % zlib.crc32(json.dumps([gathered[k] for k in sorted(gathered)]).encode())}
 
     # ---- e2e: host log-likelihoods through the C ABI, H2D inside the timed region
     e2e = None
@@ -280,16 +430,19 @@ def gpu_arm(args):
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        e_rcs = []
         for _ in range(e2e_steps):
             r = step_host()
+            e_rcs.append(int(r["rc"]))
         e1.record()
         torch.cuda.synchronize(dev)
+        assert all(x == 0 for x in e_rcs)
         ems = e0.elapsed_time(e1)
         if world > 1:
             ems, _ = reduce_over_ranks(dist, red_dev, ems, 0.0)
         d2h = B * (4 + 4 + 4 + 4 + 4 + 2 * cap * 4)
-        e2e = {"value": e2e_steps * B * T * FRAME_S * world / (ems / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": T * B * P * 4 * world, "d2h_bytes_per_step": d2h * world,
+        e2e = {"value": e2e_steps * total_streams * T * FRAME_S / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": T * total_streams * P * 4, "d2h_bytes_per_step": d2h * world,
                "steps": e2e_steps, "ms_per_step": ems / e2e_steps}
 
     if rank != 0:
@@ -298,40 +451,42 @@ def gpu_arm(args):
         return None
 
     peak, peak_src = _peaks()
-    traffic, traffic_src = args.traffic, None
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
-    if traffic is None and os.path.exists(tpath) and args.config == "c3" and args.preset == "clean":
-        with open(tpath) as f:
-            t = json.load(f)
-        traffic, traffic_src = t["dram_bytes_per_launch"], "profiles/r01_traffic.json (ncu --set full, same launch)"
+    if args.traffic is not None:
+        traffic, traffic_src = args.traffic, "--traffic"
+    else:
+        traffic, traffic_src = measured_traffic(args.config, args.preset)
     frames_per_step = B * T
     abytes = algorithmic_bytes(st, frames_per_step * args.steps, P) / args.steps
     kmean = statistics.mean(kern_ms)
     achieved = abytes / (kmean / 1e3) / 1e9
     clocks = clk.summary()
     out = {
-        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": n_dev, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config} ({wl['c']['graph'] if isinstance(wl['c']['graph'], str) else 'HCLG-shaped'}"
-                               f" {ginfo.n_states} states / {ginfo.n_arcs} arcs, {P} pdfs, {B} streams x {T} frames"
-                               f" per GPU, beam {wl['beam']}, max_active {wl['alpha']}, preset {args.preset})",
-                   "streams_per_gpu": B, "frames": T, "pdfs": P, "beam": wl["beam"], "max_active": wl["alpha"],
-                   "preset": args.preset, "frame_ms": 10, "parallelism": f"streams partitioned over {world} GPU(s)",
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config} ({wl['c'].get('graph_kind', 'HCLG-shaped') if not isinstance(wl['c']['graph'], str) else wl['c']['graph']}"
+                               f" {ginfo.n_states} states / {ginfo.n_arcs} arcs, {P} pdfs, "
+                               + (f"{total_streams} streams split over {world} rank(s)" if strong else f"{B} streams per GPU")
+                               + f" x {T} frames, beam {wl['beam']}, max_active {wl['alpha']}, preset {args.preset})",
+                   "streams_per_gpu": B, "streams_total": total_streams, "frames": T, "pdfs": P, "beam": wl["beam"],
+                   "max_active": wl["alpha"], "preset": args.preset, "frame_ms": 10,
+                   "parallelism": f"streams partitioned over {world} rank(s) on {n_dev} GPU(s)",
                    "l2": "inputs larger than L2 (log-likelihoods %.2f GB per GPU)" % (T * B * P * 4 / 1e9),
                    "frames_per_call": chunk},
         "rtfx_30ms": round(value * 3, 1),
         "arcs_per_s": round(arcs_all * 1e3 / (ms_max), 1) if ms_max else None,
-        "frames_per_s": round(args.steps * frames_per_step * world / (ms_max / 1e3), 1),
+        "frames_per_s": round(args.steps * total_streams * T / (ms_max / 1e3), 1),
         "e2e": e2e,
         # per step: reset = settle-point reset + init frame kernel, one frame-kernel launch per
         # chunk (+ one lattice launch each with --lattice, + one on reset), best paths
-        "gpu_launches": (3 + (T + chunk - 1) // chunk * (2 if args.lattice is not None else 1)
+        "gpu_launches": (3 + (T + chunk - 1) // chunk * ((2 if args.lattice is not None else 1) + (1 if args.partial else 0))
                          + (2 if args.lattice is not None else 0)) * args.steps,
         "decoder_opts": decoder_opts(args),
         "roofline": {"bound": "hbm", "kernel": "frame_kernel", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": int(abytes),
+                     "byte_model": "SURVEY §8.5: 16 n_src + 12 n_arc_e + 4 P + 8 n_cand + 16 n_surv + 16 n_arc_eps"
+                                   " + 4 n_select per stream-frame (bench.algorithmic_bytes)",
                      "kernel_ms": round(kmean, 3), "kernel_share_of_step": round(kmean / (ms_max / args.steps), 3),
                      "peak_source": peak_src},
         "counters_per_step": {k: v / args.steps for k, v in st.items()
@@ -339,7 +494,9 @@ def gpu_arm(args):
         "phase_share": {k: round(v / max(1, sum(st["phase_cycles"].values())), 4) for k, v in st["phase_cycles"].items()},
         "memory": {"graph_device_bytes": ginfo.device_bytes, "graph_eq1_bytes": ginfo.eq1_bytes,
                    "decoder_device_bytes": st["device_bytes"],
+                   "records_used_max_per_stream": st["records_used_max"],
                    "eq2_bytes_nc=nl=B": W.eq2_bytes(wl["alpha"], B, B)},
+        "gather": gather,
         "clocks": clocks,
     }
     if not args.no_cpu_baseline:
@@ -400,7 +557,8 @@ def reference_arm(args):
     value = args.steps * n * wl["T"] * FRAME_S / tot
     out = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": 0,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 1),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "higher_is_better": True, "scaling": "strong" if wl["c"].get("scaling") == "strong" else "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic",
            "config": {"workload": f"{args.config} ({n} of {wl['B']} streams per step)", "preset": args.preset,
                       "frames": wl["T"], "beam": wl["beam"], "max_active": wl["alpha"]},
            "arcs_per_s": round(arcs / tot, 1),
@@ -440,6 +598,21 @@ def main(argv=None):
         args.warmup = 3
     if args.impl == "reference":
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: launch the ranks ourselves (the driver's torchrun sets WORLD_SIZE)
+        import torch
+        n_dev = torch.cuda.device_count()
+        if args.gpus > n_dev and os.environ.get("WFST_DIST_BACKEND", "nccl") == "nccl":
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {n_dev} CUDA device(s) visible\n")
+            sys.exit(2)
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        argv = sys.argv[1:] if argv is None else list(argv)
+        sys.exit(subprocess.call(launcher_cmd(argv, args.gpus, port)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and int(os.environ.get("RANK", "0")) == 0:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} under a launcher of {world} rank(s): using {world}\n")
     return gpu_arm(args)
 
 

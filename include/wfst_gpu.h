@@ -26,9 +26,16 @@
  *   - Every function returns wfst_status; WFST_OK = 0.  On error, a
  *     thread-local message is available from wfst_last_error().
  *   - Device work is asynchronous on the caller's CUDA stream (void* =
- *     cudaStream_t, NULL = legacy default stream).  Device-side failures
- *     (capacity, no survivor) are sticky per stream and surface at
- *     wfst_decoder_sync / wfst_get_best_path / wfst_decoder_status.
+ *     cudaStream_t, NULL = legacy default stream).  A decoder's calls are
+ *     ordered among themselves even across CUDA streams: a call on stream s
+ *     first makes s wait (cudaStreamWaitEvent) for the decoder's previous
+ *     work, which shares its scratch, work queue and lane states.  Calls that
+ *     return results (best / partial paths, sync, stats) run on the stream of
+ *     the decoder's last call and wait for THIS decoder's work only (an event),
+ *     never for the whole device, so decoders on other streams or devices keep
+ *     running.  Device-side failures (capacity, no survivor) are sticky per
+ *     stream and surface at wfst_decoder_sync / wfst_get_best_path /
+ *     wfst_decoder_status.
  * Ownership
  *   - A graph is immutable after creation, bound to one device, safe for
  *     concurrent reads, and must outlive every decoder created on it.
@@ -117,6 +124,8 @@ typedef struct {
                                 1 cutoff, 2 epsilon, 3 expansion (warp tokens), 4 expansion (hub
                                 tokens), 5 frame overhead, 6 drain, 7 map build, 8 placement,
                                 9 epsilon back-pointers, 10 table reset, 11 row wait            */
+  int64_t select_entries;    /* token-table entries read by the max-active selection, summed over
+                                passes (SURVEY §8.5's passes x n_uniq term of the byte model)     */
 } wfst_stats_t;
 
 /* ---- graph (row a0 of SURVEY §8) ------------------------------------------------ */
@@ -175,7 +184,8 @@ wfst_status wfst_decode_frames_host(wfst_decoder_t d, const float* h_loglikes, i
                                     int32_t B, int32_t P, const int32_t* streams,
                                     int32_t chunk_frames, void* cuda_stream);
 
-/* Wait for all work of the decoder; returns the first sticky per-stream error, if any. */
+/* Wait for the decoder's work (its event; not the device); returns the first sticky per-stream
+ * error, if any. */
 wfst_status wfst_decoder_sync(wfst_decoder_t d);
 /* Sticky status of one lane (after sync). */
 wfst_status wfst_decoder_status(wfst_decoder_t d, int32_t stream);
@@ -183,7 +193,8 @@ wfst_status wfst_decoder_status(wfst_decoder_t d, int32_t stream);
 /* One-best result of a lane (reading R10/R11): final-cost argmin over the current survivors
  * (fallback: best cost, *reached_final = 0), then traceback.  olabels: non-zero output labels
  * in order; arcs: canonical arc ids of the path (nullable).  A too-small cap returns
- * INVALID_ARG with the needed size in *n_olabels / *n_arcs.  Synchronises the decoder. */
+ * INVALID_ARG with the needed size in *n_olabels / *n_arcs.  The traceback kernel runs on the
+ * stream of the decoder's last call, after its work; the call waits for that stream only. */
 wfst_status wfst_get_best_path(wfst_decoder_t d, int32_t stream, int32_t* olabels,
                                int32_t olabels_cap, int32_t* n_olabels, int32_t* arcs,
                                int32_t arcs_cap, int32_t* n_arcs, float* cost,
@@ -191,10 +202,17 @@ wfst_status wfst_get_best_path(wfst_decoder_t d, int32_t stream, int32_t* olabel
 
 /* Batched form: n lanes in one launch.  Per lane i: cost[i], reached_final[i], n_arcs[i], and
  * arcs[i*arcs_cap ...] (canonical ids; nullable), olabels[i*arcs_cap ...] with n_olabels[i]
- * (nullable).  All outputs are host arrays.  Returns the first error among the lanes. */
+ * (nullable).  All outputs are host arrays.  Returns the first error among the lanes; n_olabels[i]
+ * counts every olabel of the path even when the arcs were truncated to arcs_cap. */
 wfst_status wfst_get_best_paths(wfst_decoder_t d, const int32_t* streams, int32_t n, float* cost,
                                 int32_t* reached_final, int32_t* arcs, int32_t* olabels,
                                 int32_t arcs_cap, int32_t* n_arcs, int32_t* n_olabels);
+/* Same, plus status[i] (host, n entries; nullable): each lane's own result status (OK, its sticky
+ * decode error, STATE if never reset, INVALID_ARG if its path exceeded arcs_cap). */
+wfst_status wfst_get_best_paths_ex(wfst_decoder_t d, const int32_t* streams, int32_t n, float* cost,
+                                   int32_t* reached_final, int32_t* arcs, int32_t* olabels,
+                                   int32_t arcs_cap, int32_t* n_arcs, int32_t* n_olabels,
+                                   int32_t* status);
 
 wfst_status wfst_decoder_stats(wfst_decoder_t d, wfst_stats_t* s);
 wfst_status wfst_decoder_reset_stats(wfst_decoder_t d);
@@ -220,12 +238,19 @@ wfst_status wfst_debug_layer(wfst_decoder_t d, int32_t stream, int32_t layer, in
  * settled prefix, which is always a prefix of the final wfst_get_best_path result.
  *   arcs/olabels: host [n][cap] (nullable); n_arcs[i] / n_olabels[i] (nullable): counts;
  *   settled_frames[i]: frames (= layer) covered by the settled prefix so far.
- * Synchronises the decoder.  A stream whose new arcs exceed cap returns INVALID_ARG with the
- * needed count in n_arcs[i] and keeps its settle point (call again with a larger cap).
- * Layers of more than 16384 tokens return CAPACITY. */
+ * Runs on the stream of the decoder's last call after its work (waits for that stream only).
+ * A stream whose new arcs exceed cap returns INVALID_ARG with the needed count in n_arcs[i] and
+ * keeps its settle point (call again with a larger cap).  Layers of more than 16384 tokens return
+ * CAPACITY.  The return value is the first error among the streams. */
 wfst_status wfst_get_partial_paths(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
                                    int32_t* olabels, int32_t cap, int32_t* n_arcs, int32_t* n_olabels,
                                    int32_t* settled_frames);
+/* Same, plus status[i] (host, n entries; nullable): each stream's own status, so one stream's
+ * error (or cap overflow) does not hide the others' results: a stream with status OK has
+ * advanced its settle point and its arcs are valid whatever the return value. */
+wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
+                                      int32_t* olabels, int32_t cap, int32_t* n_arcs, int32_t* n_olabels,
+                                      int32_t* settled_frames, int32_t* status);
 
 /* ---- lattice (row f1 of SURVEY §8, NEXT) ----------------
  * With opts.lattice = 1 every reset and decode call also builds, per stream and frame, the lattice

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kBestPathThreads) best_path_kernel(KParams p, 
                                  int32_t n, int32_t cap, float* cost_out, int32_t* reached_out, int32_t* n_arcs_out,
                                  int32_t* arcs_out, int32_t* olab_out, int32_t* n_olab_out, int32_t* status_out) {
   __shared__ u64 s_fin[32], s_any[32];
-  __shared__ int s_idx, s_arc, s_layer, s_len, s_status;
+  __shared__ int s_idx, s_arc, s_layer, s_len, s_nol, s_status;
   const int li = blockIdx.x;
   const int lane = lanes[li];
   const int tid = threadIdx.x;
@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kBestPathThreads) best_path_kernel(KParams p, 
   if (tid == 0) {
     s_idx = -1;
     s_len = 0;
+    s_nol = 0;
     s_status = WFST_OK;
   }
   __syncthreads();
@@ -120,10 +121,12 @@ __global__ void __launch_bounds__(kBestPathThreads) best_path_kernel(KParams p, 
   const long long max_steps = (long long)L.rec_used + 2;
   for (long long step = 0; step < max_steps; step++) {
     const int arc = s_arc;
+    const int cur_layer = s_layer;
+    __syncthreads();   // every thread has read s_arc / s_layer / s_idx before thread 0 rewrites them
     if (arc < 0) break;
     // traceback GC (row f2): below the settle point the path was already handed out by
     // wfst_get_partial_paths -- stop at the settled root (entered by an emitting arc)
-    if (s_layer == L.layer_floor && L.layer_floor > 0 && __ldg(&p.arcs[arc].z) >= 0) break;
+    if (cur_layer == L.layer_floor && L.layer_floor > 0 && __ldg(&p.arcs[arc].z) >= 0) break;
     int src = 0, layer = 0;
     if (tid == 0) {
       const int4 a = __ldg(p.arcs + arc);
@@ -131,6 +134,7 @@ __global__ void __launch_bounds__(kBestPathThreads) best_path_kernel(KParams p, 
       layer = a.z >= 0 ? s_layer - 1 : s_layer;
       if (s_len < cap) out[s_len] = arc;
       s_len++;
+      if (__ldg(olabel + arc) != 0) s_nol++;   // counted over the whole walk (the size a caller needs)
       s_idx = -1;
       s_layer = layer;
       s_arc = src;   // temporarily: the state to look for
@@ -169,12 +173,9 @@ __global__ void __launch_bounds__(kBestPathThreads) best_path_kernel(KParams p, 
   int nol = 0;
   for (int k = 0; k < m; k++) {
     const int32_t ol = __ldg(olabel + out[k]);
-    if (ol != 0) {
-      if (nol < cap) olab_out[(size_t)li * cap + nol] = ol;
-      nol++;
-    }
+    if (ol != 0 && nol < cap) olab_out[(size_t)li * cap + nol++] = ol;
   }
-  n_olab_out[li] = nol;
+  n_olab_out[li] = s_nol;   // every olabel of the path, also when the arcs were truncated
   status_out[li] = s_status != WFST_OK ? s_status : (len > cap ? WFST_ERR_INVALID_ARG : WFST_OK);
 }
 
@@ -245,6 +246,15 @@ struct wfst_decoder_s {
   std::vector<int32_t> h_initialized;
   std::vector<int32_t> cur_ids;    // mapping currently in d_lane_ids
   int64_t device_bytes = 0;
+  // Stream ordering: every call that enqueues device work first orders its CUDA stream after
+  // the decoder's previous work (which shares the scratch, the work queue and the lane states
+  // and may have been enqueued on another stream), then records ev_work after its own work.
+  // Result calls (best paths, partial paths, stats) run on work_stream and wait for ev_work
+  // only -- never for the whole device.
+  cudaEvent_t ev_work = nullptr;
+  cudaStream_t work_stream = nullptr;
+  bool has_work = false;
+  int32_t* h_path = nullptr;       // pinned staging of the result calls (path_cap int32)
 };
 
 namespace {
@@ -257,6 +267,45 @@ struct DeviceGuard {
   }
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
+
+// order stream st after the decoder's previous work (no-op on the same stream)
+cudaError_t order_after_previous(wfst_decoder_t d, cudaStream_t st) {
+  if (d->has_work && st != d->work_stream) return cudaStreamWaitEvent(st, d->ev_work, 0);
+  return cudaSuccess;
+}
+// st now carries the decoder's latest work
+cudaError_t mark_work(wfst_decoder_t d, cudaStream_t st) {
+  d->work_stream = st;
+  d->has_work = true;
+  return cudaEventRecord(d->ev_work, st);
+}
+// wait for the decoder's work only (and for the copy stream of the lattice / host-input paths)
+cudaError_t wait_work(wfst_decoder_t d) {
+  cudaError_t e = d->has_work ? cudaEventSynchronize(d->ev_work) : cudaSuccess;
+  if (e == cudaSuccess && d->copy_stream) e = cudaStreamSynchronize(d->copy_stream);
+  return e;
+}
+// device -> host copy ordered after the decoder's work, on its stream (no device-wide sync)
+cudaError_t d2h(wfst_decoder_t d, void* dst, const void* src, size_t bytes) {
+  cudaError_t e = wait_work(d);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, d->work_stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(d->work_stream);
+  return e;
+}
+// grow the device + pinned result buffers of the path calls to `need` int32
+cudaError_t ensure_path(wfst_decoder_t d, size_t need) {
+  if (need <= d->path_cap) return cudaSuccess;
+  cudaError_t e = wait_work(d);
+  cudaFree(d->d_path);
+  if (d->h_path) cudaFreeHost(d->h_path);
+  d->d_path = nullptr;
+  d->h_path = nullptr;
+  d->path_cap = 0;
+  if (e == cudaSuccess) e = cudaMalloc(&d->d_path, need * 4);
+  if (e == cudaSuccess) e = cudaMallocHost(&d->h_path, need * 4);
+  if (e == cudaSuccess) d->path_cap = need;
+  return e;
+}
 
 #ifndef WFST_R1024
 #define WFST_R1024 2   // arcs in flight per thread in the default 1024-thread kernel
@@ -491,6 +540,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     e = cudaEventCreateWithFlags(&d->ev_up[k], cudaEventDisableTiming);
   if (e == cudaSuccess) d->d_lane_ids = d->d_id_ring;
   if (e == cudaSuccess) e = cudaMalloc(&d->d_settled, sizeof(int2) * L);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_work, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMemset(d->d_settled, 0xFF, sizeof(int2) * L);
   if (e != cudaSuccess) {
     cudaFree(d->d_pool);
@@ -593,7 +643,9 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
 void wfst_decoder_destroy(wfst_decoder_t d) {
   if (!d) return;
   DeviceGuard dg(d->device);
-  cudaDeviceSynchronize();
+  wait_work(d);
+  if (d->ev_work) cudaEventDestroy(d->ev_work);
+  if (d->h_path) cudaFreeHost(d->h_path);
   cudaFree(d->d_pool);
   cudaFree(d->d_lanes);
   cudaFree(d->d_qhead);
@@ -665,6 +717,8 @@ wfst_status wfst_decoder_reset(wfst_decoder_t d, const int32_t* streams, int32_t
   cudaStream_t st = (cudaStream_t)cuda_stream;
   int32_t B = streams ? n : d->n_lanes;
   if (B <= 0) return WFST_OK;
+  cudaError_t eo = order_after_previous(d, st);
+  if (eo != cudaSuccess) return cuda_fail(eo, "stream order");
   wfst_status s = set_lanes(d, streams, B, st, false);
   if (s != WFST_OK) return s;
   KParams kp = d->kp;
@@ -686,6 +740,7 @@ wfst_status wfst_decoder_reset(wfst_decoder_t d, const int32_t* streams, int32_t
   }
   for (int32_t i = 0; i < B; i++) d->h_initialized[streams ? streams[i] : i] = 1;
   e = cudaEventRecord(d->ev_ids[d->id_slot], st);   // the slot is free once this work is done
+  if (e == cudaSuccess) e = mark_work(d, st);
   return e == cudaSuccess ? WFST_OK : cuda_fail(e, "event");
 }
 
@@ -699,6 +754,8 @@ wfst_status wfst_decode_frames(wfst_decoder_t d, const float* d_loglikes, int32_
   if (P <= d->g->max_pdf) return fail(WFST_ERR_PDF_RANGE, "P=" + std::to_string(P) + " <= max pdf " + std::to_string(d->g->max_pdf));
   DeviceGuard dg(d->device);
   cudaStream_t st = (cudaStream_t)cuda_stream;
+  cudaError_t eo = order_after_previous(d, st);
+  if (eo != cudaSuccess) return cuda_fail(eo, "stream order");
   wfst_status s = set_lanes(d, streams, B, st, true);
   if (s != WFST_OK) return s;
   KParams kp = d->kp;
@@ -723,6 +780,7 @@ wfst_status wfst_decode_frames(wfst_decoder_t d, const float* d_loglikes, int32_
     if (e != cudaSuccess) return cuda_fail(e, "lattice launch");
   }
   e = cudaEventRecord(d->ev_ids[d->id_slot], st);   // the slot is free once this work is done
+  if (e == cudaSuccess) e = mark_work(d, st);
   return e == cudaSuccess ? WFST_OK : cuda_fail(e, "event");
 }
 
@@ -748,10 +806,12 @@ wfst_status wfst_decode_frames_host(wfst_decoder_t d, const float* h_loglikes, i
   cudaStream_t st = (cudaStream_t)cuda_stream;
   int32_t CF = chunk_frames > 0 ? std::min(chunk_frames, T) : std::min(T, 25);
   size_t need = (size_t)CF * B * P * 4;
-  cudaError_t e = cudaSuccess;
+  // the staging buffers below are then free once earlier work of ANY stream is done
+  cudaError_t e = order_after_previous(d, st);
+  if (e != cudaSuccess) return cuda_fail(e, "stream order");
   if (need > d->stage_bytes) {
+    wait_work(d);
     cudaStreamSynchronize(st);
-    if (d->copy_stream) cudaStreamSynchronize(d->copy_stream);
     for (int i = 0; i < wfst_decoder_s::kStages; i++) {
       cudaFree(d->d_host_stage[i]);
       d->d_host_stage[i] = nullptr;
@@ -809,10 +869,8 @@ wfst_status wfst_decode_frames_host(wfst_decoder_t d, const float* h_loglikes, i
 wfst_status wfst_decoder_sync(wfst_decoder_t d) {
   if (!d) return fail(WFST_ERR_INVALID_ARG, "NULL decoder");
   DeviceGuard dg(d->device);
-  cudaError_t e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) return cuda_fail(e, "sync");
   std::vector<LaneState> L(d->n_lanes);
-  e = cudaMemcpy(L.data(), d->d_lanes, sizeof(LaneState) * d->n_lanes, cudaMemcpyDeviceToHost);
+  cudaError_t e = d2h(d, L.data(), d->d_lanes, sizeof(LaneState) * d->n_lanes);
   if (e != cudaSuccess) return cuda_fail(e, "lane state");
   for (int i = 0; i < d->n_lanes; i++)
     if (L[i].status != WFST_OK)
@@ -825,15 +883,15 @@ wfst_status wfst_decoder_status(wfst_decoder_t d, int32_t stream) {
   if (!d || stream < 0 || stream >= d->n_lanes) return fail(WFST_ERR_INVALID_ARG, "bad argument");
   DeviceGuard dg(d->device);
   LaneState L;
-  cudaError_t e = cudaMemcpy(&L, d->d_lanes + stream, sizeof L, cudaMemcpyDeviceToHost);
+  cudaError_t e = d2h(d, &L, d->d_lanes + stream, sizeof L);
   if (e != cudaSuccess) return cuda_fail(e, "lane state");
   if (!d->h_initialized[stream]) return WFST_ERR_STATE;
   return (wfst_status)L.status;
 }
 
-wfst_status wfst_get_best_paths(wfst_decoder_t d, const int32_t* streams, int32_t n, float* cost,
-                                int32_t* reached_final, int32_t* arcs, int32_t* olabels, int32_t arcs_cap,
-                                int32_t* n_arcs, int32_t* n_olabels) {
+wfst_status wfst_get_best_paths_ex(wfst_decoder_t d, const int32_t* streams, int32_t n, float* cost,
+                                   int32_t* reached_final, int32_t* arcs, int32_t* olabels, int32_t arcs_cap,
+                                   int32_t* n_arcs, int32_t* n_olabels, int32_t* status) {
   if (!d || n < 0 || !cost || !reached_final || !n_arcs) return fail(WFST_ERR_INVALID_ARG, "bad argument");
   if (n == 0) return WFST_OK;
   DeviceGuard dg(d->device);
@@ -843,21 +901,13 @@ wfst_status wfst_get_best_paths(wfst_decoder_t d, const int32_t* streams, int32_
     if (s < 0 || s >= d->n_lanes) return fail(WFST_ERR_INVALID_ARG, "stream id out of range");
     if (!d->h_initialized[s]) return fail(WFST_ERR_STATE, "stream " + std::to_string(s) + " not reset");
   }
-  cudaError_t e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) return cuda_fail(e, "sync");
   int cap = std::max(arcs_cap, 1);
-  size_t need = (size_t)n * (6 + 2 * (size_t)cap);
-  if (need > d->path_cap) {
-    cudaFree(d->d_path);
-    d->d_path = nullptr;
-    e = cudaMalloc(&d->d_path, need * 4);
-    if (e != cudaSuccess) {
-      d->path_cap = 0;
-      return cuda_fail(e, "path buffer");
-    }
-    d->path_cap = need;
-  }
+  cudaError_t e = ensure_path(d, (size_t)n * (6 + 2 * (size_t)cap));
+  if (e != cudaSuccess) return cuda_fail(e, "path buffer");
+  // on the decoder's work stream, after its last decode: only this decoder's work is awaited
+  cudaStream_t st = d->work_stream;
   int32_t* p = d->d_path;
+  int32_t* h = d->h_path;
   int32_t* d_ids = p;
   float* d_cost = (float*)(p + n);
   int32_t* d_reached = p + 2 * n;
@@ -866,35 +916,55 @@ wfst_status wfst_get_best_paths(wfst_decoder_t d, const int32_t* streams, int32_
   int32_t* d_st = p + 5 * n;
   int32_t* d_arcs = p + 6 * n;
   int32_t* d_ol = d_arcs + (size_t)n * cap;
-  std::vector<int32_t> ids(n);
-  for (int i = 0; i < n; i++) ids[i] = streams ? streams[i] : i;
-  e = cudaMemcpy(d_ids, ids.data(), 4 * (size_t)n, cudaMemcpyHostToDevice);
+  for (int i = 0; i < n; i++) h[i] = streams ? streams[i] : i;
+  e = cudaMemcpyAsync(d_ids, h, 4 * (size_t)n, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_fail(e, "ids");
-  best_path_kernel<<<n, kBestPathThreads>>>(d->kp, d->g->d_olabel, d_ids, n, cap, d_cost, d_reached, d_nar, d_arcs, d_ol, d_nol,
-                               d_st);
+  best_path_kernel<<<n, kBestPathThreads, 0, st>>>(d->kp, d->g->d_olabel, d_ids, n, cap, d_cost, d_reached, d_nar,
+                                                   d_arcs, d_ol, d_nol, d_st);
   e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, p, 4 * 6 * (size_t)n, cudaMemcpyDeviceToHost, st);
+  // only the columns some stream used (a path is ~T arcs, cap is an upper bound)
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "best path kernel");
-  std::vector<int32_t> head(6 * (size_t)n);
-  e = cudaMemcpy(head.data(), p, 4 * head.size(), cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && arcs && arcs_cap > 0)
-    e = cudaMemcpy(arcs, d_arcs, 4 * (size_t)n * cap, cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && olabels && arcs_cap > 0)
-    e = cudaMemcpy(olabels, d_ol, 4 * (size_t)n * cap, cudaMemcpyDeviceToHost);
+  int mx_a = 0, mx_o = 0;
+  for (int i = 0; i < n; i++) {
+    mx_a = std::max(mx_a, std::min(h[3 * n + i], cap));
+    mx_o = std::max(mx_o, std::min(h[4 * n + i], cap));
+  }
+  int32_t* h_arcs = h + 6 * n;
+  int32_t* h_ol = h_arcs + (size_t)n * cap;
+  const size_t pitch = 4 * (size_t)cap;
+  if (arcs && arcs_cap > 0 && mx_a > 0)
+    e = cudaMemcpy2DAsync(h_arcs, pitch, d_arcs, pitch, 4 * (size_t)mx_a, n, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && olabels && arcs_cap > 0 && mx_o > 0)
+    e = cudaMemcpy2DAsync(h_ol, pitch, d_ol, pitch, 4 * (size_t)mx_o, n, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "path D2H");
+  if (arcs && arcs_cap > 0 && mx_a > 0)
+    for (int i = 0; i < n; i++) memcpy(arcs + (size_t)i * cap, h_arcs + (size_t)i * cap, 4 * (size_t)mx_a);
+  if (olabels && arcs_cap > 0 && mx_o > 0)
+    for (int i = 0; i < n; i++) memcpy(olabels + (size_t)i * cap, h_ol + (size_t)i * cap, 4 * (size_t)mx_o);
   wfst_status first = WFST_OK;
   for (int i = 0; i < n; i++) {
-    memcpy(&cost[i], &head[n + i], 4);
-    reached_final[i] = head[2 * n + i];
-    n_arcs[i] = head[3 * n + i];
-    if (n_olabels) n_olabels[i] = head[4 * n + i];
-    wfst_status s = (wfst_status)head[5 * n + i];
+    memcpy(&cost[i], &h[n + i], 4);
+    reached_final[i] = h[2 * n + i];
+    n_arcs[i] = h[3 * n + i];
+    if (n_olabels) n_olabels[i] = h[4 * n + i];
+    wfst_status s = (wfst_status)h[5 * n + i];
+    if (status) status[i] = s;
     if (s != WFST_OK && first == WFST_OK) {
       first = s;
-      set_error("stream " + std::to_string(ids[i]) + ": " + wfst_status_string(s));
+      set_error("stream " + std::to_string(streams ? streams[i] : i) + ": " + wfst_status_string(s));
     }
   }
   return first;
+}
+
+wfst_status wfst_get_best_paths(wfst_decoder_t d, const int32_t* streams, int32_t n, float* cost,
+                                int32_t* reached_final, int32_t* arcs, int32_t* olabels, int32_t arcs_cap,
+                                int32_t* n_arcs, int32_t* n_olabels) {
+  return wfst_get_best_paths_ex(d, streams, n, cost, reached_final, arcs, olabels, arcs_cap, n_arcs, n_olabels,
+                                nullptr);
 }
 
 wfst_status wfst_get_best_path(wfst_decoder_t d, int32_t stream, int32_t* olabels, int32_t olabels_cap,
@@ -919,7 +989,7 @@ wfst_status wfst_decoder_stats(wfst_decoder_t d, wfst_stats_t* s) {
   if (!d || !s) return fail(WFST_ERR_INVALID_ARG, "NULL argument");
   DeviceGuard dg(d->device);
   std::vector<LaneState> L(d->n_lanes);
-  cudaError_t e = cudaMemcpy(L.data(), d->d_lanes, sizeof(LaneState) * d->n_lanes, cudaMemcpyDeviceToHost);
+  cudaError_t e = d2h(d, L.data(), d->d_lanes, sizeof(LaneState) * d->n_lanes);
   if (e != cudaSuccess) return cuda_fail(e, "stats");
   memset(s, 0, sizeof *s);
   for (auto& x : L) {
@@ -933,6 +1003,7 @@ wfst_status wfst_decoder_stats(wfst_decoder_t d, wfst_stats_t* s) {
     s->alpha_frames += x.alpha_frames;
     s->records_used_max = std::max<int64_t>(s->records_used_max, x.rec_used);
     for (int k = 0; k < 12; k++) s->phase_cycles[k] += (int64_t)x.phase[k];
+    s->select_entries += (int64_t)x.sel_entries;
   }
   s->device_bytes = d->device_bytes;
   return WFST_OK;
@@ -942,14 +1013,15 @@ wfst_status wfst_decoder_reset_stats(wfst_decoder_t d) {
   if (!d) return fail(WFST_ERR_INVALID_ARG, "NULL decoder");
   DeviceGuard dg(d->device);
   std::vector<LaneState> L(d->n_lanes);
-  cudaError_t e = cudaDeviceSynchronize();
-  if (e == cudaSuccess) e = cudaMemcpy(L.data(), d->d_lanes, sizeof(LaneState) * d->n_lanes, cudaMemcpyDeviceToHost);
+  cudaError_t e = d2h(d, L.data(), d->d_lanes, sizeof(LaneState) * d->n_lanes);
   if (e != cudaSuccess) return cuda_fail(e, "stats");
   for (auto& x : L) {
     x.emit_arcs = x.eps_arcs = x.eps_relax = x.cand = x.surv = x.ovf = x.alpha_frames = x.frames_total = 0;
+    x.sel_entries = 0;
     for (int k = 0; k < 12; k++) x.phase[k] = 0;
   }
-  e = cudaMemcpy(d->d_lanes, L.data(), sizeof(LaneState) * d->n_lanes, cudaMemcpyHostToDevice);
+  e = cudaMemcpyAsync(d->d_lanes, L.data(), sizeof(LaneState) * d->n_lanes, cudaMemcpyHostToDevice, d->work_stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(d->work_stream);
   return e == cudaSuccess ? WFST_OK : cuda_fail(e, "stats");
 }
 
@@ -957,17 +1029,14 @@ wfst_status wfst_decoder_frame_stats(wfst_decoder_t d, int32_t stream, float* fs
                                      int32_t cap_frames, int32_t* n_frames) {
   if (!d || stream < 0 || stream >= d->n_lanes || !n_frames) return fail(WFST_ERR_INVALID_ARG, "bad argument");
   DeviceGuard dg(d->device);
-  cudaError_t e = cudaDeviceSynchronize();
   LaneState L;
-  if (e == cudaSuccess) e = cudaMemcpy(&L, d->d_lanes + stream, sizeof L, cudaMemcpyDeviceToHost);
+  cudaError_t e = d2h(d, &L, d->d_lanes + stream, sizeof L);
   if (e != cudaSuccess) return cuda_fail(e, "frame stats");
   int n = std::min(std::min(L.frames, d->TMAX), std::max(cap_frames, 0));
   *n_frames = std::min(L.frames, d->TMAX);
-  if (fstats && n > 0)
-    e = cudaMemcpy(fstats, d->kp.fstats + (size_t)stream * d->TMAX * 3, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost);
+  if (fstats && n > 0) e = d2h(d, fstats, d->kp.fstats + (size_t)stream * d->TMAX * 3, sizeof(float) * 3 * n);
   if (e == cudaSuccess && fcounts && n > 0)
-    e = cudaMemcpy(fcounts, d->kp.fcounts + (size_t)stream * d->TMAX * 5, sizeof(int64_t) * 5 * n,
-                   cudaMemcpyDeviceToHost);
+    e = d2h(d, fcounts, d->kp.fcounts + (size_t)stream * d->TMAX * 5, sizeof(int64_t) * 5 * n);
   return e == cudaSuccess ? WFST_OK : cuda_fail(e, "frame stats");
 }
 
@@ -976,15 +1045,13 @@ wfst_status wfst_debug_layer(wfst_decoder_t d, int32_t stream, int32_t layer, in
   if (!d || stream < 0 || stream >= d->n_lanes || !n || layer < 0) return fail(WFST_ERR_INVALID_ARG, "bad argument");
   if (layer > d->TMAX) return fail(WFST_ERR_INVALID_ARG, "layer beyond max_frames");
   DeviceGuard dg(d->device);
-  cudaError_t e = cudaDeviceSynchronize();
   LaneState L;
-  if (e == cudaSuccess) e = cudaMemcpy(&L, d->d_lanes + stream, sizeof L, cudaMemcpyDeviceToHost);
+  cudaError_t e = d2h(d, &L, d->d_lanes + stream, sizeof L);
   if (e != cudaSuccess) return cuda_fail(e, "debug layer");
   if (layer > L.frames) return fail(WFST_ERR_INVALID_ARG, "layer not decoded yet");
   if (layer < L.layer_floor || L.frames - layer > d->TMAX) return fail(WFST_ERR_INVALID_ARG, "layer reclaimed");
   int2 info;
-  e = cudaMemcpy(&info, d->kp.layer_info + (size_t)stream * (d->TMAX + 1) + layer % (d->TMAX + 1), sizeof info,
-                 cudaMemcpyDeviceToHost);
+  e = d2h(d, &info, d->kp.layer_info + (size_t)stream * (d->TMAX + 1) + layer % (d->TMAX + 1), sizeof info);
   if (e != cudaSuccess) return cuda_fail(e, "debug layer");
   *n = info.y;
   if (info.y > cap) return fail(WFST_ERR_INVALID_ARG, "capacity too small");
@@ -994,13 +1061,11 @@ wfst_status wfst_debug_layer(wfst_decoder_t d, int32_t stream, int32_t layer, in
     // the layer's records may wrap around the end of the record ring
     const int64_t r0 = (int64_t)info.x % d->R_cap, n1 = std::min<int64_t>(info.y, d->R_cap - r0);
     const size_t lb = (size_t)stream * d->R_cap;
-    e = cudaMemcpy(r.data(), d->kp.rec + lb + r0, sizeof(int2) * n1, cudaMemcpyDeviceToHost);
-    if (e == cudaSuccess && n1 < info.y)
-      e = cudaMemcpy(r.data() + n1, d->kp.rec + lb, sizeof(int2) * (info.y - n1), cudaMemcpyDeviceToHost);
-    if (e == cudaSuccess && d->kp.rec_cost)
-      e = cudaMemcpy(c.data(), d->kp.rec_cost + lb + r0, 4 * (size_t)n1, cudaMemcpyDeviceToHost);
+    e = d2h(d, r.data(), d->kp.rec + lb + r0, sizeof(int2) * n1);
+    if (e == cudaSuccess && n1 < info.y) e = d2h(d, r.data() + n1, d->kp.rec + lb, sizeof(int2) * (info.y - n1));
+    if (e == cudaSuccess && d->kp.rec_cost) e = d2h(d, c.data(), d->kp.rec_cost + lb + r0, 4 * (size_t)n1);
     if (e == cudaSuccess && d->kp.rec_cost && n1 < info.y)
-      e = cudaMemcpy(c.data() + n1, d->kp.rec_cost + lb, 4 * (size_t)(info.y - n1), cudaMemcpyDeviceToHost);
+      e = d2h(d, c.data() + n1, d->kp.rec_cost + lb, 4 * (size_t)(info.y - n1));
     if (e != cudaSuccess) return cuda_fail(e, "debug layer");
   }
   for (int i = 0; i < info.y; i++) {
@@ -1128,34 +1193,23 @@ wfst_status wfst_get_lattice(wfst_decoder_t d, int32_t stream, int32_t* seg_n, i
   return WFST_OK;
 }
 
-wfst_status wfst_get_partial_paths(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
-                                   int32_t* olabels, int32_t cap, int32_t* n_arcs, int32_t* n_olabels,
-                                   int32_t* settled_frames) {
+wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
+                                      int32_t* olabels, int32_t cap, int32_t* n_arcs, int32_t* n_olabels,
+                                      int32_t* settled_frames, int32_t* status) {
   if (!d || n < 0 || !n_arcs || !settled_frames || cap < 0) return fail(WFST_ERR_INVALID_ARG, "bad argument");
   if (n == 0) return WFST_OK;
   DeviceGuard dg(d->device);
-  std::vector<int32_t> ids(n);
   for (int i = 0; i < n; i++) {
     int32_t s = streams ? streams[i] : i;
     if (s < 0 || s >= d->n_lanes) return fail(WFST_ERR_INVALID_ARG, "stream id out of range");
     if (!d->h_initialized[s]) return fail(WFST_ERR_STATE, "stream " + std::to_string(s) + " not reset");
-    ids[i] = s;
   }
-  cudaError_t e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) return cuda_fail(e, "sync");
   const int cp = std::max(cap, 1);
-  size_t need = (size_t)n * (6 + 2 * (size_t)cp);
-  if (need > d->path_cap) {
-    cudaFree(d->d_path);
-    d->d_path = nullptr;
-    e = cudaMalloc(&d->d_path, need * 4);
-    if (e != cudaSuccess) {
-      d->path_cap = 0;
-      return cuda_fail(e, "path buffer");
-    }
-    d->path_cap = need;
-  }
+  cudaError_t e = ensure_path(d, (size_t)n * (6 + 2 * (size_t)cp));
+  if (e != cudaSuccess) return cuda_fail(e, "path buffer");
+  cudaStream_t st = d->work_stream;   // after the decoder's last decode, on its stream
   int32_t* p = d->d_path;
+  int32_t* h = d->h_path;
   PartialParams pp{};
   pp.arcs = d->kp.arcs;
   pp.olabel = d->g->d_olabel;
@@ -1184,38 +1238,53 @@ wfst_status wfst_get_partial_paths(wfst_decoder_t d, const int32_t* streams, int
     if (e != cudaSuccess) return cuda_fail(e, "partial kernel attribute");
     d->partial_smem = smem;
   }
-  e = cudaMemcpy(p, ids.data(), 4 * (size_t)n, cudaMemcpyHostToDevice);
+  for (int i = 0; i < n; i++) h[i] = streams ? streams[i] : i;
+  e = cudaMemcpyAsync(p, h, 4 * (size_t)n, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_fail(e, "ids");
-  partial_kernel<512, 2><<<n, 512, smem>>>(pp);
+  partial_kernel<512, 2><<<n, 512, smem, st>>>(pp);
   e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = mark_work(d, st);   // the kernel may move the lanes' reclaim floors
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, p, 4 * 5 * (size_t)n, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "partial kernel");
-  std::vector<int32_t> head(5 * (size_t)n);
-  e = cudaMemcpy(head.data(), p, 4 * head.size(), cudaMemcpyDeviceToHost);
   // copy only the columns some stream used (a few frames' worth of arcs per call, not cap)
   int mx_a = 0, mx_o = 0;
-  for (int i = 0; i < n && e == cudaSuccess; i++) {
-    mx_a = std::max(mx_a, std::min(head[n + i], cp));
-    mx_o = std::max(mx_o, std::min(head[2 * n + i], cp));
+  for (int i = 0; i < n; i++) {
+    mx_a = std::max(mx_a, std::min(h[n + i], cp));
+    mx_o = std::max(mx_o, std::min(h[2 * n + i], cp));
   }
   const size_t pitch = 4 * (size_t)cp;
-  if (e == cudaSuccess && arcs && cap > 0 && mx_a > 0)
-    e = cudaMemcpy2D(arcs, pitch, pp.arcs_out, pitch, 4 * (size_t)mx_a, n, cudaMemcpyDeviceToHost);
+  int32_t* h_arcs = h + 6 * n;
+  int32_t* h_ol = h_arcs + (size_t)n * cp;
+  if (arcs && cap > 0 && mx_a > 0)
+    e = cudaMemcpy2DAsync(h_arcs, pitch, pp.arcs_out, pitch, 4 * (size_t)mx_a, n, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess && olabels && cap > 0 && mx_o > 0)
-    e = cudaMemcpy2D(olabels, pitch, pp.olab_out, pitch, 4 * (size_t)mx_o, n, cudaMemcpyDeviceToHost);
+    e = cudaMemcpy2DAsync(h_ol, pitch, pp.olab_out, pitch, 4 * (size_t)mx_o, n, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "partial D2H");
+  if (arcs && cap > 0 && mx_a > 0)
+    for (int i = 0; i < n; i++) memcpy(arcs + (size_t)i * cp, h_arcs + (size_t)i * cp, 4 * (size_t)mx_a);
+  if (olabels && cap > 0 && mx_o > 0)
+    for (int i = 0; i < n; i++) memcpy(olabels + (size_t)i * cp, h_ol + (size_t)i * cp, 4 * (size_t)mx_o);
   wfst_status first = WFST_OK;
   for (int i = 0; i < n; i++) {
-    n_arcs[i] = head[n + i];
-    if (n_olabels) n_olabels[i] = head[2 * n + i];
-    settled_frames[i] = head[3 * n + i];
-    wfst_status s = (wfst_status)head[4 * n + i];
+    n_arcs[i] = h[n + i];
+    if (n_olabels) n_olabels[i] = h[2 * n + i];
+    settled_frames[i] = h[3 * n + i];
+    wfst_status s = (wfst_status)h[4 * n + i];
+    if (status) status[i] = s;
     if (s != WFST_OK && first == WFST_OK) {
       first = s;
-      set_error("stream " + std::to_string(ids[i]) + ": " + wfst_status_string(s));
+      set_error("stream " + std::to_string(streams ? streams[i] : i) + ": " + wfst_status_string(s));
     }
   }
   return first;
+}
+
+wfst_status wfst_get_partial_paths(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
+                                   int32_t* olabels, int32_t cap, int32_t* n_arcs, int32_t* n_olabels,
+                                   int32_t* settled_frames) {
+  return wfst_get_partial_paths_ex(d, streams, n, arcs, olabels, cap, n_arcs, n_olabels, settled_frames, nullptr);
 }
 
 }  // extern "C"

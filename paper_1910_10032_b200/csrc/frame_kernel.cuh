@@ -14,8 +14,6 @@
 namespace wfst_dev {
 
 typedef unsigned long long u64;
-using wfst::kArcMask;
-using wfst::kArcNone;
 
 constexpr u64 kEmpty = 0xFFFFFFFFFFFFFFFFull;
 constexpr int kNB = 1024;          // cost bins of the max-active bound
@@ -55,6 +53,8 @@ struct LaneState {
   int32_t rec_phys;     // rec_used % R_cap: the record ring slot of the next record
   int32_t rec_floor;    // records below this are reclaimed (row f2 traceback GC; 0 otherwise)
   int32_t layer_floor;  // layers below this are reclaimed (layer index ring of TMAX+1 entries)
+  int32_t pad_;
+  u64 sel_entries;      // table entries read by the max-active selection passes (entries x passes)
 };
 
 struct KParams {
@@ -107,7 +107,7 @@ struct SmemCtl {
   float beam_cut, kalpha, ref, inv_w, min_surv;
   int32_t use_alpha;
   int32_t radix_prefix, radix_k;
-  unsigned long long emit_arcs, eps_deg, eps_relax;
+  unsigned long long emit_arcs, eps_deg, eps_relax, sel_entries;
   uint32_t sclaim[kSmallClaims];   // claimed slots while the frame is small
   int32_t warp_tmp[32];
   long long warp_tmp64[32];
@@ -811,6 +811,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     }
     long long cnt = 0;
     bool first = true;
+    if (tid == 0) S.sel_entries += (unsigned long long)n_claim;   // the first pass (in-beam count)
     while (true) {
       for (int i = tid; i < kNB; i += BS) hist[i] = 0;
       __syncthreads();
@@ -864,6 +865,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         break;
       }
       shift = max(shift - 10, 0);
+      if (tid == 0) S.sel_entries += (unsigned long long)n_claim;   // one more radix pass
     }
     for (int i = tid; i < kNB; i += BS) hist[i] = 0;
     __syncthreads();
@@ -879,6 +881,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     const float best = float_of_ord(S.best_ord);
     const float inv = __fdiv_rn((float)kNB, p.beam), wd = __fdiv_rn(p.beam, (float)kNB);
     for (int i = tid; i < kNB; i += BS) hist[i] = 0;
+    if (tid == 0) S.sel_entries += (unsigned long long)min(S.n_claim, p.FCAP);
     __syncthreads();
     long long cnt = 0;
     scan_entries<4>([&](int, u64 v) {
@@ -1132,6 +1135,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       S.emit_arcs = 0;
       S.eps_relax = 0;
       S.eps_deg = 0;
+      S.sel_entries = 0;
       S.n_in = -1;
       const float half = isinf(p.beam) ? 32.0f : 0.5f * p.beam;
       S.ref = S.L.front_best - half;
@@ -1168,6 +1172,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         L.eps_relax += S.eps_relax;
         L.cand += S.n_claim;
         L.surv += n_surv;
+        L.sel_entries += S.sel_entries;
         L.ovf += S.n_ovf;
         if (emitting) {
           L.emit_arcs += S.emit_arcs;

@@ -103,7 +103,7 @@ wfst_status build_graph(int32_t Q, int32_t start, int64_t E, const int32_t* src,
   *out = nullptr;
   if (Q <= 0) return fail(WFST_ERR_GRAPH_INVALID, "graph has no states");
   if (start < 0 || start >= Q) return fail(WFST_ERR_GRAPH_INVALID, "start state out of range");
-  if (E < 0 || E > kMaxArcs) return fail(WFST_ERR_GRAPH_INVALID, "arc count out of range (max 2^28-1)");
+  if (E < 0 || E > kMaxArcs) return fail(WFST_ERR_GRAPH_INVALID, "arc count out of range (max 2^31-1)");
   if (E > 0 && (!src || !dst || !ilabel || !olabel || !weight))
     return fail(WFST_ERR_INVALID_ARG, "NULL arc array");
   if (!final_cost) return fail(WFST_ERR_INVALID_ARG, "NULL final_cost");
@@ -396,6 +396,6 @@ const char* wfst_status_string(wfst_status s) {
   return "UNKNOWN";
 }
 
-int32_t wfst_abi_version(void) { return 1; }
+int32_t wfst_abi_version(void) { return 2; }   // 2: *_ex result calls with per-stream status
 
 }  // extern "C"

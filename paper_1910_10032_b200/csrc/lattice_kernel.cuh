@@ -430,7 +430,9 @@ __global__ void __launch_bounds__(BS, 1) lattice_final_kernel(LatFinParams p) {
         }
       }
       __syncthreads();
-      if (!s_changed) break;
+      const bool more = s_changed != 0;
+      __syncthreads();   // read by every thread before thread 0 clears it for the next pass
+      if (!more) break;
     }
     for (int m = tid; m < sx.y; m += BS) {
       const int4 e = seg[sx.x + m];

@@ -142,7 +142,9 @@ __global__ void __launch_bounds__(BS, MINB) partial_kernel(PartialParams p) {
           atomicAdd(&s_nflag, 1);
         }
       __syncthreads();
-      if (!s_changed) break;
+      const bool more = s_changed != 0;
+      __syncthreads();   // read by every thread before thread 0 clears it for the next pass
+      if (!more) break;
     }
     // roots: tokens of S entered by an emitting arc or the start
     if (tid == 0) {

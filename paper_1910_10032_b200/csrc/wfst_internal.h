@@ -10,11 +10,10 @@
 
 namespace wfst {
 
-// Arc ids are stored in 28 bits inside token keys; 0x0FFFFFFF = start token.
-constexpr uint32_t kArcBits = 28;
-constexpr uint32_t kArcMask = (1u << kArcBits) - 1u;
-constexpr uint32_t kArcNone = kArcMask;
-constexpr int64_t kMaxArcs = (int64_t)kArcMask;  // ids 0 .. 2^28-2
+// Canonical arc ids are int32 everywhere on the device (winner words carry them in their low 32
+// bits with 0xFFFFFFFF = the start token, records as int32 with -1 = the start token, arc array
+// offsets as int), so a graph may have up to 2^31 - 1 arcs (ids 0 .. 2^31 - 2).
+constexpr int64_t kMaxArcs = 0x7FFFFFFFll;
 
 void set_error(const std::string& msg);
 wfst_status fail(wfst_status s, const std::string& msg);

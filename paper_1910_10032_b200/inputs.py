@@ -22,7 +22,7 @@ import math
 import numpy as np
 
 __all__ = [
-    "Wfst", "hclg_graph", "c1_graph", "random_tiny_graph", "planted_walks",
+    "Wfst", "hclg_graph", "hclg_graph_eps", "c1_graph", "random_tiny_graph", "planted_walks",
     "loglikes", "loglikes_stream", "write_text", "read_text", "PRESETS", "CONFIGS",
 ]
 
@@ -159,6 +159,73 @@ def hclg_graph(n_states: int, degree: float, n_pdfs: int, seed: int,
                cat(w1, w2, w3, w4, w5), final)
 
 
+def hclg_graph_eps(n_states: int, degree: float, n_pdfs: int, seed: int, hub_fanout: int = 20000,
+                   levels: int = 5, permute_states: bool = True) -> Wfst:
+    """Epsilon-general, id-scattered variant of hclg_graph (the paper's hard case: "chains of
+    non-emitting arcs", and their long tail).  Starting from hclg_graph:
+
+    * back-off chains of `levels` epsilon arcs: LM-history states are split into levels
+      0..levels-1 (most at the top); a state of level l > 0 backs off to a random state of level
+      l-1 (U(0.2, 0.8)), level 0 backs off to the unigram hub -- chains of length `levels`;
+    * skip arcs: every 4th history state also has a direct epsilon arc to the hub, heavier than
+      its chain (sum of U(0.2, 0.8) per level + U(1, 3)), so the closure first reaches the hub
+      expensively and later improves it through the chain (re-relaxation);
+    * backward arcs and cycles: every 8th history state h gets an epsilon arc back from its
+      back-off target b (b -> h, U(0.5, 2)): positive-weight 2-cycles h -> b -> h;
+    * with permute_states, state ids are a random permutation (start included), so epsilon arcs
+      go to lower and higher ids alike and graph reads have no id locality.
+    All epsilon weights are > 0, so every epsilon cycle has positive weight (accepted at load)."""
+    g = hclg_graph(n_states, degree, n_pdfs, seed, hub_fanout)
+    rng = np.random.default_rng([seed, 7331])
+    n_lm = max(6, int(round(0.08 * n_states)))
+    n_bi = max(1, n_lm // 500)
+    n_hist = n_lm - n_bi - 1
+    hub = n_lm - 1
+    keep = ~((g.ilabel == 0) & (g.src < n_hist))          # drop the history states' back-off arcs
+    src, dst, il, ol, w = (g.src[keep].astype(np.int64), g.dst[keep].astype(np.int64),
+                           g.ilabel[keep].astype(np.int64), g.olabel[keep].astype(np.int64),
+                           g.weight[keep].astype(np.float64))
+    # levels: level l holds a share proportional to 2^l of the history states (top level largest)
+    share = 2.0 ** np.arange(levels)
+    bounds = np.concatenate([[0], np.round(np.cumsum(share) / share.sum() * n_hist).astype(np.int64)])
+    lvl = np.zeros(n_hist, np.int64)
+    for l in range(levels):
+        lvl[bounds[l]:bounds[l + 1]] = l
+    h = np.arange(n_hist)
+    tgt = np.full(n_hist, hub, np.int64)
+    for l in range(1, levels):
+        m = lvl == l
+        lo, hi = bounds[l - 1], bounds[l]
+        if hi > lo:
+            tgt[m] = rng.integers(lo, hi, size=int(m.sum()))
+    wb = rng.uniform(0.2, 0.8, size=n_hist)
+    add_s, add_d, add_w = [h], [tgt], [wb]
+    # skip arcs: heavier than the chain below them
+    chain_cost = np.zeros(n_hist)
+    for l in range(levels):              # chain cost to the hub, level by level
+        m = lvl == l
+        chain_cost[m] = wb[m] + (0.0 if l == 0 else chain_cost[tgt[m]])
+    sk = h[(h % 4 == 3) & (lvl > 0)]
+    add_s.append(sk); add_d.append(np.full(sk.size, hub)); add_w.append(chain_cost[sk] + rng.uniform(1.0, 3.0, sk.size))
+    # backward arcs: positive 2-cycles h -> tgt(h) -> h
+    bk = h[(h % 8 == 5) & (tgt != hub)]
+    add_s.append(tgt[bk]); add_d.append(bk); add_w.append(rng.uniform(0.5, 2.0, bk.size))
+    es, ed, ew = np.concatenate(add_s), np.concatenate(add_d), np.concatenate(add_w)
+    src = np.concatenate([src, es]); dst = np.concatenate([dst, ed]); w = np.concatenate([w, ew])
+    il = np.concatenate([il, np.zeros(es.size, np.int64)]); ol = np.concatenate([ol, np.zeros(es.size, np.int64)])
+    final = g.final.astype(np.float64)
+    start = g.start
+    if permute_states:
+        perm = rng.permutation(n_states)          # old id -> new id
+        src, dst = perm[src], perm[dst]
+        nf = np.empty_like(final)
+        nf[perm] = final
+        final, start = nf, int(perm[start])
+        order = rng.permutation(src.size)         # and a scrambled input arc order
+        src, dst, il, ol, w = src[order], dst[order], il[order], ol[order], w[order]
+    return _mk(n_states, start, src, dst, il, ol, w, final)
+
+
 # --------------------------------------------------------------------------
 # C1: tiny hand-built graph (BASELINE.json configs[0]; SURVEY §8.5 C1 row)
 # --------------------------------------------------------------------------
@@ -211,14 +278,18 @@ def c1_graph() -> Wfst:
 
 
 def random_tiny_graph(seed: int, n_states: int = 6, n_arcs: int = 14, n_pdfs: int = 4,
-                      eps_frac: float = 0.25, n_final: int = 2) -> Wfst:
+                      eps_frac: float = 0.25, n_final: int = 2, eps_back: bool = False) -> Wfst:
     """Random small graph for brute-force checking (C1' in SURVEY §8.5).
-    Epsilon arcs go from lower to higher ids (acyclic)."""
+    Epsilon arcs go from lower to higher ids (acyclic), or with eps_back to any other state
+    (cycles possible; every epsilon weight is >= 0.25, so every epsilon cycle is positive)."""
     rng = np.random.default_rng(seed)
     src, dst, il, ol, w = [], [], [], [], []
     for _ in range(n_arcs):
         s = int(rng.integers(0, n_states))
-        if rng.random() < eps_frac and s < n_states - 1:
+        if eps_back and rng.random() < eps_frac:
+            d = int((s + rng.integers(1, n_states)) % n_states)
+            lab = 0
+        elif not eps_back and rng.random() < eps_frac and s < n_states - 1:
             d = int(rng.integers(s + 1, n_states))
             lab = 0
         else:
@@ -226,7 +297,7 @@ def random_tiny_graph(seed: int, n_states: int = 6, n_arcs: int = 14, n_pdfs: in
             lab = int(rng.integers(1, n_pdfs + 1))
         src.append(s); dst.append(d); il.append(lab)
         ol.append(int(rng.integers(1, 9)) if rng.random() < 0.5 else 0)
-        w.append(float(rng.uniform(0.0, 2.0)))
+        w.append(float(rng.uniform(0.25 if (eps_back and lab == 0) else 0.0, 2.0)))
     final = np.full(n_states, np.inf)
     for q in rng.choice(n_states, size=n_final, replace=False):
         final[q] = float(rng.uniform(0.0, 1.5))
@@ -385,9 +456,18 @@ CONFIGS = {
     "c4": dict(graph=dict(n_states=50_000_000, degree=3.0, n_pdfs=5700), n_pdfs=5700, streams=1024,
                frames=500, beam=15.0, max_active=10_000, preset="clean", graph_seed=4, ll_seed=40004,
                chunk=50),
+    # C5: 4096 streams in total, split 4096/N over N GPUs (strong scaling, BASELINE configs[4])
     "c5": dict(graph=dict(n_states=5_000_000, degree=3.0, n_pdfs=5700), n_pdfs=5700, streams=4096,
                frames=500, beam=15.0, max_active=10_000, preset="clean", graph_seed=3, ll_seed=50005,
-               chunk=50),
+               chunk=50, scaling="strong"),
+    # C2 on the epsilon-general, id-permuted generator (SURVEY §8.5 --permute-states)
+    "c2eps": dict(graph=dict(n_states=50_000, degree=6.0, n_pdfs=2000), graph_kind="eps", n_pdfs=2000,
+                  streams=100, frames=500, beam=10.0, max_active=10_000, preset="clean", graph_seed=2,
+                  ll_seed=20002),
+    # C3 on the epsilon-general, id-permuted generator: the pessimistic-locality variant
+    "c3eps": dict(graph=dict(n_states=5_000_000, degree=3.0, n_pdfs=5700), graph_kind="eps", n_pdfs=5700,
+                  streams=512, frames=500, beam=15.0, max_active=10_000, preset="clean", graph_seed=3,
+                  ll_seed=30003),
 }
 
 
@@ -395,6 +475,8 @@ def config_graph(name: str) -> Wfst:
     c = CONFIGS[name]
     if c["graph"] == "c1":
         return c1_graph()
+    if c.get("graph_kind") == "eps":
+        return hclg_graph_eps(seed=c["graph_seed"], **c["graph"])
     return hclg_graph(seed=c["graph_seed"], **c["graph"])
 
 

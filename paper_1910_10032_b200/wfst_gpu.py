@@ -24,14 +24,16 @@ SYMBOLS = ["wfst_load_graph", "wfst_graph_from_arrays", "wfst_graph_info", "wfst
            "wfst_decode_frames_host", "wfst_decoder_sync", "wfst_decoder_status", "wfst_get_best_path",
            "wfst_get_best_paths", "wfst_decoder_stats", "wfst_decoder_reset_stats", "wfst_decoder_frame_stats",
            "wfst_debug_layer", "wfst_synth_loglikes", "wfst_last_error", "wfst_status_string",
-           "wfst_abi_version", "wfst_get_lattice", "wfst_get_partial_paths", "wfst_graph_replicate"]
+           "wfst_abi_version", "wfst_get_lattice", "wfst_get_partial_paths", "wfst_graph_replicate",
+           "wfst_get_best_paths_ex", "wfst_get_partial_paths_ex"]
 
 
 class WfstError(RuntimeError):
-    def __init__(self, code: int, msg: str):
+    def __init__(self, code: int, msg: str, result=None):
         super().__init__(f"{STATUS.get(code, code)}: {msg}")
         self.code = code
         self.status = STATUS.get(code, str(code))
+        self.result = result   # per-stream results of a batched call that failed for some streams
 
 
 class GraphInfo(C.Structure):
@@ -51,7 +53,7 @@ class DecoderOpts(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("frames", "emit_arcs", "eps_arcs", "eps_relax", "candidates", "survivors",
                                          "overflow_inserts", "alpha_frames", "device_bytes", "records_used_max")] + \
-        [("phase_cycles", C.c_int64 * 12)]
+        [("phase_cycles", C.c_int64 * 12), ("select_entries", C.c_int64)]
     PHASES = ("prefetch", "cutoff", "epsilon", "expand_warp", "expand_hub", "overhead", "drain", "map_build", "placement",
               "eps_backptr", "table_reset", "row_wait")
 
@@ -101,6 +103,8 @@ def lib():
             "wfst_abi_version": [],
             "wfst_get_lattice": [P, I32, P, I32, P, P, P, P, P, P, I64, P, P, I64, P, P, P],
             "wfst_get_partial_paths": [P, P, I32, P, P, I32, P, P, P],
+            "wfst_get_best_paths_ex": [P, P, I32, P, P, P, P, I32, P, P, P],
+            "wfst_get_partial_paths_ex": [P, P, I32, P, P, I32, P, P, P, P],
             "wfst_graph_replicate": [P, C.c_int, P],
         }
         for name, args in sig.items():
@@ -304,11 +308,14 @@ class Decoder:
         ols = np.zeros((n, cap), np.int32)
         nar = np.zeros(n, np.int32)
         nol = np.zeros(n, np.int32)
-        rc = lib().wfst_get_best_paths(self.h, _ptr(ids), n, _ptr(cost), _ptr(rf), _ptr(arcs), _ptr(ols), cap,
-                                       _ptr(nar), _ptr(nol))
-        if raise_on_error:
-            _check(rc)
-        return dict(cost=cost, reached_final=rf, arcs=arcs, n_arcs=nar, olabels=ols, n_olabels=nol, rc=rc)
+        status = np.zeros(n, np.int32)
+        rc = lib().wfst_get_best_paths_ex(self.h, _ptr(ids), n, _ptr(cost), _ptr(rf), _ptr(arcs), _ptr(ols), cap,
+                                          _ptr(nar), _ptr(nol), _ptr(status))
+        out = dict(cost=cost, reached_final=rf, arcs=arcs, n_arcs=nar, olabels=ols, n_olabels=nol, rc=rc,
+                   status=status)
+        if raise_on_error and rc != 0:
+            raise WfstError(rc, lib().wfst_last_error().decode(errors="replace"), out)
+        return out
 
     def stats(self) -> dict:
         s = Stats()
@@ -336,33 +343,39 @@ class Decoder:
         return st[:k].copy(), ar[:k].copy(), co[:k].copy()
 
 
-    def partial_paths(self, streams=None, cap: int = 512) -> dict:
+    def partial_paths(self, streams=None, cap: int = 512, raise_on_error: bool = True) -> dict:
         """Row f2: the arcs/olabels settled since the previous call, per stream
-        (wfst_get_partial_paths), and the frames the settled prefix covers.  cap grows on demand
-        (a stream that does not fit keeps its settle point, so the call is simply repeated)."""
+        (wfst_get_partial_paths_ex), the frames the settled prefix covers and each stream's status.
+        cap grows on demand (a stream that does not fit keeps its settle point, so the call is simply
+        repeated).  A stream with an error raises WfstError after the others' arcs are collected
+        (e.result holds them); raise_on_error=False returns them with status instead."""
         ids = np.arange(self.n_streams, dtype=np.int32) if streams is None else _np(streams, np.int32)
         n = ids.size
         arcs = np.empty((n, cap), np.int32)
         ols = np.empty((n, cap), np.int32)
         nar, nol, fr = np.zeros(n, np.int32), np.zeros(n, np.int32), np.zeros(n, np.int32)
-        rc = lib().wfst_get_partial_paths(self.h, _ptr(ids), n, _ptr(arcs), _ptr(ols), cap, _ptr(nar), _ptr(nol),
-                                          _ptr(fr))
-        if rc == 1 and int(nar.max(initial=0)) > cap:
-            return self._partial_merge(ids, arcs, ols, nar, nol, fr, cap)
-        _check(rc)
-        # views into this call's fresh buffers (no per-stream copies: this runs every chunk)
-        return dict(arcs=[arcs[i, :nar[i]] for i in range(n)], olabels=[ols[i, :nol[i]] for i in range(n)],
-                    settled_frames=fr)
-
-    def _partial_merge(self, ids, arcs, ols, nar, nol, fr, cap):
-        """Streams whose new arcs exceeded cap kept their settle point: fetch them again."""
-        big = nar > cap
-        out_a = [arcs[i, :nar[i]].copy() if not big[i] else None for i in range(ids.size)]
-        out_o = [ols[i, :nol[i]].copy() if not big[i] else None for i in range(ids.size)]
-        again = self.partial_paths(ids[big], cap=int(nar.max()) + 64)
-        for k, i in enumerate(np.nonzero(big)[0]):
-            out_a[i], out_o[i], fr[i] = again["arcs"][k], again["olabels"][k], again["settled_frames"][k]
-        return dict(arcs=out_a, olabels=out_o, settled_frames=fr)
+        status = np.zeros(n, np.int32)
+        rc = lib().wfst_get_partial_paths_ex(self.h, _ptr(ids), n, _ptr(arcs), _ptr(ols), cap, _ptr(nar), _ptr(nol),
+                                             _ptr(fr), _ptr(status))
+        if rc == 0:   # views into this call's fresh buffers (no per-stream copies: this runs every chunk)
+            return dict(arcs=[arcs[i, :nar[i]] for i in range(n)], olabels=[ols[i, :nol[i]] for i in range(n)],
+                        settled_frames=fr, status=status)
+        # per stream: OK streams advanced their settle point (their arcs must not be dropped);
+        # streams whose new arcs exceeded cap kept theirs and are fetched again with a larger cap
+        big = (status == 1) & (nar > cap)
+        out_a = [arcs[i, :nar[i]].copy() if status[i] == 0 else None for i in range(n)]
+        out_o = [ols[i, :nol[i]].copy() if status[i] == 0 else None for i in range(n)]
+        if big.any():
+            again = self.partial_paths(ids[big], cap=int(nar.max()) + 64, raise_on_error=False)
+            for k, i in enumerate(np.nonzero(big)[0]):
+                out_a[i], out_o[i], fr[i] = again["arcs"][k], again["olabels"][k], again["settled_frames"][k]
+                status[i] = again["status"][k]
+        out = dict(arcs=out_a, olabels=out_o, settled_frames=fr, status=status)
+        bad = np.nonzero(status != 0)[0]
+        if raise_on_error and bad.size:
+            msg = ", ".join(f"stream {int(ids[i])}: {STATUS.get(int(status[i]), int(status[i]))}" for i in bad[:8])
+            raise WfstError(int(status[bad[0]]), msg, out)
+        return out
 
     def lattice(self, stream: int, arcs_cap: int = 1 << 20, layers_cap: int = 1 << 14,
                 gamma_cap: int = 1 << 22) -> dict:

@@ -92,9 +92,12 @@ def trellis_kbest(g, ll: np.ndarray, k: int = 2):
     return out
 
 
-def enumerate_paths(g, ll: np.ndarray, max_states: int = 8, max_frames: int = 8):
+def enumerate_paths(g, ll: np.ndarray, max_states: int = 8, max_frames: int = 8, simple_eps: bool = False):
     """All complete paths as (cost_fp64, arcs, ends_final) with cost including F
-    for final end states.  Epsilon steps bounded by |Q| per frame."""
+    for final end states.  Epsilon steps bounded by |Q| per frame.  simple_eps: only paths
+    whose epsilon runs inside a frame visit no state twice -- every path when epsilon cycles
+    are absent, and it still contains every optimal path when all epsilon cycles have positive
+    weight (dropping a cycle makes a path strictly cheaper)."""
     assert g.n_states <= max_states and ll.shape[0] <= max_frames, "instance-size guard"
     ll = np.asarray(ll, dtype=np.float64)
     T = ll.shape[0]
@@ -103,23 +106,23 @@ def enumerate_paths(g, ll: np.ndarray, max_states: int = 8, max_frames: int = 8)
         out_arcs.setdefault(int(g.src[i]), []).append(i)
     res = []
 
-    def dfs(t, q, c, path, eps_steps):
+    def dfs(t, q, c, path, eps_steps, run):
         if t == T:
             F = float(g.final[q])
             res.append((c + F if math.isfinite(F) else c, list(path), math.isfinite(F)))
         for a in out_arcs.get(q, []):
             d = int(g.dst[a])
             if g.ilabel[a] == 0:
-                if eps_steps < g.n_states:
+                if eps_steps < g.n_states and not (simple_eps and d in run):
                     path.append(a)
-                    dfs(t, d, c + float(g.weight[a]), path, eps_steps + 1)
+                    dfs(t, d, c + float(g.weight[a]), path, eps_steps + 1, run | {d})
                     path.pop()
             elif t < T:
                 path.append(a)
-                dfs(t + 1, d, c + float(g.weight[a]) - ll[t, g.ilabel[a] - 1], path, 0)
+                dfs(t + 1, d, c + float(g.weight[a]) - ll[t, g.ilabel[a] - 1], path, 0, frozenset([d]))
                 path.pop()
 
-    dfs(0, g.start, 0.0, [], 0)
+    dfs(0, g.start, 0.0, [], 0, frozenset([g.start]))
     return res
 
 

@@ -38,7 +38,7 @@ def test_exports_every_declared_symbol(W):
     missing = [n for n in names if n not in exported]
     assert not missing, missing
     assert set(W.SYMBOLS) == set(names)
-    assert W.lib().wfst_abi_version() == 1
+    assert W.lib().wfst_abi_version() == 2
 
 
 def test_sass_is_sm100a(W):

@@ -66,3 +66,41 @@ def test_random_configurations(W, torch, oracle_mod, case):
         n = res["n_arcs"][b]
         assert list(res["arcs"][b, :n]) == list(r.arcs), (case, b)
         assert res["cost"][b] == r.cost32 and res["reached_final"][b] == r.reached_final, (case, b)
+
+
+@pytest.mark.parametrize("case", range(30))
+def test_random_eps_general(W, torch, oracle_mod, case):
+    """The same sweep on epsilon-general graphs ("chains of non-emitting arcs"): the
+    id-permuted back-off-chain generator (chains of 2-6, skip arcs, positive 2-cycles) and tiny
+    random graphs with epsilon arcs in both directions and epsilon cycles (infinite beam too)."""
+    rng = np.random.default_rng(5000 + case)
+    if case % 3 == 2:
+        g = I.random_tiny_graph(int(rng.integers(1 << 30)), n_states=int(rng.integers(3, 9)),
+                                n_arcs=int(rng.integers(6, 30)), eps_frac=0.4, eps_back=True)
+        P = 4
+    else:
+        P = int(rng.integers(20, 300))
+        g = I.hclg_graph_eps(int(rng.integers(2000, 12000)), float(rng.choice([3.0, 5.0])), P,
+                             seed=int(rng.integers(1 << 30)), levels=int(rng.integers(2, 7)),
+                             permute_states=bool(rng.random() < 0.8))
+    beam = float(rng.choice([5.0, 10.0, 15.0, math.inf]))
+    alpha = int(rng.choice([0, 50, 400]))
+    B, T = int(rng.integers(1, 8)), int(rng.integers(1, 30))
+    pl = I.planted_walks(g, B, T, seed=int(rng.integers(1 << 30)))
+    ll = I.loglikes(int(rng.integers(1 << 30)), range(B), T, P, pl, 1.0, float(rng.choice([0.0, 4.0])))
+    shape = [(1024, 1), (256, 2)][case % 2]
+    G = W.Graph.from_arrays(g)
+    D = W.Decoder(G, B, beam, alpha, threads=shape[0], ctas_per_sm=shape[1])
+    D.reset()
+    D.decode_frames(torch.from_numpy(ll).cuda())
+    res = D.best_paths(cap=8 * T + 64, raise_on_error=False)
+    og = oracle_mod.OracleGraph(g)
+    for b in range(B):
+        try:
+            r = og.decode(ll[:, b, :], beam, alpha)
+        except oracle_mod.OracleError as e:
+            assert res["rc"] != 0, (case, b, str(e))
+            continue
+        n = res["n_arcs"][b]
+        assert list(res["arcs"][b, :n]) == list(r.arcs), (case, b)
+        assert res["cost"][b] == r.cost32 and res["reached_final"][b] == r.reached_final, (case, b)

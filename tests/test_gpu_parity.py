@@ -241,21 +241,79 @@ def test_host_input_path_and_determinism(W, torch, oracle_mod):
         assert np.array_equal(a["arcs"][k, :n], b["arcs"][k, :n]) and np.array_equal(b["arcs"][k, :n], c["arcs"][k, :n])
 
 
+def _all_streams_vs_oracle(og, gen_ll, streams, beam, alpha, res, lane_of=None, batch=48):
+    """Every stream of a full-size run against the oracle: host log-likelihoods regenerated by
+    inputs.py (never copied from the device) in batches, decoded by the oracle's threaded batch
+    driver on all host cores, compared element by element (path, olabel-bearing arcs, flag, cost
+    bits)."""
+    import concurrent.futures as cf
+    import os
+    cores = os.cpu_count() or 1
+    streams = list(streams)
+    cap = res["arcs"].shape[1]
+    n = 0
+    for k in range(0, len(streams), batch):
+        ids = streams[k:k + batch]
+        with cf.ThreadPoolExecutor(cores) as ex:
+            rows = list(ex.map(gen_ll, ids))
+        ll = np.ascontiguousarray(np.stack(rows, axis=1))
+        cost, reached, rc, _, arcs, n_arcs = og.decode_batch(ll, beam, alpha, cores, arcs_cap=cap)
+        for j, b in enumerate(ids):
+            lane = b if lane_of is None else lane_of(b)
+            assert rc[j] == 0, (b, rc[j])
+            m = res["n_arcs"][lane]
+            assert m == n_arcs[j] and np.array_equal(res["arcs"][lane, :m], arcs[j, :m]), b
+            assert res["reached_final"][lane] == reached[j], b
+            assert res["cost"][lane].view(np.uint32) == cost[j].view(np.uint32), b
+            n += 1
+    return n
+
+
 @pytest.mark.slow
-def test_c3_full_size_sampled(W, torch, oracle_mod):
-    """C3 at full size in bench.py's launch configuration (512 streams x 500 frames, device
-    generated log-likelihoods); the oracle checks a sample of streams one by one."""
+@pytest.mark.parametrize("preset", ["clean", "other"])
+def test_c3_full_size_all_streams(W, torch, oracle_mod, preset):
+    """C3 (the bench workload) at full size in bench.py's launch configuration: 512 streams x
+    500 frames, 5M-state graph, beam 15, max-active 10k, device-generated log-likelihoods --
+    EVERY stream against the oracle, for the clean preset and the alpha-saturated "other"."""
     import bench
-    res, ctx = bench.run_gpu_once("c3", "clean", with_paths=True)
+    res, ctx = bench.run_gpu_once("c3", preset, with_paths=True)
+    assert res["rc"] == 0
     og = oracle_mod.OracleGraph(ctx["graph"])
     c = I.CONFIGS["c3"]
-    for b in (0, 1, 255, 511):
-        ll = I.loglikes_stream(c["ll_seed"], b, c["frames"], c["n_pdfs"], ctx["planted"][:, b], **I.preset("clean"))
-        r = og.decode(ll, c["beam"], c["max_active"])
-        n = res["n_arcs"][b]
-        assert res["reached_final"][b] == r.reached_final
-        assert list(res["arcs"][b, :n]) == list(r.arcs)
-        assert res["cost"][b] == r.cost32
+    gen = lambda b: I.loglikes_stream(c["ll_seed"], b, c["frames"], c["n_pdfs"], ctx["planted"][:, b],
+                                      **I.preset(preset))
+    assert _all_streams_vs_oracle(og, gen, range(c["streams"]), c["beam"], c["max_active"], res) == 512
+
+
+def test_eps_general_permuted_c2_all_streams(W, torch, oracle_mod):
+    """C2's shape (50k states, degree 6, 2k pdfs, 100 streams x 500 frames, beam 10, max-active
+    10k) on the epsilon-general generator: random state ids, back-off chains of 5 epsilon arcs,
+    heavier skip arcs (re-relaxation), positive epsilon 2-cycles -- every stream, plus the
+    survivor sets of a few layers on the alpha-saturated preset."""
+    c = I.CONFIGS["c2"]
+    g = I.hclg_graph_eps(50_000, 6.0, 2000, seed=2)
+    T, B, P = c["frames"], c["streams"], c["n_pdfs"]
+    pl = I.planted_walks(g, B, T, seed=c["ll_seed"])
+    og = oracle_mod.OracleGraph(g)
+    G = W.Graph.from_arrays(g)
+    ll = I.loglikes(c["ll_seed"], range(B), T, P, pl, **I.preset(c["preset"]))
+    D, res = _gpu_run(W, torch, g, ll, c["beam"], c["max_active"], G=G)
+    assert res["rc"] == 0
+    gen = lambda b: np.ascontiguousarray(ll[:, b, :])
+    assert _all_streams_vs_oracle(og, gen, range(B), c["beam"], c["max_active"], res) == B
+    st = D.stats()
+    assert st["eps_relax"] > st["eps_arcs"] > 0      # epsilon work happened (incl. re-relaxations)
+    llo = I.loglikes(c["ll_seed"] + 1, range(4), 40, P, pl[:40, :4], **I.preset("other"))
+    D, res = _gpu_run(W, torch, g, llo, c["beam"], 600, G=G, debug_costs=1)
+    for b in range(4):
+        r = og.decode(llo[:, b, :], c["beam"], 600, survivors=True)
+        _compare(og, llo, c["beam"], 600, res, b)
+        for k in (0, 1, 13, 40):
+            st_, ar, co = D.debug_layer(b, k)
+            o = np.argsort(st_)
+            ost, oar, oco = r.layers[k]
+            assert np.array_equal(st_[o], ost) and np.array_equal(ar[o], oar)
+            assert np.array_equal(co[o].view(np.uint32), oco.view(np.uint32))
 
 
 @pytest.mark.parametrize("threads,ctas", [(256, 1), (256, 2), (512, 2), (256, 3), (256, 4), (1024, 1)])
@@ -373,6 +431,9 @@ def test_c5_online_chunks_full_size(W, torch, oracle_mod):
         n = res["n_arcs"][b]
         assert list(res["arcs"][b, :n]) == list(r.arcs) and res["cost"][b] == r.cost32
         assert acc[b] == list(r.arcs[:len(acc[b])]) and len(acc[b]) > 100
+    # final paths of 512 of the 4096 streams (every 8th), all against the oracle
+    gen = lambda b: I.loglikes_stream(c["ll_seed"], b, T, P, wl["planted"][:, b], **wl["preset"])
+    assert _all_streams_vs_oracle(og, gen, range(0, B, 8), wl["beam"], wl["alpha"], res) == 512
 
 
 def test_graph_replicate(W, torch, oracle_mod):

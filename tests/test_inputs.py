@@ -102,3 +102,22 @@ def test_text_roundtrip(tmp_path):
     h = I.read_text(str(p))
     assert h.n_states == g.n_states and np.array_equal(h.src, g.src) and np.array_equal(h.weight, g.weight)
     assert np.array_equal(h.final, g.final)
+
+
+def test_eps_general_generator_shape():
+    """hclg_graph_eps: back-off chains of `levels` epsilon arcs, skip arcs, positive epsilon
+    2-cycles, epsilon arcs to lower ids, scattered state ids, every epsilon weight > 0."""
+    g = I.hclg_graph_eps(20000, 5.0, 400, seed=3, levels=5)
+    e = g.ilabel == 0
+    assert np.all(g.weight[e] > 0)
+    assert np.any(g.dst[e] < g.src[e]) and np.any(g.dst[e] > g.src[e])
+    pairs = set(zip(g.src[e].tolist(), g.dst[e].tolist()))
+    assert sum((d, s) in pairs for s, d in pairs) >= 20          # 2-cycles
+    # longest epsilon chain without repeating a state (DFS over the epsilon subgraph, from sources)
+    out = {}
+    for s, d in zip(g.src[e].tolist(), g.dst[e].tolist()):
+        out.setdefault(s, []).append(d)
+    def depth(q, seen):
+        return max((1 + depth(d, seen | {d}) for d in out.get(q, []) if d not in seen), default=0)
+    assert max(depth(q, {q}) for q in list(out)[:300]) >= 4
+    assert g.start != 0 or g.n_states < 2   # ids permuted (start no longer state 0)

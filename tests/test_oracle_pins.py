@@ -312,3 +312,55 @@ def test_batch_driver_matches_single(oracle_mod):
         r = og.decode(ll[:, b, :], 10.0, 200)
         assert rc[b] == 0 and cost[b] == r.cost32 and list(arcs[b, :n_arcs[b]]) == list(r.arcs)
         assert cnt[b] == int(r.frame_counts[:, 3].sum() + r.frame_counts[:, 4].sum())
+
+
+def test_eps_general_infinite_beam_equals_bruteforce(oracle_mod):
+    """Epsilon arcs in both directions with positive-weight epsilon cycles (inputs
+    random_tiny_graph(eps_back=True)): with beam = +inf the oracle's cost equals the exhaustive
+    minimum over complete paths (DFS enumeration, fp64), and its path when the best is unique."""
+    n_checked = n_path = n_cyc = 0
+    for seed in range(200):
+        g = I.random_tiny_graph(seed, n_states=5, n_arcs=12, eps_frac=0.35, eps_back=True)
+        e = g.ilabel == 0
+        n_cyc += int(np.any(g.dst[e] < g.src[e]))
+        rng = np.random.default_rng(seed + 11)
+        T = int(rng.integers(1, 5))
+        ll = rng.uniform(-3, 0, (T, 4)).astype(np.float32)
+        paths = BF.enumerate_paths(g, ll, simple_eps=True)
+        og = oracle_mod.OracleGraph(g)
+        try:
+            r = og.decode(ll, INF, 0)
+        except oracle_mod.OracleError as ex:
+            assert ex.rc == 7 and not paths, seed
+            continue
+        pool, fin = BF.best_of_enumeration(paths)
+        assert bool(r.reached_final) == fin, seed
+        assert abs(r.cost - pool[0][0]) <= 1e-4 * max(1.0, abs(pool[0][0])), seed
+        n_checked += 1
+        second = next((p[0] for p in pool[1:] if p[1] != pool[0][1]), INF)
+        if second - pool[0][0] > 1e-4:
+            canon = BF.canonical_order(g)
+            assert [int(canon[a]) for a in r.arcs] == pool[0][1], seed
+            n_path += 1
+    assert n_checked > 150 and n_path > 100 and n_cyc > 100
+
+
+def test_eps_general_order_invariance(oracle_mod):
+    """R7 (least fixed point, any relaxation order): on the epsilon-general, id-permuted
+    generator (back-off chains of 5, skip arcs, positive 2-cycles) a permutation of the input arc
+    order -- which changes the canonical ids and hence the closure's visiting order -- leaves the
+    decoded path (as input arcs) and its cost unchanged at finite beam and max-active."""
+    g = I.hclg_graph_eps(6000, 6.0, 300, seed=12)
+    perm = np.random.default_rng(1).permutation(g.n_arcs)
+    h = I._mk(g.n_states, g.start, g.src[perm], g.dst[perm], g.ilabel[perm], g.olabel[perm], g.weight[perm], g.final)
+    og, oh = oracle_mod.OracleGraph(g), oracle_mod.OracleGraph(h)
+    cg, ch = BF.canonical_order(g), BF.canonical_order(h)
+    n_eps = 0
+    for s in range(4):
+        ll = _stream_ll(g, 51, s, 30, 300, "clean")
+        a, b = og.decode(ll, 10.0, 150), oh.decode(ll, 10.0, 150)
+        pa = [int(cg[x]) for x in a.arcs]
+        assert pa == [int(perm[ch[x]]) for x in b.arcs]
+        assert a.cost32 == b.cost32
+        n_eps += sum(int(g.ilabel[x] == 0) for x in pa)
+    assert n_eps > 0
