@@ -490,8 +490,11 @@ def gpu_arm(args):
                      "kernel_ms": round(kmean, 3), "kernel_share_of_step": round(kmean / (ms_max / args.steps), 3),
                      "peak_source": peak_src},
         "counters_per_step": {k: v / args.steps for k, v in st.items()
-                              if k not in ("device_bytes", "records_used_max", "phase_cycles")},
+                              if k not in ("device_bytes", "records_used_max", "phase_cycles", "phase_cycles_alpha")},
         "phase_share": {k: round(v / max(1, sum(st["phase_cycles"].values())), 4) for k, v in st["phase_cycles"].items()},
+        # the same cycles restricted to frames where max-active bound, as a share of ALL cycles
+        "phase_share_alpha_frames": {k: round(v / max(1, sum(st["phase_cycles"].values())), 4)
+                                     for k, v in st["phase_cycles_alpha"].items()},
         "memory": {"graph_device_bytes": ginfo.device_bytes, "graph_eq1_bytes": ginfo.eq1_bytes,
                    "decoder_device_bytes": st["device_bytes"],
                    "records_used_max_per_stream": st["records_used_max"],

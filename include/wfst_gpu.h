@@ -126,6 +126,7 @@ typedef struct {
                                 9 epsilon back-pointers, 10 table reset, 11 row wait            */
   int64_t select_entries;    /* token-table entries read by the max-active selection, summed over
                                 passes (SURVEY §8.5's passes x n_uniq term of the byte model)     */
+  int64_t phase_cycles_alpha[12]; /* phase_cycles restricted to frames where max-active bound      */
 } wfst_stats_t;
 
 /* ---- graph (row a0 of SURVEY §8) ------------------------------------------------ */

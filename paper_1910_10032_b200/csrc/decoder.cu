@@ -302,6 +302,8 @@ cudaError_t ensure_path(wfst_decoder_t d, size_t need) {
   d->h_path = nullptr;
   d->path_cap = 0;
   if (e == cudaSuccess) e = cudaMalloc(&d->d_path, need * 4);
+  // the kernels write each row's used columns only; the D2H copies whole column ranges
+  if (e == cudaSuccess) e = cudaMemset(d->d_path, 0, need * 4);
   if (e == cudaSuccess) e = cudaMallocHost(&d->h_path, need * 4);
   if (e == cudaSuccess) d->path_cap = need;
   return e;
@@ -618,6 +620,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     if (e == cudaSuccess) e = cudaMalloc(&d->d_lat_q, 4);
     if (e == cudaSuccess) e = cudaMalloc(&d->d_lat_lane, 4);
     if (e == cudaSuccess) e = cudaMalloc(&d->d_lat_out, 16);
+    if (e == cudaSuccess) e = cudaMemset(d->d_lat_out, 0, 16);   // {best, reached, status, unused}
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_lat, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMemset(lp.seg_cursor, 0, L * 8);
     if (e == cudaSuccess) e = cudaMemset(lp.lat_status, 0, L * 4);
@@ -1003,6 +1006,7 @@ wfst_status wfst_decoder_stats(wfst_decoder_t d, wfst_stats_t* s) {
     s->alpha_frames += x.alpha_frames;
     s->records_used_max = std::max<int64_t>(s->records_used_max, x.rec_used);
     for (int k = 0; k < 12; k++) s->phase_cycles[k] += (int64_t)x.phase[k];
+    for (int k = 0; k < 12; k++) s->phase_cycles_alpha[k] += (int64_t)x.phase_alpha[k];
     s->select_entries += (int64_t)x.sel_entries;
   }
   s->device_bytes = d->device_bytes;
@@ -1018,7 +1022,7 @@ wfst_status wfst_decoder_reset_stats(wfst_decoder_t d) {
   for (auto& x : L) {
     x.emit_arcs = x.eps_arcs = x.eps_relax = x.cand = x.surv = x.ovf = x.alpha_frames = x.frames_total = 0;
     x.sel_entries = 0;
-    for (int k = 0; k < 12; k++) x.phase[k] = 0;
+    for (int k = 0; k < 12; k++) x.phase[k] = x.phase_alpha[k] = 0;
   }
   e = cudaMemcpyAsync(d->d_lanes, L.data(), sizeof(LaneState) * d->n_lanes, cudaMemcpyHostToDevice, d->work_stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(d->work_stream);

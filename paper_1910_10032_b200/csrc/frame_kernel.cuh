@@ -50,6 +50,7 @@ struct LaneState {
   float front_best;     // min cost of the current survivors
   u64 emit_arcs, eps_arcs, eps_relax, cand, surv, ovf, alpha_frames, frames_total;
   u64 phase[12];        // clock64 cycles per phase (see wfst_stats_t.phase_cycles)
+  u64 phase_alpha[12];  // the same, frames where max-active bound only
   int32_t rec_phys;     // rec_used % R_cap: the record ring slot of the next record
   int32_t rec_floor;    // records below this are reclaimed (row f2 traceback GC; 0 otherwise)
   int32_t layer_floor;  // layers below this are reclaimed (layer index ring of TMAX+1 entries)
@@ -102,6 +103,7 @@ struct SmemCtl {
   int32_t pl_base[kPlace];   // placement cursors
   int32_t n_app;             // survivors appended in the cutoff's bin
   long long t_mark;
+  u64 ph[12];                    // this frame's phase cycles (thread 0), flushed by flush_phases
   unsigned long long row_mbar;   // mbarrier of the row's bulk copy
   int32_t row_parity, row_pending, row_off, t_cur;
   float beam_cut, kalpha, ref, inv_w, min_surv;
@@ -347,6 +349,7 @@ __device__ __forceinline__ long long block_sum64(long long v, long long* s_tmp) 
     long long t = lane < BS / 32 ? s_tmp[lane] : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    __syncwarp();   // lane 31 has read s_tmp[31] before lane 0 overwrites it
     if (lane == 0) s_tmp[32 - 1] = t;
   }
   __syncthreads();
@@ -1241,27 +1244,40 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     eps_closure();
     contract();
     finish_frame(-1, false);
+    flush_phases(false);
   }
 
   __device__ __forceinline__ void mark(int ph) {   // thread 0, after a barrier
     if (threadIdx.x == 0) {
       const long long t1 = clock64();
-      S.L.phase[ph] += (u64)(t1 - S.t_mark);
+      S.ph[ph] += (u64)(t1 - S.t_mark);
       S.t_mark = t1;
     }
   }
   __device__ __forceinline__ void tick(long long& t0, int ph) {
     if (threadIdx.x == 0) {
       const long long t1 = clock64();
-      S.L.phase[ph] += (u64)(t1 - t0);
+      S.ph[ph] += (u64)(t1 - t0);
       t0 = t1;
+    }
+  }
+  // a frame's phase cycles go to the lane's totals, and to the alpha-bound totals when
+  // max-active bound in it (thread 0, after the frame's last tick)
+  __device__ __forceinline__ void flush_phases(bool alpha_frame) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < 12; k++) {
+        S.L.phase[k] += S.ph[k];
+        if (alpha_frame) S.L.phase_alpha[k] += S.ph[k];
+        S.ph[k] = 0;
+      }
     }
   }
   // contraction sub-phases are marked inside contract(); this closes the last one
   __device__ __forceinline__ void tick_contract(long long& t0) {
     if (threadIdx.x == 0) {
       const long long t1 = clock64();
-      S.L.phase[10] += (u64)(t1 - S.t_mark);
+      S.ph[10] += (u64)(t1 - S.t_mark);
       t0 = t1;
     }
   }
@@ -1319,12 +1335,14 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
 #ifdef WFST_COUNT   // frame cycles split by frame kind: phase[7] alpha-bound frames, phase[9] others
     if (tid == 0) {
       (void)t_frame0;
-      S.L.phase[7] += S.dbgc[0] + S.dbgc[1];   // (slots reused by this instrumentation build)
-      S.L.phase[9] += S.dbgc[2] + S.dbgc[3];
+      S.ph[7] += S.dbgc[0] + S.dbgc[1];   // (slots reused by this instrumentation build)
+      S.ph[9] += S.dbgc[2] + S.dbgc[3];
     }
 #endif
+    const bool alpha_frame = S.use_alpha != 0;
     finish_frame(t, true);
     tick(t0, 5);
+    flush_phases(alpha_frame);
   }
 };
 
@@ -1341,6 +1359,7 @@ __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
   const uint32_t tab_sa = saddr(tab);
   for (int i = tid; i < p.C; i += BS) sts64(tab_sa + 8u * i, kEmpty);
   s_wbuf[tid] = -1;
+  if (tid < 12) S.ph[tid] = 0;
   if (tid == 0) {
     S.status = WFST_OK;
     S.row_parity = 0;

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(BS, MINB) partial_kernel(PartialParams p) {
       const int a = __ldcg(&rec[R((int64_t)Lk.x + i)].x);
       if (a < 0 || __ldg(&p.arcs[a].z) >= 0) {
         atomicAdd(&s_roots, 1);
-        s_root = Lk.x + i;
+        atomicMax(&s_root, Lk.x + i);   // used only when there is exactly one root
       }
     }
     __syncthreads();

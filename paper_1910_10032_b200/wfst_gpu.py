@@ -53,13 +53,14 @@ class DecoderOpts(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("frames", "emit_arcs", "eps_arcs", "eps_relax", "candidates", "survivors",
                                          "overflow_inserts", "alpha_frames", "device_bytes", "records_used_max")] + \
-        [("phase_cycles", C.c_int64 * 12), ("select_entries", C.c_int64)]
+        [("phase_cycles", C.c_int64 * 12), ("select_entries", C.c_int64), ("phase_cycles_alpha", C.c_int64 * 12)]
     PHASES = ("prefetch", "cutoff", "epsilon", "expand_warp", "expand_hub", "overhead", "drain", "map_build", "placement",
               "eps_backptr", "table_reset", "row_wait")
 
     def as_dict(self):
-        d = {n: int(getattr(self, n)) for n, _ in self._fields_ if n != "phase_cycles"}
+        d = {n: int(getattr(self, n)) for n, _ in self._fields_ if not n.startswith("phase_cycles")}
         d["phase_cycles"] = dict(zip(self.PHASES, (int(x) for x in self.phase_cycles)))
+        d["phase_cycles_alpha"] = dict(zip(self.PHASES, (int(x) for x in self.phase_cycles_alpha)))
         return d
 
 
