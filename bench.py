@@ -273,7 +273,7 @@ def run_gpu_once(cfg="c3", preset="clean", with_paths=True):
 
 def decoder_opts(args) -> dict:
     o = {}
-    for k in ("threads", "ctas_per_sm", "table_slots", "frames_per_item"):
+    for k in ("threads", "ctas_per_sm", "table_slots", "frames_per_item", "insert_order", "bin_capacity"):
         v = getattr(args, k, 0)
         if v:
             o[k] = v
@@ -592,6 +592,9 @@ def main(argv=None):
     ap.add_argument("--ctas-per-sm", dest="ctas_per_sm", type=int, default=0)
     ap.add_argument("--table-slots", dest="table_slots", type=int, default=0)
     ap.add_argument("--frames-per-item", dest="frames_per_item", type=int, default=0)
+    ap.add_argument("--insert-order", dest="insert_order", type=int, default=0,
+                    help="0 auto (bin order after alpha-bound frames), 1 arrival order, 2 always bin order")
+    ap.add_argument("--bin-capacity", dest="bin_capacity", type=int, default=0)
     ap.add_argument("--beam", type=float, default=None, help="override the config's beam (experiments)")
     ap.add_argument("--max-active", dest="max_active", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")

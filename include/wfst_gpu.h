@@ -107,6 +107,11 @@ typedef struct {
                                 arcs AFTER the settled prefix.  Exclusive with lattice.  Record
                                 numbers are int32: an utterance may write up to 2^31 records
                                 (~650k frames at 3.3k survivors), beyond that CAPACITY.            */
+  int32_t insert_order;      /* order in which a frame's candidates enter the token table (results
+                                never depend on it, R7/R9): 0 auto (default: bin order after a
+                                frame where max-active bound), 1 arrival order, 2 always bin order */
+  int32_t bin_capacity;      /* bin-ordered frames: candidates buffered per coarse cost bin and CTA
+                                (default 8192; a full bin inserts directly)                       */
 } wfst_decoder_opts_t;
 
 typedef struct {

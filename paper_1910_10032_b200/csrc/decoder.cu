@@ -200,6 +200,7 @@ struct wfst_decoder_s {
   int64_t R_cap = 0;
   int n_sm = 0, threads = 512, ctas_per_sm = 1;
   int n_scratch = 0;   // persistent CTAs (= per-CTA scratch sets)
+  int sort_mode = 1, cbuf_cap = 0;   // bin-ordered insertion (opts.insert_order, opts.bin_capacity)
   const WfstVariant* variant = nullptr;
   size_t smem_bytes = 0;
   KParams kp{};
@@ -414,6 +415,10 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   d->ctas_per_sm = d->o.ctas_per_sm > 0 ? d->o.ctas_per_sm : 1;
   d->n_scratch = d->o.max_ctas > 0 ? d->o.max_ctas : d->n_sm * d->ctas_per_sm;
   d->threads = d->o.threads > 0 ? d->o.threads : (d->ctas_per_sm == 1 ? 1024 : 256);
+  if (d->o.insert_order < 0 || d->o.insert_order > 2) {
+    delete d;
+    return fail(WFST_ERR_INVALID_ARG, "insert_order must be 0 (auto), 1 (arrival order) or 2 (bin order)");
+  }
   if (d->o.max_active_mode != 0 && d->o.max_active_mode != 1) {
     delete d;
     return fail(WFST_ERR_INVALID_ARG, "max_active_mode must be 0 (exact) or 1 (histogram)");
@@ -497,6 +502,10 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   size_t i_win = add(NS * FC * 8);
   size_t i_ovf = add(NS * (size_t)d->C_ovf * 8);
   size_t i_wl = add(NS * 2 * FC * 4);
+  // bin-ordered insertion: candidate buffers per CTA and coarse cost bin
+  d->sort_mode = d->o.insert_order == 1 ? 0 : d->o.insert_order == 2 ? 2 : 1;
+  d->cbuf_cap = d->alpha > 0 && d->sort_mode ? (d->o.bin_capacity > 0 ? d->o.bin_capacity : 8192) : 0;
+  size_t i_cbuf = d->cbuf_cap ? add(NS * (size_t)kPlace * (size_t)d->cbuf_cap * sizeof(int4)) : (size_t)-1;
   size_t i_rec = add(L * (size_t)d->R_cap * sizeof(int2));
   d->lattice = d->o.lattice != 0;
   if (d->lattice && d->o.reclaim) {
@@ -583,6 +592,9 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   kp.fstats = (float*)(base + parts[i_fst].off);
   kp.fcounts = (long long*)(base + parts[i_fcn].off);
   kp.layer_info = (int2*)(base + parts[i_linfo].off);
+  kp.cbuf = i_cbuf != (size_t)-1 ? (int4*)(base + parts[i_cbuf].off) : nullptr;
+  kp.cbuf_cap = d->cbuf_cap;
+  kp.sort_mode = d->sort_mode;
   kp.q_head = d->d_qhead;
   kp.lane_round = d->d_round;
   if (d->lattice) {

@@ -34,6 +34,7 @@ constexpr int kBig = WFST_KBIG;    // tokens with more emitting arcs are expande
 #define WFST_THSHIFT 10
 #endif
 constexpr int kThShift = WFST_THSHIFT;   // the max-active bound is refreshed every 2^kThShift claims
+constexpr int kThShiftSorted = 7;        // ... every 128 claims in bin-ordered frames
 constexpr int kBigCap = 256;
 constexpr int kStage = 32;         // per-warp staging buffer (candidates awaiting insertion)
 constexpr int kPlace = 64;         // coarse cost bins ordering the next frontier (kNB / 16 each)
@@ -54,8 +55,12 @@ struct LaneState {
   int32_t rec_phys;     // rec_used % R_cap: the record ring slot of the next record
   int32_t rec_floor;    // records below this are reclaimed (row f2 traceback GC; 0 otherwise)
   int32_t layer_floor;  // layers below this are reclaimed (layer index ring of TMAX+1 entries)
-  int32_t pad_;
+  int32_t last_alpha;   // max-active bound in the lane's previous frame (selects the insertion order)
   u64 sel_entries;      // table entries read by the max-active selection passes (entries x passes)
+  float cpa[2];         // moving average of SM cycles per emitting arc in alpha-bound frames,
+                        // arrival order [0] and bin order [1] (insert_order = auto picks the cheaper)
+  int32_t n_alpha_seen; // alpha-bound frames seen by the chooser
+  int32_t pad2_;
 };
 
 struct KParams {
@@ -88,6 +93,9 @@ struct KParams {
   float* fstats;      // [lane][TMAX][3]
   long long* fcounts; // [lane][TMAX][5]
   int2* layer_info;   // [lane][TMAX+1]   {record base, survivors}
+  int4* cbuf;         // [cta][kPlace][cbuf_cap] candidates of a bin-ordered frame, by coarse cost bin
+  int32_t cbuf_cap;   // entries per coarse bin (0: bin-ordered insertion off)
+  int32_t sort_mode;  // 0 never, 1 after a frame where max-active bound, 2 always (tests)
 };
 
 struct SmemCtl {
@@ -100,6 +108,11 @@ struct SmemCtl {
   unsigned long long dbgc[4];   // alpha-bound frames: claims above k_alpha by (0,0.5], (0.5,2], (2,5], >5
 #endif
   int32_t pl[kPlace];        // placement histogram: live entries per coarse cost bin
+  int32_t bcnt[kPlace];      // bin-ordered frames: candidates appended per coarse cost bin
+  int32_t bbase[kPlace + 1]; // bin-ordered frames: their prefix sums (drain order)
+  int32_t next_chunk;        // bin-ordered frames: drain cursor
+  int32_t sorted;            // this frame inserts its candidates in coarse-bin order
+  int32_t choose;            // the order of this frame was chosen by the auto rule
   int32_t pl_base[kPlace];   // placement cursors
   int32_t n_app;             // survivors appended in the cutoff's bin
   long long t_mark;
@@ -377,6 +390,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   u64* win;
   u64* ovf;
   uint32_t* wl0;      // epsilon worklist 0; worklist 1 follows at +FCAP
+  int4* cb;           // this CTA's coarse-bin candidate buffers (bin-ordered frames)
   int2* rec;
   float* rec_cost;
   int4* rec_si;
@@ -426,6 +440,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     win = p.win + X * FC;
     ovf = p.ovf + X * (size_t)p.C_ovf;
     wl0 = p.wl + X * 2 * FC;
+    cb = p.cbuf ? p.cbuf + X * (size_t)kPlace * (size_t)p.cbuf_cap : nullptr;
   }
   __device__ void bind(int lane) {
     const size_t L = (size_t)lane, FC = (size_t)p.FCAP;
@@ -461,12 +476,14 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     }
   }
 
-  __device__ __forceinline__ int insert(uint32_t q, u64 key, bool& claimed, bool& logit, bool& strict) {
+  // agg_claims: the caller adds the claims to the placement histogram itself (warp-aggregated)
+  __device__ __forceinline__ int insert(uint32_t q, u64 key, bool& claimed, bool& logit, bool& strict,
+                                        bool agg_claims = false) {
     uint32_t old_hi = 0xFFFFFFFFu;
     int s = insert_s(tab_sa, (uint32_t)p.NBK, q, key, claimed, logit, strict, old_hi);
     if (s < 0) s = insert_g(ovf, (uint32_t)(p.C_ovf / 4), q, key, claimed, logit, strict, old_hi);
     else {
-      pl_update(s, claimed, strict, old_hi, (uint32_t)(key >> 32));
+      pl_update(s, claimed && !agg_claims, strict && !claimed, old_hi, (uint32_t)(key >> 32));
       return s;
     }
     if (s < 0) {
@@ -474,7 +491,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       return -1;
     }
     if (claimed) atomicAdd(&S.n_ovf, 1);
-    pl_update(s, claimed, strict, old_hi, (uint32_t)(key >> 32));
+    pl_update(s, claimed && !agg_claims, strict && !claimed, old_hi, (uint32_t)(key >> 32));
     return s + p.C;
   }
 
@@ -502,10 +519,16 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         if (oi < p.C_ovf) claim[oi] = (uint32_t)slot;
         else S.status = WFST_ERR_CAPACITY;
       }
-      if (bin >= 0) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
+      if (bin >= 0 && !S.sorted) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
+    }
+    if (S.sorted) {   // bin-ordered frames: a warp's claims share few bins -- one atomic per bin
+      const int key = claimed && bin >= 0 ? bin : -1;
+      const unsigned grp = __match_any_sync(0xffffffffu, key);
+      if (key >= 0 && lane == __ffs(grp) - 1) red_add_s(hist_sa + 4u * (uint32_t)key, __popc(grp));
     }
     const int end = base + __popc(m);
-    return p.alpha > 0 && end >= p.alpha && (end >> kThShift) != (base >> kThShift);
+    const int sh = S.sorted ? kThShiftSorted : kThShift;   // bin order: claims past alpha are waste
+    return p.alpha > 0 && end >= p.alpha && (end >> sh) != (base >> sh);
   }
 
   // Candidates in bins >= theta are provably above the exact k_alpha (R6).  The histogram rule
@@ -538,8 +561,47 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     __syncwarp();
   }
 
+  // Bin-ordered frames: instead of inserting, append the first n staged
+  // candidates of this warp to their coarse cost bin's buffer (L2); drain_bins() inserts them
+  // cheapest bin first, so the exact max-active bound theta is known after ~alpha claims and
+  // whole bins above it are never inserted.  A full bin buffer inserts directly (the result
+  // never depends on the insertion order: R7, R9).  Warp-collective.
+  __device__ __forceinline__ void append(int n, float beam, uint32_t best_sa, uint32_t theta_sa) {
+    const int lane = threadIdx.x & 31;
+    int4 e = make_int4(0, 0, 0, 0);
+    bool ok = false;
+    if (lane < n) {
+      e = lds128(stage_sa + 16u * lane);   // {q, ord, arc id, bin | eps flag << 31}
+      const uint32_t o = (uint32_t)e.y;
+      const uint32_t bo = (uint32_t)lds32(best_sa);
+      ok = bo == 0xFFFFFFFFu || float_of_ord(o) < __fadd_rn(float_of_ord(bo), beam);
+      if (ok && o < bo) red_min_s32(best_sa, o);
+    }
+    const int pb = ok ? (e.w & 0x7FFFFFFF) / (kNB / kPlace) : kPlace;
+    const unsigned grp = __match_any_sync(0xffffffffu, pb);
+    const int leader = __ffs(grp) - 1;
+    int base = 0;
+    if (pb < kPlace && lane == leader) base = atom_add_s(saddr(&S.bcnt[pb]), __popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    const int idx = base + __popc(grp & ((1u << lane) - 1u));
+    const bool direct = ok && idx >= p.cbuf_cap;
+    if (ok && !direct) __stcg(cb + (size_t)pb * p.cbuf_cap + idx, e);
+    if (__any_sync(0xffffffffu, direct)) {   // bin buffer full: insert those now (rare)
+      __syncwarp();
+      const int m = __ballot_sync(0xffffffffu, direct);
+      if (direct) sts128(stage_sa + 16u * __popc(m & ((1u << lane) - 1u)), e);
+      __syncwarp();
+      insert_staged(__popc(m), beam, best_sa, theta_sa);
+    }
+  }
+
   // insert the first n staged candidates of this warp (warp-collective)
   __device__ __forceinline__ void flush(int n, float beam, uint32_t best_sa, uint32_t theta_sa) {
+    if (S.sorted) append(n, beam, best_sa, theta_sa);
+    else insert_staged(n, beam, best_sa, theta_sa);
+  }
+
+  __device__ __forceinline__ void insert_staged(int n, float beam, uint32_t best_sa, uint32_t theta_sa) {
     const int lane = threadIdx.x & 31;
     bool claimed = false, logit = false, strict = false;
     int slot = -1, bin = -1;
@@ -556,9 +618,18 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       if (ok) {
         if (o < bo) red_min_s32(best_sa, o);
         const uint32_t qf = (uint32_t)e.x | (flag << 31);   // state | has-epsilon flag
-        slot = insert(qf, ((u64)o << 32) | qf, claimed, logit, strict);
+        slot = insert(qf, ((u64)o << 32) | qf, claimed, logit, strict, true);
         if (slot >= 0 && logit) red_min_g64(win + slot, ((u64)o << 32) | (uint32_t)e.z);
         if (slot < 0) claimed = false;
+      }
+    }
+    {   // the claims' placement bins (bin / 16 == pbin of the cost), one atomic per distinct bin
+      const int key = claimed ? (bin / (kNB / kPlace)) : -1;
+      if (S.sorted) {
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        if (key >= 0 && lane == __ffs(grp) - 1) red_add_s(saddr(&S.pl[key]), __popc(grp));
+      } else if (key >= 0) {
+        red_add_s(saddr(&S.pl[key]), 1);
       }
     }
     if (add_claim(slot, claimed, flag, bin)) update_theta();
@@ -722,6 +793,48 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     }
     __syncthreads();
     mark(4);   // hub tokens done
+    if (S.sorted) {
+      drain_bins(beam, best_sa, theta_sa);
+      mark(7);   // bin-ordered insertion done
+    }
+  }
+
+  // Bin-ordered frames: insert the appended candidates cheapest coarse bin first.  The bins
+  // are concatenated (prefix sums of their counts) and warps take 32-entry chunks in that order
+  // from a shared cursor, so no barrier separates the bins; candidates in bins >= theta are
+  // provably above k_alpha (R6): the first chunk whose bin lies at or beyond theta ends the
+  // drain for every warp (later chunks lie in the same or later bins).
+  __device__ void drain_bins(float beam, uint32_t best_sa, uint32_t theta_sa) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    static_assert(kPlace == 64, "warp 0 scans two bins per lane");
+    if (tid < 32) {
+      const int c0 = min(S.bcnt[2 * lane], p.cbuf_cap), c1 = min(S.bcnt[2 * lane + 1], p.cbuf_cap);
+      const int incl = warp_incl_scan(c0 + c1);
+      S.bbase[2 * lane] = incl - c0 - c1;
+      S.bbase[2 * lane + 1] = incl - c1;
+      if (lane == 31) S.bbase[kPlace] = incl;
+    }
+    __syncthreads();
+    const int total = S.bbase[kPlace];
+    const uint32_t cur_sa = saddr(&S.next_chunk);
+    while (true) {
+      int c0 = 0;
+      if (lane == 0) c0 = atom_add_s(cur_sa, 32);
+      c0 = __shfl_sync(0xffffffffu, c0, 0);
+      if (c0 >= total) break;
+      const int i = c0 + lane;
+      int pb = 0;   // bin of entry i: the last b with bbase[b] <= i
+#pragma unroll
+      for (int step = kPlace / 2; step > 0; step >>= 1)
+        if (pb + step < kPlace && S.bbase[pb + step] <= i) pb += step;
+      const int pb0 = __shfl_sync(0xffffffffu, pb, 0);
+      if (pb0 * (kNB / kPlace) >= lds32(theta_sa)) break;
+      if (i < total) sts128(stage_sa + 16u * lane, __ldcg(cb + (size_t)pb * p.cbuf_cap + (i - S.bbase[pb])));
+      __syncwarp();
+      insert_staged(min(32, total - c0), beam, best_sa, theta_sa);
+      __syncwarp();
+    }
+    __syncthreads();
   }
 
   // Visit every live token-table entry: the on-chip table is scanned directly (strided, so a
@@ -1116,11 +1229,25 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     mark(8);   // placement done
   }
 
-  __device__ void begin_frame(float beam_cut_fixed) {
+  __device__ void begin_frame(float beam_cut_fixed, bool emitting) {
     const int tid = threadIdx.x;
     for (int i = tid; i < kNB; i += BS) hist[i] = 0;
-    if (tid < kPlace) S.pl[tid] = 0;
+    if (tid < kPlace) {
+      S.pl[tid] = 0;
+      S.bcnt[tid] = 0;
+    }
     if (tid == 0) {
+      // insertion order of this frame (results never depend on it): bin order when forced, or
+      // (auto) after an alpha-bound frame when bin order has been the cheaper one per emitting
+      // arc on this lane lately; every 8th alpha-bound frame tries the other order
+      bool sorted = false;
+      if (emitting && p.cbuf_cap > 0 && p.alpha > 0) {
+        if (p.sort_mode == 2) sorted = true;
+        else if (p.sort_mode == 1 && S.L.last_alpha)
+          sorted = (S.L.cpa[1] <= S.L.cpa[0]) != ((S.L.n_alpha_seen & 7) == 7);
+      }
+      S.sorted = sorted;
+      S.choose = emitting && p.cbuf_cap > 0 && p.alpha > 0 && p.sort_mode == 1 && S.L.last_alpha;
       S.best_ord = 0xFFFFFFFFu;
       S.theta = kNB;
       S.n_claim = 0;
@@ -1128,6 +1255,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       S.n_ovf = 0;
       S.n_big = 0;
       S.next_group = 0;
+      S.next_chunk = 0;
 #ifdef WFST_COUNT
       S.dbgc[0] = S.dbgc[1] = S.dbgc[2] = S.dbgc[3] = 0;
 #endif
@@ -1181,6 +1309,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
           L.emit_arcs += S.emit_arcs;
           L.alpha_frames += S.use_alpha;
           L.frames_total++;
+          L.last_alpha = S.use_alpha;
         }
         const size_t lane = (size_t)S.lane;
         p.layer_info[lane * (p.TMAX + 1) + layer % (p.TMAX + 1)] = make_int2(L.layer_base, n_surv);
@@ -1215,12 +1344,13 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       L.rec_phys = 0;
       L.rec_floor = 0;
       L.layer_floor = 0;
+      L.last_alpha = 0;
       L.status = WFST_OK;
       L.initialized = 1;
       L.front_best = 0.0f;
     }
     __syncthreads();
-    begin_frame(__fadd_rn(0.0f, p.beam));
+    begin_frame(__fadd_rn(0.0f, p.beam), false);
     if (tid < 32) {
       bool claimed = false, logit = false, strict = false;
       int slot = -1;
@@ -1265,11 +1395,19 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   // max-active bound in it (thread 0, after the frame's last tick)
   __device__ __forceinline__ void flush_phases(bool alpha_frame) {
     if (threadIdx.x == 0) {
+      u64 cyc = 0;
 #pragma unroll
       for (int k = 0; k < 12; k++) {
+        cyc += S.ph[k];
         S.L.phase[k] += S.ph[k];
         if (alpha_frame) S.L.phase_alpha[k] += S.ph[k];
         S.ph[k] = 0;
+      }
+      if (alpha_frame && S.choose) {   // feed the insertion-order chooser
+        const float x = (float)cyc / (float)max(1ull, S.emit_arcs);
+        float& m = S.L.cpa[S.sorted ? 1 : 0];
+        m = m == 0.0f ? x : 0.875f * m + 0.125f * x;
+        S.L.n_alpha_seen++;
       }
     }
   }
@@ -1300,7 +1438,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
 #if WFST_ROWSMEM
     if (tid == 0 && !S.row_pending) row_issue(row_ptr(t));   // first frame of a work item
 #endif
-    begin_frame(INFINITY);
+    begin_frame(INFINITY, true);
     tick(t0, 5);
 #if WFST_ROWSMEM
     row_wait();

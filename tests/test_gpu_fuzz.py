@@ -42,7 +42,7 @@ def test_random_configurations(W, torch, oracle_mod, case):
     pl = I.planted_walks(g, B, T, seed=int(rng.integers(1 << 30)))
     ll = I.loglikes(int(rng.integers(1 << 30)), range(B), T, P, pl, sigma, boost)
     shape = [(1024, 1), (512, 1), (256, 2)][int(rng.integers(3))] if not hist else (1024, 1)
-    opts = dict(threads=shape[0], ctas_per_sm=shape[1])
+    opts = dict(threads=shape[0], ctas_per_sm=shape[1], insert_order=int(rng.integers(3)))
     if hist:
         opts["max_active_mode"] = 1
     G = W.Graph.from_arrays(g)
@@ -90,7 +90,7 @@ def test_random_eps_general(W, torch, oracle_mod, case):
     ll = I.loglikes(int(rng.integers(1 << 30)), range(B), T, P, pl, 1.0, float(rng.choice([0.0, 4.0])))
     shape = [(1024, 1), (256, 2)][case % 2]
     G = W.Graph.from_arrays(g)
-    D = W.Decoder(G, B, beam, alpha, threads=shape[0], ctas_per_sm=shape[1])
+    D = W.Decoder(G, B, beam, alpha, threads=shape[0], ctas_per_sm=shape[1], insert_order=2 - case % 3)
     D.reset()
     D.decode_frames(torch.from_numpy(ll).cuda())
     res = D.best_paths(cap=8 * T + 64, raise_on_error=False)
