@@ -273,12 +273,15 @@ def run_gpu_once(cfg="c3", preset="clean", with_paths=True):
 
 def decoder_opts(args) -> dict:
     o = {}
-    for k in ("threads", "ctas_per_sm", "table_slots", "frames_per_item", "insert_order", "bin_capacity"):
+    for k in ("threads", "ctas_per_sm", "table_slots", "frames_per_item", "insert_order", "bin_capacity",
+              "records_per_stream", "max_frames"):
         v = getattr(args, k, 0)
         if v:
             o[k] = v
     if getattr(args, "hist", False):   # row f4: the paper's histogram max-active instead of the exact one
         o["max_active_mode"] = 1
+    if getattr(args, "reclaim", False):   # row f2 traceback GC: records below the settle point are reused
+        o["reclaim"] = 1
     if getattr(args, "lattice", None) is not None:   # row f1: segments built inside every decode call
         o["lattice"] = 1
         o["lattice_beam"] = args.lattice
@@ -403,8 +406,10 @@ def gpu_arm(args):
     gather = None
     if rank == 0:
         assert sorted(gathered) == list(range(total_streams)), "streams missing from the gather"
+        # (with --reclaim the timed steps' paths are the tails after the settled prefixes: the
+        # re-decode, which fetches no partial results, is compared only without --partial)
         n_chk, n_bad = cross_check(W, torch, args.config, args.preset, wl["graph"], G, gathered, world, dev, args) \
-            if world > 1 else (0, 0)
+            if world > 1 and not args.partial else (0, 0)
         assert n_bad == 0, f"{n_bad} of {n_chk} streams decoded differently on rank 0"
         gather = {"streams": len(gathered), "rechecked_on_rank0": n_chk, "mismatches": n_bad,
                   "digest": "%08x" % zlib.crc32(json.dumps([gathered[k] for k in sorted(gathered)]).encode())}
@@ -491,10 +496,13 @@ def gpu_arm(args):
                      "peak_source": peak_src},
         "counters_per_step": {k: v / args.steps for k, v in st.items()
                               if k not in ("device_bytes", "records_used_max", "phase_cycles", "phase_cycles_alpha")},
-        "phase_share": {k: round(v / max(1, sum(st["phase_cycles"].values())), 4) for k, v in st["phase_cycles"].items()},
+        # per-phase SM cycles (clock64 marks of thread 0; -DWFST_PHASES=0 builds have none)
+        "phase_share": {k: round(v / max(1, sum(st["phase_cycles"].values())), 4) for k, v in st["phase_cycles"].items()}
+        if sum(st["phase_cycles"].values()) else None,
         # the same cycles restricted to frames where max-active bound, as a share of ALL cycles
         "phase_share_alpha_frames": {k: round(v / max(1, sum(st["phase_cycles"].values())), 4)
-                                     for k, v in st["phase_cycles_alpha"].items()},
+                                     for k, v in st["phase_cycles_alpha"].items()}
+        if sum(st["phase_cycles"].values()) else None,
         "memory": {"graph_device_bytes": ginfo.device_bytes, "graph_eq1_bytes": ginfo.eq1_bytes,
                    "decoder_device_bytes": st["device_bytes"],
                    "records_used_max_per_stream": st["records_used_max"],
@@ -595,6 +603,10 @@ def main(argv=None):
     ap.add_argument("--insert-order", dest="insert_order", type=int, default=0,
                     help="0 auto (bin order after alpha-bound frames), 1 arrival order, 2 always bin order")
     ap.add_argument("--bin-capacity", dest="bin_capacity", type=int, default=0)
+    ap.add_argument("--reclaim", action="store_true",
+                    help="traceback GC (row f2): with --partial, records below each stream's settle point are reused")
+    ap.add_argument("--records-per-stream", dest="records_per_stream", type=int, default=0)
+    ap.add_argument("--max-frames", dest="max_frames", type=int, default=0)
     ap.add_argument("--beam", type=float, default=None, help="override the config's beam (experiments)")
     ap.add_argument("--max-active", dest="max_active", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
@@ -602,6 +614,8 @@ def main(argv=None):
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
+    if args.reclaim and not args.partial:
+        ap.error("--reclaim needs --partial (records are released by the settled partial results)")
     if args.impl == "reference":
         return reference_arm(args)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

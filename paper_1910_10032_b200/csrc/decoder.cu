@@ -452,7 +452,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   d->C = C;
   // overflow table: room for every distinct candidate a frame can hold beyond the on-chip table
   int Co = d->o.overflow_slots > 0 ? d->o.overflow_slots : std::max(std::max(C, 32768), 4 * d->alpha);
-  d->C_ovf = std::max(64, (Co + 3) / 4 * 4);
+  d->C_ovf = std::max(64, (Co + 7) / 8 * 8);   // FCAP % 8 == 0: frontier buffers are 128-B aligned
   d->FCAP = d->C + d->C_ovf;
   d->TMAX = d->o.max_frames > 0 ? d->o.max_frames : 4096;
   int64_t per_frame = d->alpha > 0 ? std::min<int64_t>((int64_t)d->alpha * 5 / 4 + 1024, d->FCAP) : d->FCAP;
@@ -505,6 +505,7 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   // bin-ordered insertion: candidate buffers per CTA and coarse cost bin
   d->sort_mode = d->o.insert_order == 1 ? 0 : d->o.insert_order == 2 ? 2 : 1;
   d->cbuf_cap = d->alpha > 0 && d->sort_mode ? (d->o.bin_capacity > 0 ? d->o.bin_capacity : 8192) : 0;
+  d->cbuf_cap = (d->cbuf_cap + 7) / 8 * 8;   // 128-B aligned bins (discarded line by line)
   size_t i_cbuf = d->cbuf_cap ? add(NS * (size_t)kPlace * (size_t)d->cbuf_cap * sizeof(int4)) : (size_t)-1;
   size_t i_rec = add(L * (size_t)d->R_cap * sizeof(int2));
   d->lattice = d->o.lattice != 0;

@@ -26,6 +26,9 @@ constexpr int kNB = 1024;          // cost bins of the max-active bound (DESIGN.
 constexpr int kMaxProbeS = WFST_MAXPROBE;   // buckets probed in the on-chip table before overflowing
 constexpr int kMaxProbeG = 512;    // buckets probed in the global overflow table
 constexpr int kModeFrames = 0, kModeInit = 1;
+#ifndef WFST_PHASES
+#define WFST_PHASES 1   // per-phase clock64 marks (wfst_stats_t.phase_cycles): measured free (A/B)
+#endif
 #ifndef WFST_KBIG
 #define WFST_KBIG 64
 #endif
@@ -204,6 +207,16 @@ __device__ __forceinline__ void sts32(uint32_t a, int v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ u64 ldg_volatile64(const u64* p) { return *(const volatile u64*)p; }
+// drop a dead 128-B line of per-frame scratch from L2 without writing it back to DRAM
+#ifndef WFST_DISCARD_FRONT
+#define WFST_DISCARD_FRONT 1
+#endif
+#ifndef WFST_DISCARD_BINS
+#define WFST_DISCARD_BINS 0   // measured: saves 12 GB of DRAM writes per C3 launch but costs 3.6% (A/B)
+#endif
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 __device__ __forceinline__ void red_min_g64(u64* p, u64 v) {
   asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -793,6 +806,11 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     }
     __syncthreads();
     mark(4);   // hub tokens done
+    // the consumed frontier is dead (the next contraction writes the other buffer): drop its
+    // lines from L2 so they are never written back (buffers are 128-B aligned: FCAP % 8 == 0)
+#if WFST_DISCARD_FRONT
+    for (int l = tid; l < (n_f + 7) / 8; l += BS) discard_l2(Fin + 8 * l);
+#endif
     if (S.sorted) {
       drain_bins(beam, best_sa, theta_sa);
       mark(7);   // bin-ordered insertion done
@@ -835,6 +853,13 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       __syncwarp();
     }
     __syncthreads();
+    // the bin buffers are dead: drop them from L2 without write-back (bins are 128-B aligned)
+#if WFST_DISCARD_BINS
+    for (int pb = 0; pb < kPlace; pb++) {
+      const int nl = (min(S.bcnt[pb], p.cbuf_cap) + 7) / 8;
+      for (int l = tid; l < nl; l += BS) discard_l2(cb + (size_t)pb * p.cbuf_cap + 8 * l);
+    }
+#endif
   }
 
   // Visit every live token-table entry: the on-chip table is scanned directly (strided, so a
@@ -1333,8 +1358,8 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   // R3: start token + epsilon closure with keep(c) = c < beam
   __device__ void init_lane() {
     const int tid = threadIdx.x;
+    set_mark();   // the contraction's phase marks measure from here
     if (tid == 0) {
-      S.t_mark = clock64();   // the contraction's phase marks measure from here
       LaneState& L = S.L;   // a new utterance: keep the lifetime counters
       L.n_front = 0;
       L.cur = 0;
@@ -1374,35 +1399,45 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     eps_closure();
     contract();
     finish_frame(-1, false);
-    flush_phases(false);
+    flush_phases(false, 0);
   }
 
   __device__ __forceinline__ void mark(int ph) {   // thread 0, after a barrier
+#if WFST_PHASES
     if (threadIdx.x == 0) {
       const long long t1 = clock64();
       S.ph[ph] += (u64)(t1 - S.t_mark);
       S.t_mark = t1;
     }
+#endif
   }
   __device__ __forceinline__ void tick(long long& t0, int ph) {
+#if WFST_PHASES
     if (threadIdx.x == 0) {
       const long long t1 = clock64();
       S.ph[ph] += (u64)(t1 - t0);
       t0 = t1;
     }
+#endif
+  }
+  __device__ __forceinline__ void set_mark() {
+#if WFST_PHASES
+    if (threadIdx.x == 0) S.t_mark = clock64();
+#endif
   }
   // a frame's phase cycles go to the lane's totals, and to the alpha-bound totals when
   // max-active bound in it (thread 0, after the frame's last tick)
-  __device__ __forceinline__ void flush_phases(bool alpha_frame) {
+  // cyc: the frame's SM cycles (thread 0's clock; the insertion-order chooser's measure)
+  __device__ __forceinline__ void flush_phases(bool alpha_frame, u64 cyc) {
     if (threadIdx.x == 0) {
-      u64 cyc = 0;
+#if WFST_PHASES
 #pragma unroll
       for (int k = 0; k < 12; k++) {
-        cyc += S.ph[k];
         S.L.phase[k] += S.ph[k];
         if (alpha_frame) S.L.phase_alpha[k] += S.ph[k];
         S.ph[k] = 0;
       }
+#endif
       if (alpha_frame && S.choose) {   // feed the insertion-order chooser
         const float x = (float)cyc / (float)max(1ull, S.emit_arcs);
         float& m = S.L.cpa[S.sorted ? 1 : 0];
@@ -1413,11 +1448,13 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   }
   // contraction sub-phases are marked inside contract(); this closes the last one
   __device__ __forceinline__ void tick_contract(long long& t0) {
+#if WFST_PHASES
     if (threadIdx.x == 0) {
       const long long t1 = clock64();
       S.ph[10] += (u64)(t1 - S.t_mark);
       t0 = t1;
     }
+#endif
   }
 
   __device__ const float* row_ptr(int t) const { return p.ll + ((size_t)t * p.B + S.b) * (size_t)p.P; }
@@ -1431,9 +1468,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       return;
     }
     long long t0 = clock64();
-#ifdef WFST_COUNT
     const long long t_frame0 = t0;
-#endif
     if (tid == 0) S.t_cur = t;
 #if WFST_ROWSMEM
     if (tid == 0 && !S.row_pending) row_issue(row_ptr(t));   // first frame of a work item
@@ -1444,9 +1479,11 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     row_wait();
 #endif
     tick(t0, 11);
-    if (tid == 0) S.t_mark = clock64();
+    set_mark();
     expand();
+#if WFST_PHASES
     if (tid == 0) t0 = clock64();   // expansion itself is timed by the marks inside expand()
+#endif
 #if WFST_ROWSMEM
     if (tid == 0 && t_next >= 0) row_issue(row_ptr(t_next));   // overlaps the frame's tail
 #endif
@@ -1467,12 +1504,11 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     tick(t0, 1);
     eps_closure();
     tick(t0, 2);
-    if (tid == 0) S.t_mark = clock64();
+    set_mark();
     contract();
     tick_contract(t0);
 #ifdef WFST_COUNT   // frame cycles split by frame kind: phase[7] alpha-bound frames, phase[9] others
     if (tid == 0) {
-      (void)t_frame0;
       S.ph[7] += S.dbgc[0] + S.dbgc[1];   // (slots reused by this instrumentation build)
       S.ph[9] += S.dbgc[2] + S.dbgc[3];
     }
@@ -1480,7 +1516,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     const bool alpha_frame = S.use_alpha != 0;
     finish_frame(t, true);
     tick(t0, 5);
-    flush_phases(alpha_frame);
+    flush_phases(alpha_frame, (u64)(clock64() - t_frame0));
   }
 };
 
