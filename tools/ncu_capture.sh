@@ -5,6 +5,7 @@ TAG=${1:-r02}; shift || true
 mkdir -p gpurun_out
 python -c "from paper_1910_10032_b200 import build; build.build()" || exit 1
 export WFST_NO_BUILD=1
+python -c "import bench; print(bench.kernel_source_sha())" > gpurun_out/prof_$TAG.sha
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline "$@" > gpurun_out/launches_bench_$TAG.log 2>&1
