@@ -16,7 +16,8 @@
  * Conventions
  *   - Graph arcs are (src, dst, ilabel, olabel, weight).  ilabel 0 = epsilon
  *     (non-emitting); an emitting arc reads log-likelihood column pdf =
- *     ilabel - 1 ("arcs with non-null labels").  The start state is
+ *     ilabel - 1 ("arcs with non-null labels"), or column = ilabel with
+ *     opts.ll_columns = 1 (SPEC's layout, column 0 unused).  The start state is
  *     given explicitly (text files: state 0).  final cost +INF =
  *     non-final.  Weights and costs are fp32, tropical (min, +) semiring.
  *   - Canonical arc ids: arcs stably ordered by (src, emitting first) in
@@ -112,6 +113,15 @@ typedef struct {
                                 frame where max-active bound), 1 arrival order, 2 always bin order */
   int32_t bin_capacity;      /* bin-ordered frames: candidates buffered per coarse cost bin and CTA
                                 (default 8192; a full bin inserts directly)                       */
+  int32_t ll_columns;        /* which log-likelihood column an emitting arc reads (reading R2):
+                                0 (default): pdf columns, column = ilabel - 1, requires P > max_pdf
+                                  (Kaldi-style transition -> pdf + 1 labels);
+                                1: ilabel columns: column = ilabel,
+                                  column 0 unused, requires P >= 1 + max ilabel = max_pdf + 2.
+                                The two layouts of the same scores differ by one leading column;
+                                a P that fits only layout 0 is rejected under layout 1 (PDF_RANGE)
+                                and the caller chooses the layout explicitly, so a SPEC-shaped
+                                matrix is never read one column off by default-guessing.        */
 } wfst_decoder_opts_t;
 
 typedef struct {

@@ -415,6 +415,10 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   d->ctas_per_sm = d->o.ctas_per_sm > 0 ? d->o.ctas_per_sm : 1;
   d->n_scratch = d->o.max_ctas > 0 ? d->o.max_ctas : d->n_sm * d->ctas_per_sm;
   d->threads = d->o.threads > 0 ? d->o.threads : (d->ctas_per_sm == 1 ? 1024 : 256);
+  if (d->o.ll_columns < 0 || d->o.ll_columns > 1) {
+    delete d;
+    return fail(WFST_ERR_INVALID_ARG, "opts.ll_columns must be 0 (pdf columns) or 1 (ilabel columns)");
+  }
   if (d->o.insert_order < 0 || d->o.insert_order > 2) {
     delete d;
     return fail(WFST_ERR_INVALID_ARG, "insert_order must be 0 (auto), 1 (arrival order) or 2 (bin order)");
@@ -767,7 +771,13 @@ wfst_status wfst_decode_frames(wfst_decoder_t d, const float* d_loglikes, int32_
   if (T == 0 || B == 0) return WFST_OK;
   if (!d_loglikes) return fail(WFST_ERR_INVALID_ARG, "NULL loglikes");
   if (B > d->n_lanes) return fail(WFST_ERR_INVALID_ARG, "B exceeds n_streams");
-  if (P <= d->g->max_pdf) return fail(WFST_ERR_PDF_RANGE, "P=" + std::to_string(P) + " <= max pdf " + std::to_string(d->g->max_pdf));
+  // ll_columns = 1 (SPEC layout): column ilabel = column pdf + 1, so the rows are read from one
+  // column in (the stride stays P) and the last column read is max_pdf + 1
+  const int32_t col0 = d->o.ll_columns == 1 ? 1 : 0;
+  if (P <= d->g->max_pdf + col0)
+    return fail(WFST_ERR_PDF_RANGE, "P=" + std::to_string(P) + " too small for max pdf " + std::to_string(d->g->max_pdf) +
+                                        (col0 ? " with ilabel columns (P >= max ilabel + 1)" : " (P > max pdf)"));
+  d_loglikes += col0;
   DeviceGuard dg(d->device);
   cudaStream_t st = (cudaStream_t)cuda_stream;
   cudaError_t eo = order_after_previous(d, st);

@@ -48,7 +48,7 @@ class DecoderOpts(C.Structure):
                 ("max_ctas", C.c_int32), ("debug_costs", C.c_int32), ("ctas_per_sm", C.c_int32),
                 ("lattice", C.c_int32), ("lattice_beam", C.c_float), ("lattice_arcs_per_stream", C.c_int64),
                 ("max_active_mode", C.c_int32), ("reclaim", C.c_int32), ("insert_order", C.c_int32),
-                ("bin_capacity", C.c_int32)]
+                ("bin_capacity", C.c_int32), ("ll_columns", C.c_int32)]
 
 
 class Stats(C.Structure):
