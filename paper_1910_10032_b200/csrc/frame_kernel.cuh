@@ -7,6 +7,7 @@
 // sorted by state id, with traceback records.  DESIGN.md §5 explains the layout.
 #pragma once
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include "wfst_internal.h"
@@ -198,6 +199,22 @@ __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
 __device__ __forceinline__ void red_add_s(uint32_t a, int v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+// Predicated forms: the condition becomes an instruction predicate instead of a branch around
+// the atomic/store (no BSSY/BSYNC reconvergence per call site in the hot loops).
+__device__ __forceinline__ void red_add_s_if(bool c, uint32_t a, int v) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p red.shared.add.u32 [%0], %1;\n}" ::"r"(a), "r"(v),
+               "r"((uint32_t)c) : "memory");
+}
+__device__ __forceinline__ int atom_add_s_if(bool c, uint32_t a, int v) {
+  int old = 0;
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n @p atom.shared.add.u32 %0, [%1], %2;\n}"
+               : "+r"(old) : "r"(a), "r"(v), "r"((uint32_t)c) : "memory");
+  return old;
+}
+__device__ __forceinline__ void sts128_if(bool c, uint32_t a, int4 v) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %5, 0;\n @p st.shared.v4.s32 [%0], {%1, %2, %3, %4};\n}"
+               ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"((uint32_t)c) : "memory");
+}
 __device__ __forceinline__ int lds32(uint32_t a) {
   int v;
   asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
@@ -358,8 +375,7 @@ __device__ __forceinline__ int warp_append(bool need, uint32_t counter_sa) {
   const unsigned m = __ballot_sync(0xffffffffu, need);
   if (m == 0) return -1;
   const int leader = __ffs(m) - 1;
-  int base = 0;
-  if (lane == leader) base = atom_add_s(counter_sa, __popc(m));
+  int base = atom_add_s_if(lane == leader, counter_sa, __popc(m));
   base = __shfl_sync(0xffffffffu, base, leader);
   return need ? base + __popc(m & ((1u << lane) - 1u)) : -1;
 }
@@ -384,6 +400,10 @@ __device__ __forceinline__ long long block_sum64(long long v, long long* s_tmp) 
   return t;
 }
 
+// shared address of a field (optionally indexed) of the Frame's SmemCtl
+#define SA(field) (S_sa + (uint32_t)offsetof(SmemCtl, field))
+#define SAI(field, i) (S_sa + (uint32_t)offsetof(SmemCtl, field) + 4u * (uint32_t)(i))
+
 // ---------------- one lane's frames ----------------
 template <int BS, int R, int AM>
 struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a template parameter so
@@ -395,6 +415,8 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   uint32_t hist_sa;   // shared address of the cost histogram (kNB ints)
   uint32_t stage_sa;  // shared address of this warp's staging buffer (kStage x 16 B)
   uint32_t row_sa;    // shared address of the staged log-likelihood row region
+  uint32_t S_sa;      // shared address of S (field addresses are S_sa + offsetof: no per-use
+                      // generic-to-shared conversion, which re-reads the CTA's window base)
   int* hist;
   int* wbuf;          // this warp's owner buffer (32 ints, -1 when idle)
   // lane buffers
@@ -410,8 +432,8 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
 
   __device__ Frame(const KParams& p_, SmemCtl& S_, uint32_t tab_sa_, int* hist_, int* wbuf_, uint32_t stage_sa_,
                    uint32_t row_sa_)
-      : p(p_), S(S_), tab_sa(tab_sa_), hist_sa(saddr(hist_)), stage_sa(stage_sa_), row_sa(row_sa_), hist(hist_),
-        wbuf(wbuf_) {}
+      : p(p_), S(S_), tab_sa(tab_sa_), hist_sa(saddr(hist_)), stage_sa(stage_sa_), row_sa(row_sa_),
+        S_sa(saddr(&S_)), hist(hist_), wbuf(wbuf_) {}
 
   // ---- row a0: the frame's log-likelihood row is staged in shared memory by one TMA bulk
   // copy (issued by thread 0; the next frame's row is prefetched during this frame's tail)
@@ -479,12 +501,12 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   __device__ __forceinline__ void pl_update(int slot, bool claimed, bool strict, uint32_t old_hi, uint32_t new_hi) {
     if (slot < 0) return;
     if (claimed) {
-      red_add_s(saddr(&S.pl[pbin(float_of_ord(new_hi))]), 1);
+      red_add_s(SAI(pl, pbin(float_of_ord(new_hi))), 1);
     } else if (strict) {
       const int ob = pbin(float_of_ord(old_hi)), nb = pbin(float_of_ord(new_hi));
       if (ob != nb) {
-        red_add_s(saddr(&S.pl[ob]), -1);
-        red_add_s(saddr(&S.pl[nb]), 1);
+        red_add_s(SAI(pl, ob), -1);
+        red_add_s(SAI(pl, nb), 1);
       }
     }
   }
@@ -517,12 +539,11 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     if (m == 0) return false;
     if (seed) {   // claimed states with epsilon arcs seed the closure (no table scan later)
       const bool e = claimed && eps_flag;
-      const int idx = warp_append(e, saddr(&S.n_wl));
+      const int idx = warp_append(e, SA(n_wl));
       if (e) wl0[idx] = (uint32_t)slot;
     }
     const int leader = __ffs(m) - 1;
-    int base = 0;
-    if (lane == leader) base = atom_add_s(saddr(&S.n_claim), __popc(m));
+    int base = atom_add_s_if(lane == leader, SA(n_claim), __popc(m));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (claimed) {
       const int ci = base + __popc(m & ((1u << lane) - 1u));
@@ -532,12 +553,12 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         if (oi < p.C_ovf) claim[oi] = (uint32_t)slot;
         else S.status = WFST_ERR_CAPACITY;
       }
-      if (bin >= 0 && !S.sorted) red_add_s(hist_sa + 4u * (uint32_t)bin, 1);
+      red_add_s_if(bin >= 0 && !S.sorted, hist_sa + 4u * (uint32_t)bin, 1);
     }
     if (S.sorted) {   // bin-ordered frames: a warp's claims share few bins -- one atomic per bin
       const int key = claimed && bin >= 0 ? bin : -1;
       const unsigned grp = __match_any_sync(0xffffffffu, key);
-      if (key >= 0 && lane == __ffs(grp) - 1) red_add_s(hist_sa + 4u * (uint32_t)key, __popc(grp));
+      red_add_s_if(key >= 0 && lane == __ffs(grp) - 1, hist_sa + 4u * (uint32_t)max(key, 0), __popc(grp));
     }
     const int end = base + __popc(m);
     const int sh = S.sorted ? kThShiftSorted : kThShift;   // bin order: claims past alpha are waste
@@ -593,8 +614,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     const int pb = ok ? (e.w & 0x7FFFFFFF) / (kNB / kPlace) : kPlace;
     const unsigned grp = __match_any_sync(0xffffffffu, pb);
     const int leader = __ffs(grp) - 1;
-    int base = 0;
-    if (pb < kPlace && lane == leader) base = atom_add_s(saddr(&S.bcnt[pb]), __popc(grp));
+    int base = atom_add_s_if(pb < kPlace && lane == leader, SAI(bcnt, min(pb, kPlace - 1)), __popc(grp));
     base = __shfl_sync(0xffffffffu, base, leader);
     const int idx = base + __popc(grp & ((1u << lane) - 1u));
     const bool direct = ok && idx >= p.cbuf_cap;
@@ -640,9 +660,9 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       const int key = claimed ? (bin / (kNB / kPlace)) : -1;
       if (S.sorted) {
         const unsigned grp = __match_any_sync(0xffffffffu, key);
-        if (key >= 0 && lane == __ffs(grp) - 1) red_add_s(saddr(&S.pl[key]), __popc(grp));
-      } else if (key >= 0) {
-        red_add_s(saddr(&S.pl[key]), 1);
+        red_add_s_if(key >= 0 && lane == __ffs(grp) - 1, SAI(pl, max(key, 0)), __popc(grp));
+      } else {
+        red_add_s_if(key >= 0, SAI(pl, max(key, 0)), 1);
       }
     }
     if (add_claim(slot, claimed, flag, bin)) update_theta();
@@ -656,7 +676,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     const int n = __popc(m);
     const int rank = __popc(m & ((1u << lane) - 1u));
     if (staged + n < kStage) {
-      if (pass) sts128(stage_sa + 16u * (staged + rank), entry);
+      sts128_if(pass, stage_sa + 16u * (staged + rank), entry);
       staged += n;
     } else {
       const int room = kStage - staged;
@@ -683,15 +703,14 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     const float ref = S.ref, inv_w = S.inv_w, beam = p.beam;
     const uint32_t rowp = row_sa + (uint32_t)S.row_off;
     rowg = row_ptr(S.t_cur);
-    const uint32_t best_sa = saddr(&S.best_ord), theta_sa = saddr(&S.theta);
+    const uint32_t best_sa = SA(best_ord), theta_sa = SA(theta);
     long long arcs_total = 0;
     int staged = 0;   // warp-uniform
     // token groups of 32 are handed out dynamically (warps whose groups hold long arc lists
     // do not hold the CTA back at the barrier)
-    const uint32_t next_sa = saddr(&S.next_group);
+    const uint32_t next_sa = SA(next_group);
     while (true) {
-      int tb = 0;
-      if (lane == 0) tb = atom_add_s(next_sa, 32);
+      int tb = atom_add_s_if(lane == 0, next_sa, 32);
       tb = __shfl_sync(0xffffffffu, tb, 0);
       if (tb >= n_f) break;
       const int i = tb + lane;
@@ -802,7 +821,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     if (staged > 0) flush(staged, beam, best_sa, theta_sa);
     {
       const unsigned long long wsum = warp_sum64((unsigned long long)arcs_total);
-      if (lane == 0 && wsum) red_add_s64(saddr(&S.emit_arcs), wsum);
+      if (lane == 0 && wsum) red_add_s64(SA(emit_arcs), wsum);
     }
     __syncthreads();
     mark(4);   // hub tokens done
@@ -834,10 +853,9 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     }
     __syncthreads();
     const int total = S.bbase[kPlace];
-    const uint32_t cur_sa = saddr(&S.next_chunk);
+    const uint32_t cur_sa = SA(next_chunk);
     while (true) {
-      int c0 = 0;
-      if (lane == 0) c0 = atom_add_s(cur_sa, 32);
+      int c0 = atom_add_s_if(lane == 0, cur_sa, 32);
       c0 = __shfl_sync(0xffffffffu, c0, 0);
       if (c0 >= total) break;
       const int i = c0 + lane;
@@ -940,12 +958,14 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       return;
     }
     // exact alpha-th smallest in-beam cost by radix select on rk = ord(c) - ord(best) (every
-    // entry is >= best), 10-bit digits from the top set bit of ord(beam_cut) - ord(best); the
-    // first pass also counts the in-beam entries.
+    // entry is >= best): digits of up to 10 bits from the top set bit of the span
+    // ord(beam_cut) - ord(best) down (every in-beam rk < span), so the first pass spreads the
+    // entries over up to 1024 counters (a degenerate 1-2 bit top digit would send them all to
+    // the same shared counter); the first pass also counts the in-beam entries.
     const uint32_t ob = S.best_ord;
     const uint32_t span = ord_of(beam_cut) - ob;
     const int nbits = span ? 32 - __clz(span) : 1;
-    int shift = ((nbits + 9) / 10) * 10 - 10;
+    int hi = nbits, shift = max(nbits - 10, 0);
     if (tid == 0) {
       S.radix_prefix = 0;
       S.radix_k = p.alpha;
@@ -957,12 +977,13 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       for (int i = tid; i < kNB; i += BS) hist[i] = 0;
       __syncthreads();
       const uint32_t prefix = (uint32_t)S.radix_prefix;
-      const uint32_t hmask = (shift + 10 >= 32) ? 0u : (0xFFFFFFFFu << (shift + 10));
+      const uint32_t hmask = hi >= 32 ? 0u : (0xFFFFFFFFu << hi);
+      const uint32_t dmask = (1u << (hi - shift)) - 1u;
       scan_entries<4>([&](int, u64 v) {
         if (v == kEmpty || !(key_cost(v) < beam_cut)) return;
         if (first) cnt++;
         const uint32_t rk = (uint32_t)(v >> 32) - ob;
-        if ((rk & hmask) == (prefix & hmask)) red_add_s(hist_sa + 4u * ((rk >> shift) & 1023u), 1);
+        red_add_s_if((rk & hmask) == (prefix & hmask), hist_sa + 4u * ((rk >> shift) & dmask), 1);
       });
       if (first) {
         const long long n_in = block_sum64<BS>(cnt, S.warp_tmp64);   // includes a barrier
@@ -1005,7 +1026,8 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         }
         break;
       }
-      shift = max(shift - 10, 0);
+      hi = shift;
+      shift = max(hi - 10, 0);
       if (tid == 0) S.sel_entries += (unsigned long long)n_claim;   // one more radix pass
     }
     for (int i = tid; i < kNB; i += BS) hist[i] = 0;
@@ -1124,7 +1146,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
           const uint32_t has_eps = (uint32_t)arc.w >> 31;
           add_claim(slot, claimed, has_eps, -1, false);
           const bool push = strict && has_eps;
-          const int wi = warp_append(push, saddr(&S.wlc[rn]));
+          const int wi = warp_append(push, SAI(wlc, rn));
           if (push) {
             if (wi < p.FCAP) Wn[wi] = (uint32_t)slot;
             else S.status = WFST_ERR_CAPACITY;
@@ -1137,7 +1159,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     }
     {
       const unsigned long long wsum = warp_sum64((unsigned long long)relax);
-      if ((tid & 31) == 0 && wsum) red_add_s64(saddr(&S.eps_relax), wsum);
+      if ((tid & 31) == 0 && wsum) red_add_s64(SA(eps_relax), wsum);
     }
   }
 
@@ -1200,16 +1222,17 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         const int bk = k ? min(pbin(c), bc) : kPlace;   // bin bc: the append region
         const unsigned grp = __match_any_sync(0xffffffffu, bk);
         const int leader = __ffs(grp) - 1;
-        int base = 0;
-        if (bk < kPlace && lane == leader)
-          base = bk < bc ? atom_add_s(saddr(&S.pl_base[bk]), __popc(grp)) : app0 + atom_add_s(saddr(&S.n_app), __popc(grp));
+        const bool lead = bk < kPlace && lane == leader;
+        int base = atom_add_s_if(lead && bk < bc, SAI(pl_base, min(bk, kPlace - 1)), __popc(grp));
+        base += atom_add_s_if(lead && bk >= bc, SA(n_app), __popc(grp));
+        if (bk >= bc) base += app0;
         base = __shfl_sync(0xffffffffu, base, leader);
         pos[u] = k ? base + __popc(grp & ((1u << lane) - 1u)) : (live ? -1 : -2);
         if (live) clear_slot(sl[u]);
 #ifdef WFST_COUNT
         if (live && !k && S.use_alpha && c < cut_b) {
           const float d = __fsub_rn(c, cut_a);
-          red_add_s64(saddr(&S.dbgc[d <= 0.5f ? 0 : d <= 2.0f ? 1 : d <= 5.0f ? 2 : 3]), 1ull);
+          red_add_s64((SA(dbgc) + 8u * (d <= 0.5f ? 0u : d <= 2.0f ? 1u : d <= 5.0f ? 2u : 3u)), 1ull);
         }
 #endif
 
@@ -1240,7 +1263,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     });
     {
       const unsigned long long wsum = warp_sum64(epsd);
-      if (lane == 0 && wsum) red_add_s64(saddr(&S.eps_deg), wsum);
+      if (lane == 0 && wsum) red_add_s64(SA(eps_deg), wsum);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
       if (lane == 0 && mn < INFINITY) atomicMin((unsigned int*)&S.warp_tmp[0], ord_of(mn));
@@ -1515,6 +1538,10 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
 #endif
     const bool alpha_frame = S.use_alpha != 0;
     finish_frame(t, true);
+#ifdef WFST_FRAMECYC   // instrumentation build: the frame's SM cycles replace its epsilon-degree count
+    if (tid == 0 && S.L.status == WFST_OK)
+      p.fcounts[((size_t)S.lane * p.TMAX + (S.L.frames - 1) % p.TMAX) * 5 + 4] = clock64() - t_frame0;
+#endif
     tick(t0, 5);
     flush_phases(alpha_frame, (u64)(clock64() - t_frame0));
   }
