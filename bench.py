@@ -274,7 +274,7 @@ def run_gpu_once(cfg="c3", preset="clean", with_paths=True):
 def decoder_opts(args) -> dict:
     o = {}
     for k in ("threads", "ctas_per_sm", "table_slots", "frames_per_item", "insert_order", "bin_capacity",
-              "records_per_stream", "max_frames"):
+              "records_per_stream", "max_frames", "gc_frames"):
         v = getattr(args, k, 0)
         if v:
             o[k] = v
@@ -505,7 +505,11 @@ def gpu_arm(args):
         if sum(st["phase_cycles"].values()) else None,
         "memory": {"graph_device_bytes": ginfo.device_bytes, "graph_eq1_bytes": ginfo.eq1_bytes,
                    "decoder_device_bytes": st["device_bytes"],
+                   "record_arena_bytes": st["record_bytes"],
+                   "decoder_state_bytes": st["device_bytes"] - st["record_bytes"],
+                   "records_per_stream": st["records_per_stream"],
                    "records_used_max_per_stream": st["records_used_max"],
+                   "records_written_per_step_bytes": int(8 * st["survivors"] / max(1, args.steps)),
                    "eq2_bytes_nc=nl=B": W.eq2_bytes(wl["alpha"], B, B)},
         "gather": gather,
         "clocks": clocks,
@@ -607,6 +611,8 @@ def main(argv=None):
                     help="traceback GC (row f2): with --partial, records below each stream's settle point are reused")
     ap.add_argument("--records-per-stream", dest="records_per_stream", type=int, default=0)
     ap.add_argument("--max-frames", dest="max_frames", type=int, default=0)
+    ap.add_argument("--gc-frames", dest="gc_frames", type=int, default=0,
+                    help="traceback GC every N frames (opts.gc_frames): records of dead branches are dropped")
     ap.add_argument("--beam", type=float, default=None, help="override the config's beam (experiments)")
     ap.add_argument("--max-active", dest="max_active", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")

@@ -122,6 +122,15 @@ typedef struct {
                                 a P that fits only layout 0 is rejected under layout 1 (PDF_RANGE)
                                 and the caller chooses the layout explicitly, so a SPEC-shaped
                                 matrix is never read one column off by default-guessing.        */
+  int32_t gc_frames;         /* traceback GC: > 0 = every decode call runs its
+                                frames in launches of at most gc_frames frames, each followed by
+                                a compaction that drops the records no current survivor's
+                                traceback reaches; a stream then holds only its live traceback tree
+                                plus gc_frames frames of new records, however long the utterance,
+                                and records_per_stream defaults to that (gc_frames + 64 frames at
+                                the max-active bound).  Results are unchanged (wfst_debug_layer of
+                                an older layer lists only its live tokens).  Exclusive with
+                                lattice.  0 (default): off.                                     */
 } wfst_decoder_opts_t;
 
 typedef struct {
@@ -142,6 +151,11 @@ typedef struct {
   int64_t select_entries;    /* token-table entries read by the max-active selection, summed over
                                 passes (SURVEY §8.5's passes x n_uniq term of the byte model)     */
   int64_t phase_cycles_alpha[12]; /* phase_cycles restricted to frames where max-active bound      */
+  int64_t records_per_stream;/* traceback record capacity per stream (the history arena)          */
+  int64_t record_bytes;      /* device bytes of the history arena (records, + costs if kept); the
+                                rest of device_bytes is decoder state proper (frontiers, lane
+                                state, per-CTA scratch): the counterpart of P:117-126's Eq. 2,
+                                whose decoder keeps no traceback on the device        */
 } wfst_stats_t;
 
 /* ---- graph (row a0 of SURVEY §8) ------------------------------------------------ */
@@ -235,8 +249,9 @@ wfst_status wfst_decoder_reset_stats(wfst_decoder_t d);
 
 /* Per-frame record of a lane's current utterance (frames < opts.max_frames):
  * fstats[t*3+{0,1,2}] = best candidate cost, beam cutoff, max-active cutoff k_alpha (+INF if
- * unused); fcounts[t*5+{0..4}] = distinct candidates, in-beam candidates, survivors, emitting
- * arcs expanded, epsilon out-degree of survivors.  Either pointer may be NULL. */
+ * unused); fcounts[t*5+{0..4}] = distinct candidates, in-beam candidates (-1 when the cutoff
+ * did not need the exact count: max-active provably bound or could not bind), survivors,
+ * emitting arcs expanded, epsilon out-degree of survivors.  Either pointer may be NULL. */
 wfst_status wfst_decoder_frame_stats(wfst_decoder_t d, int32_t stream, float* fstats,
                                      int64_t* fcounts, int32_t cap_frames, int32_t* n_frames);
 

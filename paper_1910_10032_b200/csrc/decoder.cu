@@ -18,6 +18,7 @@
 #include "frame_kernel.cuh"
 #include "lattice_kernel.cuh"
 #include "partial_kernel.cuh"
+#include "gc_kernel.cuh"
 #include "wfst_internal.h"
 
 using namespace wfst;
@@ -230,6 +231,7 @@ struct wfst_decoder_s {
   cudaEvent_t ev_copy[kStages] = {}, ev_use[kStages] = {};
   int2* d_settled = nullptr;        // [lane] last settle point of the partial results (row f2)
   size_t partial_smem = 0;
+  size_t gc_smem = 0;               // traceback GC kernel (opts.gc_frames)
   // lattice (row f1)
   bool lattice = false;
   int64_t S_cap = 0;
@@ -337,6 +339,29 @@ cudaError_t launch_frames(wfst_decoder_t d, KParams kp, cudaStream_t st) {
   e = cudaMemsetAsync(kp.lane_round, 0, sizeof(int32_t) * kp.B, st);
   if (e != cudaSuccess) return e;
   d->variant->launch(grid, d->smem_bytes, st, kp);
+  return cudaGetLastError();
+}
+
+// traceback GC (opts.gc_frames): compact every lane of the current batch (gc_kernel.cuh)
+cudaError_t launch_gc(wfst_decoder_t d, int32_t B, cudaStream_t st) {
+  GcParams gp{};
+  gp.arcs = d->kp.arcs;
+  gp.lanes = d->d_lane_ids;
+  gp.lanes_st = d->d_lanes;
+  gp.rec = d->kp.rec;
+  gp.rec_cost = d->kp.rec_cost;
+  gp.R_cap = d->R_cap;
+  gp.layer_info = d->kp.layer_info;
+  gp.TMAX = d->TMAX;
+  gp.settled = d->d_settled;
+  gp.wcap = 53248;   // 208 KB: two (epsilon, emitting) source-set pairs of 4k + 22.5k slots
+  const size_t smem = (size_t)gp.wcap * 4;
+  if (d->gc_smem != smem) {
+    cudaError_t e = cudaFuncSetAttribute(gc_kernel<kGcThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    d->gc_smem = smem;
+  }
+  gc_kernel<kGcThreads><<<B, kGcThreads, smem, st>>>(gp);
   return cudaGetLastError();
 }
 
@@ -460,8 +485,20 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
   d->FCAP = d->C + d->C_ovf;
   d->TMAX = d->o.max_frames > 0 ? d->o.max_frames : 4096;
   int64_t per_frame = d->alpha > 0 ? std::min<int64_t>((int64_t)d->alpha * 5 / 4 + 1024, d->FCAP) : d->FCAP;
+  if (d->o.gc_frames < 0) {
+    delete d;
+    return fail(WFST_ERR_INVALID_ARG, "opts.gc_frames must be >= 0");
+  }
+  if (d->o.gc_frames > 0 && d->o.lattice) {
+    delete d;
+    return fail(WFST_ERR_INVALID_ARG, "opts.gc_frames and opts.lattice are exclusive (the lattice needs every record)");
+  }
   if (d->o.records_per_stream > 0) {
     d->R_cap = d->o.records_per_stream;
+  } else if (d->o.gc_frames > 0) {
+    // traceback GC: a stream holds its live traceback tree plus the records of the frames since
+    // the last collection -- gc_frames + 64 frames at the max-active bound
+    d->R_cap = (int64_t)(d->o.gc_frames + 64) * per_frame;
   } else {
     // default: ~max_frames/4 frames at the alpha bound, capped to half of the free device memory
     d->R_cap = (int64_t)(d->TMAX / 4 + 1) * per_frame;
@@ -795,11 +832,21 @@ wfst_status wfst_decode_frames(wfst_decoder_t d, const float* d_loglikes, int32_
   int K = d->o.frames_per_item;
   int max_ctas = d->o.max_ctas > 0 ? d->o.max_ctas : d->n_sm;
   if (B <= max_ctas) K = T;
-  kp.K = K;
-  long long items = (long long)((T + K - 1) / K) * B;
-  if (items > INT32_MAX) return fail(WFST_ERR_INVALID_ARG, "too many work items");
-  kp.n_items = (int32_t)items;
-  cudaError_t e = launch_frames(d, kp, st);
+  // traceback GC: the frames run in launches of at most gc_frames frames, each followed by a
+  // compaction of the batch's records (stream-ordered, no host synchronisation)
+  const int32_t G = d->o.gc_frames > 0 ? d->o.gc_frames : T;
+  cudaError_t e = cudaSuccess;
+  for (int32_t t0 = 0; t0 < T && e == cudaSuccess; t0 += G) {
+    KParams kq = kp;
+    kq.T = std::min(G, T - t0);
+    kq.ll = d_loglikes + (size_t)t0 * B * P;
+    kq.K = std::min(K, kq.T);
+    long long items = (long long)((kq.T + kq.K - 1) / kq.K) * B;
+    if (items > INT32_MAX) return fail(WFST_ERR_INVALID_ARG, "too many work items");
+    kq.n_items = (int32_t)items;
+    e = launch_frames(d, kq, st);
+    if (e == cudaSuccess && d->o.gc_frames > 0) e = launch_gc(d, B, st);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");
   if (d->lattice) {
     e = launch_lattice(d, d_loglikes, T, B, P, kModeFrames, st);
@@ -1027,12 +1074,15 @@ wfst_status wfst_decoder_stats(wfst_decoder_t d, wfst_stats_t* s) {
     s->survivors += x.surv;
     s->overflow_inserts += x.ovf;
     s->alpha_frames += x.alpha_frames;
-    s->records_used_max = std::max<int64_t>(s->records_used_max, x.rec_used);
+    s->records_used_max = std::max<int64_t>(s->records_used_max, x.rec_peak);
     for (int k = 0; k < 12; k++) s->phase_cycles[k] += (int64_t)x.phase[k];
     for (int k = 0; k < 12; k++) s->phase_cycles_alpha[k] += (int64_t)x.phase_alpha[k];
     s->select_entries += (int64_t)x.sel_entries;
   }
   s->device_bytes = d->device_bytes;
+  s->records_per_stream = d->R_cap;
+  s->record_bytes = (int64_t)d->n_lanes * d->R_cap * (int64_t)(sizeof(int2) + (d->kp.rec_cost ? 4 : 0) +
+                                                               (d->kp.rec_si ? sizeof(int4) : 0));
   return WFST_OK;
 }
 

@@ -64,7 +64,9 @@ struct LaneState {
   float cpa[2];         // moving average of SM cycles per emitting arc in alpha-bound frames,
                         // arrival order [0] and bin order [1] (insert_order = auto picks the cheaper)
   int32_t n_alpha_seen; // alpha-bound frames seen by the chooser
-  int32_t pad2_;
+  int32_t gc_layer;     // newest layer the last traceback GC compacted (-1: none; gc_kernel.cuh)
+  int32_t rec_peak;     // most records held at once (rec_used - rec_floor after a frame)
+  int32_t pad3_;
 };
 
 struct KParams {
@@ -111,7 +113,6 @@ struct SmemCtl {
 #ifdef WFST_COUNT
   unsigned long long dbgc[4];   // alpha-bound frames: claims above k_alpha by (0,0.5], (0.5,2], (2,5], >5
 #endif
-  int32_t pl[kPlace];        // placement histogram: live entries per coarse cost bin
   int32_t bcnt[kPlace];      // bin-ordered frames: candidates appended per coarse cost bin
   int32_t bbase[kPlace + 1]; // bin-ordered frames: their prefix sums (drain order)
   int32_t next_chunk;        // bin-ordered frames: drain cursor
@@ -126,6 +127,8 @@ struct SmemCtl {
   float beam_cut, kalpha, ref, inv_w, min_surv;
   int32_t use_alpha;
   int32_t radix_prefix, radix_k;
+  int32_t sel_mode, sel_bin, sel_cnt, sel_h;   // fast selection: mode, bin b*, its entries, H(bb)
+  uint32_t sel_span;
   unsigned long long emit_arcs, eps_deg, eps_relax, sel_entries;
   uint32_t sclaim[kSmallClaims];   // claimed slots while the frame is small
   int32_t warp_tmp[32];
@@ -165,6 +168,20 @@ __device__ __forceinline__ int4 lds128(uint32_t a) {
                : "r"(a)
                : "memory");
   return v;
+}
+// sum of 4*N consecutive ints at a 16-B aligned shared address (N 128-bit loads in flight).
+// Lanes reading blocks 128 B apart start at rotated offsets, so a warp's loads spread over the
+// banks instead of all lanes hitting the same four.
+template <int N>
+__device__ __forceinline__ int lds_sum(uint32_t a) {
+  const uint32_t rot = threadIdx.x & (N - 1);
+  int4 v[N];
+#pragma unroll
+  for (int i = 0; i < N; i++) v[i] = lds128(a + 16u * ((i + rot) & (N - 1)));
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < N; i++) t += v[i].x + v[i].y + v[i].z + v[i].w;
+  return t;
 }
 __device__ __forceinline__ void sts128(uint32_t a, int4 v) {
   asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -417,7 +434,10 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   uint32_t row_sa;    // shared address of the staged log-likelihood row region
   uint32_t S_sa;      // shared address of S (field addresses are S_sa + offsetof: no per-use
                       // generic-to-shared conversion, which re-reads the CTA's window base)
-  int* hist;
+  int* hist;          // exact count of live table entries per fine cost bin (bin_of), kept by every
+                      // insert: +1 on a claim, a move between bins on a strict improvement
+  int* sel;           // selection scratch (kNB ints): the stage buffers, idle after the expansion
+  uint32_t sel_sa;
   int* wbuf;          // this warp's owner buffer (32 ints, -1 when idle)
   // lane buffers
   int4* F0;           // frontier buffer 0; buffer 1 follows at +FCAP
@@ -431,9 +451,9 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   int4* rec_si;
 
   __device__ Frame(const KParams& p_, SmemCtl& S_, uint32_t tab_sa_, int* hist_, int* wbuf_, uint32_t stage_sa_,
-                   uint32_t row_sa_)
+                   uint32_t row_sa_, int* sel_)
       : p(p_), S(S_), tab_sa(tab_sa_), hist_sa(saddr(hist_)), stage_sa(stage_sa_), row_sa(row_sa_),
-        S_sa(saddr(&S_)), hist(hist_), wbuf(wbuf_) {}
+        S_sa(saddr(&S_)), hist(hist_), sel(sel_), sel_sa(saddr(sel_)), wbuf(wbuf_) {}
 
   // ---- row a0: the frame's log-likelihood row is staged in shared memory by one TMA bulk
   // copy (issued by thread 0; the next frame's row is prefetched during this frame's tail)
@@ -494,19 +514,24 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     return slot < p.C ? slot_key(slot) : ldg_volatile64(ovf + (slot - p.C));
   }
 
-  // coarse placement bin of a cost: kNB/kPlace consecutive max-active bins (monotone in c)
+  // coarse placement bin of a cost: kNB/kPlace consecutive fine bins (monotone in c)
   __device__ __forceinline__ int pbin(float c) const { return bin_of(c, S.ref, S.inv_w) / (kNB / kPlace); }
-  // keep the placement histogram equal to the table's current costs: +1 on a claim, a move
-  // between bins on a strict improvement (DESIGN.md §5.2 contraction)
-  __device__ __forceinline__ void pl_update(int slot, bool claimed, bool strict, uint32_t old_hi, uint32_t new_hi) {
+  __device__ __forceinline__ int fbin(float c) const { return bin_of(c, S.ref, S.inv_w); }
+  // keep the fine histogram equal to the table's current costs: +1 on a claim, a move between
+  // bins on a strict improvement (DESIGN.md §5.2 contraction, §10 selection)
+  // fine: keep every fine bin exact (the emitting phase: the cutoff selection reads fine counts);
+  // otherwise only the coarse sums (the epsilon closure and the initial frame: only the
+  // contraction's cursors read the histogram after the selection)
+  __device__ __forceinline__ void hist_update(int slot, bool claimed, bool strict, uint32_t old_hi, uint32_t new_hi,
+                                              bool fine) {
     if (slot < 0) return;
     if (claimed) {
-      red_add_s(SAI(pl, pbin(float_of_ord(new_hi))), 1);
+      red_add_s(hist_sa + 4u * (uint32_t)fbin(float_of_ord(new_hi)), 1);
     } else if (strict) {
-      const int ob = pbin(float_of_ord(old_hi)), nb = pbin(float_of_ord(new_hi));
-      if (ob != nb) {
-        red_add_s(SAI(pl, ob), -1);
-        red_add_s(SAI(pl, nb), 1);
+      const int ob = fbin(float_of_ord(old_hi)), nb = fbin(float_of_ord(new_hi));
+      if (fine ? ob != nb : (ob >> 4) != (nb >> 4)) {
+        red_add_s(hist_sa + 4u * (uint32_t)ob, -1);
+        red_add_s(hist_sa + 4u * (uint32_t)nb, 1);
       }
     }
   }
@@ -518,7 +543,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     int s = insert_s(tab_sa, (uint32_t)p.NBK, q, key, claimed, logit, strict, old_hi);
     if (s < 0) s = insert_g(ovf, (uint32_t)(p.C_ovf / 4), q, key, claimed, logit, strict, old_hi);
     else {
-      pl_update(s, claimed && !agg_claims, strict && !claimed, old_hi, (uint32_t)(key >> 32));
+      hist_update(s, claimed && !agg_claims, strict && !claimed, old_hi, (uint32_t)(key >> 32), agg_claims);
       return s;
     }
     if (s < 0) {
@@ -526,7 +551,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       return -1;
     }
     if (claimed) atomicAdd(&S.n_ovf, 1);
-    pl_update(s, claimed && !agg_claims, strict && !claimed, old_hi, (uint32_t)(key >> 32));
+    hist_update(s, claimed && !agg_claims, strict && !claimed, old_hi, (uint32_t)(key >> 32), agg_claims);
     return s + p.C;
   }
 
@@ -574,9 +599,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   __device__ void update_theta() {
     const int lane = threadIdx.x & 31;
     const int base = lane * (kNB / 32);
-    int s = 0;
-#pragma unroll 8
-    for (int i = 0; i < kNB / 32; i++) s += lds32(hist_sa + 4u * (base + i));
+    const int s = lds_sum<kNB / 128>(hist_sa + 4u * base);
     const int incl = warp_incl_scan(s);
     const unsigned m = __ballot_sync(0xffffffffu, incl >= p.alpha);
     if (m != 0) {
@@ -656,16 +679,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         if (slot < 0) claimed = false;
       }
     }
-    {   // the claims' placement bins (bin / 16 == pbin of the cost), one atomic per distinct bin
-      const int key = claimed ? (bin / (kNB / kPlace)) : -1;
-      if (S.sorted) {
-        const unsigned grp = __match_any_sync(0xffffffffu, key);
-        red_add_s_if(key >= 0 && lane == __ffs(grp) - 1, SAI(pl, max(key, 0)), __popc(grp));
-      } else {
-        red_add_s_if(key >= 0, SAI(pl, max(key, 0)), 1);
-      }
-    }
-    if (add_claim(slot, claimed, flag, bin)) update_theta();
+    if (add_claim(slot, claimed, flag, bin)) update_theta();   // counts the claims in hist
   }
 
   // stage one round of candidates (warp-collective); flushes when the buffer fills
@@ -957,6 +971,128 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       select_hist();
       return;
     }
+    // Fast path: hist holds the exact count of live entries per fine cost bin.  bin_of is
+    // monotone, so the entries of bins < bb = bin(beam_cut) are in beam and every in-beam entry
+    // lies in a bin <= bb.  With H(b) = entries in bins < b: H(bb + 1) <= alpha -> max-active
+    // cannot bind; H(bb) > alpha -> it binds and k_alpha is the r-th smallest cost of the bin b*
+    // where H reaches alpha (r = alpha - H(b*)): one pass collects that bin's costs, a small
+    // radix select over them finds k_alpha.  Otherwise (the bound depends on how bin bb splits
+    // at the cutoff, or b* holds too many entries) the general radix select below runs.
+    const int bb = bin_of(beam_cut, S.ref, S.inv_w);
+    if (tid < 32) {
+      const int lane = tid;
+      int sum = 0;
+      sum = lds_sum<8>(hist_sa + 128u * (uint32_t)lane);
+      const int incl = warp_incl_scan(sum);
+      const int excl = incl - sum;
+      if (lane == (bb >> 5)) {   // H(bb), hist[bb]
+        int c = excl;
+        for (int d = lane * 32; d < bb; d++) c += lds32(hist_sa + 4u * (uint32_t)d);
+        S.sel_h = c;
+        S.n_in = lds32(hist_sa + 4u * (uint32_t)bb);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, incl >= p.alpha);
+      const int L = m ? __ffs(m) - 1 : 32;
+      if (lane == L) {   // b* and H(b*)
+        int c = excl, d = lane * 32;
+        for (; d < lane * 32 + 31; d++) {
+          const int h = lds32(hist_sa + 4u * (uint32_t)d);
+          if (c + h >= p.alpha) break;
+          c += h;
+        }
+        S.radix_k = p.alpha - c;   // rank within bin d (1-based)
+        S.sel_bin = d;
+        S.sel_cnt = lds32(hist_sa + 4u * (uint32_t)d);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int Hbb = S.sel_h, hbb = S.n_in;
+        int mode;   // 0 cannot bind, 1 binds in bin b*, 2 general select
+        if (Hbb + hbb <= p.alpha) mode = 0;
+        else if (Hbb > p.alpha && S.sel_cnt <= kNB - 256) mode = 1;
+        else mode = 2;
+        S.sel_mode = mode;
+        S.n_in = -1;                         // exact in-beam count: only the general select has it
+        if (mode == 0) {
+          S.use_alpha = 0;
+          S.kalpha = INFINITY;
+        }
+      }
+    }
+    __syncthreads();
+    const int smode = S.sel_mode;
+    if (smode == 0) return;
+    if (smode == 1) {
+      // collect the orderable costs of bin b*'s entries (all in beam) into sel[256..], their
+      // min into sel[0]; then 8-bit radix digits over ord - min select the r-th smallest
+      const int bs = S.sel_bin, cap = kNB - 256;
+      if (tid == 0) {
+        S.n_app = 0;
+        S.sel_span = 0;
+        sel[0] = -1;
+        S.sel_entries += (unsigned long long)n_claim;
+      }
+      __syncthreads();
+      const uint32_t cnt_sa = SA(n_app);
+      scan_entries<4>([&](int, u64 v) {
+        const bool in = v != kEmpty && fbin(key_cost(v)) == bs;
+        const int i = warp_append(in, cnt_sa);
+        if (in && i < cap) {   // i < hist[b*] <= cap: hist is exact
+          sel[256 + i] = (int)(uint32_t)(v >> 32);
+          atomicMin((unsigned int*)&sel[0], (uint32_t)(v >> 32));
+        }
+      });
+      __syncthreads();
+      const int m = min(S.n_app, cap);
+      const uint32_t lo = (uint32_t)sel[0];
+      uint32_t mx = 0;
+      for (int i = tid; i < m; i += BS) mx = max(mx, (uint32_t)sel[256 + i] - lo);
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      if ((tid & 31) == 0 && mx) atomicMax(&S.sel_span, mx);
+      __syncthreads();
+      const uint32_t span = S.sel_span;
+      int shift = span ? ((32 - __clz(span) + 7) / 8) * 8 - 8 : 0;
+      uint32_t prefix = 0;
+      int k = S.radix_k;
+      while (true) {
+        if (tid < 256) sel[tid] = 0;   // sel[0] (the min) is in lo already
+        __syncthreads();
+        const uint32_t hmask = shift + 8 >= 32 ? 0u : (0xFFFFFFFFu << (shift + 8));
+        for (int i = tid; i < m; i += BS) {
+          const uint32_t rk = (uint32_t)sel[256 + i] - lo;
+          red_add_s_if((rk & hmask) == (prefix & hmask), sel_sa + 4u * ((rk >> shift) & 255u), 1);
+        }
+        __syncthreads();
+        if (tid < 32) {   // warp 0: the digit holding rank k (8 digits per lane)
+          const int lane = tid;
+          int sum = 0;
+          sum = lds_sum<2>(sel_sa + 32u * (uint32_t)lane);
+          const int incl = warp_incl_scan(sum);
+          const unsigned bm = __ballot_sync(0xffffffffu, incl >= k);
+          const int L = __ffs(bm) - 1;
+          if (lane == L) {
+            int c = incl - sum, d = lane * 8;
+            for (; d < lane * 8 + 7; d++) {
+              if (c + sel[d] >= k) break;
+              c += sel[d];
+            }
+            S.radix_k = k - c;
+            S.radix_prefix = (int)(prefix | ((uint32_t)d << shift));
+          }
+        }
+        __syncthreads();
+        prefix = (uint32_t)S.radix_prefix;
+        k = S.radix_k;
+        if (shift == 0) break;
+        shift -= 8;
+      }
+      if (tid == 0) {
+        S.kalpha = float_of_ord(lo + prefix);
+        S.use_alpha = 1;
+      }
+      __syncthreads();
+      return;
+    }
     // exact alpha-th smallest in-beam cost by radix select on rk = ord(c) - ord(best) (every
     // entry is >= best): digits of up to 10 bits from the top set bit of the span
     // ord(beam_cut) - ord(best) down (every in-beam rk < span), so the first pass spreads the
@@ -974,7 +1110,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     bool first = true;
     if (tid == 0) S.sel_entries += (unsigned long long)n_claim;   // the first pass (in-beam count)
     while (true) {
-      for (int i = tid; i < kNB; i += BS) hist[i] = 0;
+      for (int i = tid; i < kNB; i += BS) sel[i] = 0;
       __syncthreads();
       const uint32_t prefix = (uint32_t)S.radix_prefix;
       const uint32_t hmask = hi >= 32 ? 0u : (0xFFFFFFFFu << hi);
@@ -983,7 +1119,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         if (v == kEmpty || !(key_cost(v) < beam_cut)) return;
         if (first) cnt++;
         const uint32_t rk = (uint32_t)(v >> 32) - ob;
-        red_add_s_if((rk & hmask) == (prefix & hmask), hist_sa + 4u * ((rk >> shift) & dmask), 1);
+        red_add_s_if((rk & hmask) == (prefix & hmask), sel_sa + 4u * ((rk >> shift) & dmask), 1);
       });
       if (first) {
         const long long n_in = block_sum64<BS>(cnt, S.warp_tmp64);   // includes a barrier
@@ -1003,7 +1139,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         const int lane = tid;
         const int k = S.radix_k;
         int sum = 0;
-        for (int i = 0; i < 32; i++) sum += hist[lane * 32 + i];
+        sum = lds_sum<8>(sel_sa + 128u * (uint32_t)lane);
         const int incl = warp_incl_scan(sum);
         const unsigned m = __ballot_sync(0xffffffffu, incl >= k);
         const int L = __ffs(m) - 1;
@@ -1011,8 +1147,8 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
           int c = incl - sum;
           int d = lane * 32;
           for (; d < lane * 32 + 31; d++) {
-            if (c + hist[d] >= k) break;
-            c += hist[d];
+            if (c + sel[d] >= k) break;
+            c += sel[d];
           }
           S.radix_k = k - c;
           S.radix_prefix = (int)(prefix | ((uint32_t)d << shift));
@@ -1030,7 +1166,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       shift = max(hi - 10, 0);
       if (tid == 0) S.sel_entries += (unsigned long long)n_claim;   // one more radix pass
     }
-    for (int i = tid; i < kNB; i += BS) hist[i] = 0;
+    for (int i = tid; i < kNB; i += BS) sel[i] = 0;
     __syncthreads();
   }
 
@@ -1043,7 +1179,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     const float beam_cut = S.beam_cut;
     const float best = float_of_ord(S.best_ord);
     const float inv = __fdiv_rn((float)kNB, p.beam), wd = __fdiv_rn(p.beam, (float)kNB);
-    for (int i = tid; i < kNB; i += BS) hist[i] = 0;
+    for (int i = tid; i < kNB; i += BS) sel[i] = 0;
     if (tid == 0) S.sel_entries += (unsigned long long)min(S.n_claim, p.FCAP);
     __syncthreads();
     long long cnt = 0;
@@ -1053,22 +1189,22 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       cnt++;
       float x = __fmul_rn(__fsub_rn(c, best), inv);
       x = fmaxf(fminf(x, (float)(kNB - 1)), 0.0f);
-      red_add_s(hist_sa + 4u * (uint32_t)(int)x, 1);
+      red_add_s(sel_sa + 4u * (uint32_t)(int)x, 1);
     });
     const long long n_in = block_sum64<BS>(cnt, S.warp_tmp64);   // includes a barrier
     if (tid < 32) {
       const int lane = tid;
       if (n_in > p.alpha) {   // warp 0: the bin where the cumulative count reaches alpha
         int sum = 0;
-        for (int i = 0; i < 32; i++) sum += hist[lane * 32 + i];
+        sum = lds_sum<8>(sel_sa + 128u * (uint32_t)lane);
         const int incl = warp_incl_scan(sum);
         const unsigned m = __ballot_sync(0xffffffffu, incl >= p.alpha);
         const int L = __ffs(m) - 1;
         if (lane == L) {
           int c = incl - sum, d = lane * 32;
           for (; d < lane * 32 + 31; d++) {
-            if (c + hist[d] >= p.alpha) break;
-            c += hist[d];
+            if (c + sel[d] >= p.alpha) break;
+            c += sel[d];
           }
           const float ca = __fadd_rn(best, __fmul_rn((float)(d + 1), wd));
           S.kalpha = nextafterf(ca, -INFINITY);
@@ -1081,7 +1217,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       if (lane == 0) S.n_in = (int)n_in;
     }
     __syncthreads();
-    for (int i = tid; i < kNB; i += BS) hist[i] = 0;
+    for (int i = tid; i < kNB; i += BS) sel[i] = 0;
     __syncthreads();
   }
 
@@ -1170,23 +1306,27 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   __device__ void contract() {
     const int tid = threadIdx.x, lane = tid & 31;
     const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
-    // The placement histogram counts the table's live entries per coarse cost bin (kept exact
-    // by every insert).  pbin is monotone, so bins below bc = min(pbin(cut_b), pbin(cut_a)) hold
-    // only survivors and no survivor lies above bc: their counts give exact cursors, and the
-    // survivors of bin bc are appended after them.  One pass over the table, no counting pass.
+    // The fine histogram counts the table's live entries per cost bin (kept exact by every
+    // insert); a coarse placement bin is kNB/kPlace consecutive fine bins.  pbin is monotone, so
+    // coarse bins below bc = min(pbin(cut_b), pbin(cut_a)) hold only survivors and no survivor
+    // lies above bc: their counts give exact cursors, and the survivors of bin bc are appended
+    // after them.  One pass over the table, no counting pass.
     const int bc = min(pbin(cut_b), pbin(cut_a));
-    static_assert(kPlace == 64, "warp 0 scans two placement bins per lane");
+    static_assert(kPlace == 64 && kNB == 1024, "warp 0 scans two coarse (32 fine) bins per lane");
     if (tid < 32) {   // exclusive scan of the bins below bc (per-frame critical path: no serial loop)
       const int b0 = 2 * lane, b1 = b0 + 1;
-      const int c0 = b0 < bc ? S.pl[b0] : 0, c1 = b1 < bc ? S.pl[b1] : 0;
+      const int f0 = lds_sum<4>(hist_sa + 128u * (uint32_t)lane);         // coarse bin b0
+      const int f1 = lds_sum<4>(hist_sa + 128u * (uint32_t)lane + 64u);   // coarse bin b1
+      const int c0 = b0 < bc ? f0 : 0, c1 = b1 < bc ? f1 : 0;
       const int incl = warp_incl_scan(c0 + c1);
       const int excl = incl - c0 - c1;
       if (b0 < bc) S.pl_base[b0] = excl;
       if (b1 < bc) S.pl_base[b1] = excl + c0;
       const int acc = __shfl_sync(0xffffffffu, incl, 31);
+      const int pbc = __shfl_sync(0xffffffffu, (bc & 1) ? f1 : f0, min(bc, kPlace - 1) >> 1);
       if (lane == 0) {
         S.pl_base[bc] = acc;
-        S.n_surv = acc + S.pl[bc];   // upper bound until the appended count is known
+        S.n_surv = acc + (bc < kPlace ? pbc : 0);   // upper bound until the appended count is known
         S.n_app = 0;
         S.min_surv = INFINITY;
         S.warp_tmp[0] = -1;   // min survivor cost, orderable (0xFFFFFFFF: none)
@@ -1280,10 +1420,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   __device__ void begin_frame(float beam_cut_fixed, bool emitting) {
     const int tid = threadIdx.x;
     for (int i = tid; i < kNB; i += BS) hist[i] = 0;
-    if (tid < kPlace) {
-      S.pl[tid] = 0;
-      S.bcnt[tid] = 0;
-    }
+    if (tid < kPlace) S.bcnt[tid] = 0;
     if (tid == 0) {
       // insertion order of this frame (results never depend on it): bin order when forced, or
       // (auto) after an alpha-bound frame when bin order has been the cheaper one per emitting
@@ -1340,6 +1477,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       if (L.status == WFST_OK) {
         L.layer_base = L.rec_used;
         L.rec_used += n_surv;
+        L.rec_peak = max(L.rec_peak, L.rec_used - L.rec_floor);
         L.rec_phys += n_surv;
         if (L.rec_phys >= p.R_cap) L.rec_phys -= (int32_t)p.R_cap;
         L.n_front = n_surv;
@@ -1393,6 +1531,8 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       L.rec_floor = 0;
       L.layer_floor = 0;
       L.last_alpha = 0;
+      L.gc_layer = -1;
+      L.rec_peak = 0;
       L.status = WFST_OK;
       L.initialized = 1;
       L.front_best = 0.0f;
@@ -1569,7 +1709,9 @@ __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
     mbar_init(saddr(&S.row_mbar), 1);
   }
   __syncthreads();
-  Frame<BS, R, AM> fr(p, S, tab_sa, hist, s_wbuf + (tid & ~31), saddr(s_stage + (tid >> 5) * kStage), saddr(rowmem));
+  static_assert((BS / 32) * kStage * 4 >= kNB, "selection scratch lives in the stage buffers");
+  Frame<BS, R, AM> fr(p, S, tab_sa, hist, s_wbuf + (tid & ~31), saddr(s_stage + (tid >> 5) * kStage), saddr(rowmem),
+                      (int*)s_stage);
   fr.bind_scratch();
   while (true) {
     if (tid == 0) S.item = atomicAdd(p.q_head, 1);

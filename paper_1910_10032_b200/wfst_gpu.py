@@ -48,13 +48,15 @@ class DecoderOpts(C.Structure):
                 ("max_ctas", C.c_int32), ("debug_costs", C.c_int32), ("ctas_per_sm", C.c_int32),
                 ("lattice", C.c_int32), ("lattice_beam", C.c_float), ("lattice_arcs_per_stream", C.c_int64),
                 ("max_active_mode", C.c_int32), ("reclaim", C.c_int32), ("insert_order", C.c_int32),
-                ("bin_capacity", C.c_int32), ("ll_columns", C.c_int32)]
+                ("bin_capacity", C.c_int32), ("ll_columns", C.c_int32),
+                ("gc_frames", C.c_int32)]
 
 
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("frames", "emit_arcs", "eps_arcs", "eps_relax", "candidates", "survivors",
                                          "overflow_inserts", "alpha_frames", "device_bytes", "records_used_max")] + \
-        [("phase_cycles", C.c_int64 * 12), ("select_entries", C.c_int64), ("phase_cycles_alpha", C.c_int64 * 12)]
+        [("phase_cycles", C.c_int64 * 12), ("select_entries", C.c_int64), ("phase_cycles_alpha", C.c_int64 * 12),
+         ("records_per_stream", C.c_int64), ("record_bytes", C.c_int64)]
     PHASES = ("prefetch", "cutoff", "epsilon", "expand_warp", "expand_hub", "overhead", "drain", "bin_insert", "placement",
               "eps_backptr", "table_reset", "row_wait")
 

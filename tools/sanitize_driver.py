@@ -41,6 +41,9 @@ if which in ("all", "c2"):
     run(c2s, 12, 4, 400, 10.0, 300, threads=256, ctas_per_sm=2, table_slots=512, overflow_slots=4096)
 if which in ("all", "lat"):
     run(c2s, 8, 3, 400, 10.0, 300, lattice=1, lattice_beam=6.0)
+if which in ("all", "gc"):   # traceback GC (gc_kernel) with partial results and reclaim
+    run(c2s, 12, 4, 400, 10.0, 300, gc_frames=3)
+    run(c2s, 12, 3, 400, 10.0, 300, gc_frames=4, reclaim=1)
 if which in ("all", "eps") and hasattr(I, "hclg_graph_eps"):
     run(I.hclg_graph_eps(20000, 5.0, 400, seed=6), 12, 4, 400, 10.0, 300)
 print("done", flush=True)
