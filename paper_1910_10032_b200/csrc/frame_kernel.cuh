@@ -42,7 +42,10 @@ constexpr int kThShiftSorted = 7;        // ... every 128 claims in bin-ordered 
 constexpr int kBigCap = 256;
 constexpr int kStage = 32;         // per-warp staging buffer (candidates awaiting insertion)
 constexpr int kPlace = 64;         // coarse cost bins ordering the next frontier (kNB / 16 each)
-constexpr int kSmallClaims = 2048; // frames with at most this many claims use an on-chip claim list
+#ifndef WFST_SMALLCLAIMS
+#define WFST_SMALLCLAIMS 2048
+#endif
+constexpr int kSmallClaims = WFST_SMALLCLAIMS;   // frames with at most this many claims use an on-chip claim list
 
 struct LaneState {
   int32_t status;       // wfst_status, sticky
@@ -250,6 +253,15 @@ __device__ __forceinline__ u64 ldg_volatile64(const u64* p) { return *(const vol
 #endif
 __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+#ifndef WFST_PREFETCH
+#define WFST_PREFETCH 1
+#endif
+// pull a line into L2 ahead of a dependent gather that comes a phase later
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+#if WFST_PREFETCH
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#endif
 }
 __device__ __forceinline__ void red_min_g64(u64* p, u64 v) {
   asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -676,6 +688,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         const uint32_t qf = (uint32_t)e.x | (flag << 31);   // state | has-epsilon flag
         slot = insert(qf, ((u64)o << 32) | qf, claimed, logit, strict, true);
         if (slot >= 0 && logit) red_min_g64(win + slot, ((u64)o << 32) | (uint32_t)e.z);
+        if (claimed && flag) prefetch_l2(p.state_info + (uint32_t)e.x);   // the closure reads it
         if (slot < 0) claimed = false;
       }
     }
@@ -1284,6 +1297,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
           const bool push = strict && has_eps;
           const int wi = warp_append(push, SAI(wlc, rn));
           if (push) {
+            prefetch_l2(p.state_info + (uint32_t)arc.x);   // the next closure iteration reads it
             if (wi < p.FCAP) Wn[wi] = (uint32_t)slot;
             else S.status = WFST_ERR_CAPACITY;
           }
@@ -1394,6 +1408,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         const int32_t arc = (uint32_t)(w[u] >> 32) == (uint32_t)(v[u] >> 32) ? (int32_t)(uint32_t)w[u] : -2;
         if (arc == -2) S.status = WFST_ERR_STATE;
         Fout[pos[u]] = make_int4((int)q, __float_as_int(c), si[u].x, si[u].y - si[u].x);
+        if (si[u].y > si[u].x) prefetch_l2(p.arcs + si[u].x);   // the next frame expands these arcs
         const int64_t r = (int64_t)rp + pos[u] - (rp + pos[u] >= p.R_cap ? p.R_cap : 0);   // record ring
         rec[r] = make_int2(arc, (int)q);
         if (rec_cost) rec_cost[r] = c;
@@ -1647,6 +1662,9 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
 #if WFST_PHASES
     if (tid == 0) t0 = clock64();   // expansion itself is timed by the marks inside expand()
 #endif
+#ifdef WFST_FRAMECYC
+    const long long t_exp = clock64() - t_frame0;
+#endif
 #if WFST_ROWSMEM
     if (tid == 0 && t_next >= 0) row_issue(row_ptr(t_next));   // overlaps the frame's tail
 #endif
@@ -1667,6 +1685,9 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     tick(t0, 1);
     eps_closure();
     tick(t0, 2);
+#ifdef WFST_FRAMECYC
+    const long long t_eps = clock64() - t_frame0;
+#endif
     set_mark();
     contract();
     tick_contract(t0);
@@ -1679,8 +1700,12 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     const bool alpha_frame = S.use_alpha != 0;
     finish_frame(t, true);
 #ifdef WFST_FRAMECYC   // instrumentation build: the frame's SM cycles replace its epsilon-degree count
-    if (tid == 0 && S.L.status == WFST_OK)
-      p.fcounts[((size_t)S.lane * p.TMAX + (S.L.frames - 1) % p.TMAX) * 5 + 4] = clock64() - t_frame0;
+    if (tid == 0 && S.L.status == WFST_OK) {   // (and [1] = cycles to the end of the expansion |
+                                               //  cycles to the end of the epsilon closure << 32)
+      const size_t fi = ((size_t)S.lane * p.TMAX + (S.L.frames - 1) % p.TMAX) * 5;
+      p.fcounts[fi + 4] = clock64() - t_frame0;
+      p.fcounts[fi + 1] = (long long)(((unsigned long long)t_eps << 32) | (unsigned long long)(uint32_t)t_exp);
+    }
 #endif
     tick(t0, 5);
     flush_phases(alpha_frame, (u64)(clock64() - t_frame0));
