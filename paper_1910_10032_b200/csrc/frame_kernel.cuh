@@ -254,15 +254,6 @@ __device__ __forceinline__ u64 ldg_volatile64(const u64* p) { return *(const vol
 __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
-#ifndef WFST_PREFETCH
-#define WFST_PREFETCH 1
-#endif
-// pull a line into L2 ahead of a dependent gather that comes a phase later
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-#if WFST_PREFETCH
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-#endif
-}
 __device__ __forceinline__ void red_min_g64(u64* p, u64 v) {
   asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -688,7 +679,6 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         const uint32_t qf = (uint32_t)e.x | (flag << 31);   // state | has-epsilon flag
         slot = insert(qf, ((u64)o << 32) | qf, claimed, logit, strict, true);
         if (slot >= 0 && logit) red_min_g64(win + slot, ((u64)o << 32) | (uint32_t)e.z);
-        if (claimed && flag) prefetch_l2(p.state_info + (uint32_t)e.x);   // the closure reads it
         if (slot < 0) claimed = false;
       }
     }
@@ -1297,7 +1287,6 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
           const bool push = strict && has_eps;
           const int wi = warp_append(push, SAI(wlc, rn));
           if (push) {
-            prefetch_l2(p.state_info + (uint32_t)arc.x);   // the next closure iteration reads it
             if (wi < p.FCAP) Wn[wi] = (uint32_t)slot;
             else S.status = WFST_ERR_CAPACITY;
           }
@@ -1408,7 +1397,6 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         const int32_t arc = (uint32_t)(w[u] >> 32) == (uint32_t)(v[u] >> 32) ? (int32_t)(uint32_t)w[u] : -2;
         if (arc == -2) S.status = WFST_ERR_STATE;
         Fout[pos[u]] = make_int4((int)q, __float_as_int(c), si[u].x, si[u].y - si[u].x);
-        if (si[u].y > si[u].x) prefetch_l2(p.arcs + si[u].x);   // the next frame expands these arcs
         const int64_t r = (int64_t)rp + pos[u] - (rp + pos[u] >= p.R_cap ? p.R_cap : 0);   // record ring
         rec[r] = make_int2(arc, (int)q);
         if (rec_cost) rec_cost[r] = c;
