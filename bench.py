@@ -315,6 +315,38 @@ def cross_check(W, torch, wl_cfg, preset, graph, G, gathered: dict, world: int, 
     return n_checked, n_bad
 
 
+def launcher_selftest(args):
+    """`--launcher-selftest` (CPU, WFST_DIST_BACKEND=gloo; tests/test_bench_host.py): the multi-rank
+    plumbing of the GPU arm without a GPU -- this process was started by bench's own launcher,
+    takes its share of the config's streams (config_streams), stands in for decoding with a digest
+    of each stream's synthetic inputs (keyed by global id, inputs.loglikes_stream), and goes
+    through the same max-over-ranks reduction and rank-0 result gather as a GPU run.  Rank 0
+    checks that every global stream arrived exactly once with the digest a single process
+    computes, and prints one JSON line."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    c = dict(I.CONFIGS[args.config])
+    ids = config_streams(c, rank, world)
+
+    def digest(sid):
+        row = I.loglikes_stream(c["ll_seed"], sid, 2, 64, None, 1.0, 0.0)
+        return (sid, zlib.crc32(row.tobytes()))
+
+    gathered = gather_results(dist, world, ids, [digest(s) for s in ids])
+    ms, units = reduce_over_ranks(dist, "cpu", 1.0 + rank, float(len(ids))) if world > 1 else (1.0, float(len(ids)))
+    if rank == 0:
+        total = c["streams"] * (world if c.get("scaling") != "strong" else 1)
+        ok = (sorted(gathered) == list(range(total)) and all(gathered[s] == digest(s) for s in gathered)
+              and units == total and ms == float(world))
+        print(json.dumps({"selftest": "launcher", "config": args.config, "world": world, "streams": len(gathered),
+                          "expected_streams": total, "scaling": c.get("scaling", "weak"), "ok": bool(ok)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def gpu_arm(args):
     import torch
     import torch.distributed as dist
@@ -616,6 +648,8 @@ def main(argv=None):
     ap.add_argument("--beam", type=float, default=None, help="override the config's beam (experiments)")
     ap.add_argument("--max-active", dest="max_active", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--launcher-selftest", dest="launcher_selftest", action="store_true",
+                    help="CPU check of the multi-rank launcher, partition and gather (no GPU; tests)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.warmup < 3:
@@ -628,6 +662,8 @@ def main(argv=None):
         # one process per GPU: launch the ranks ourselves (the driver's torchrun sets WORLD_SIZE)
         import torch
         n_dev = torch.cuda.device_count()
+        if args.launcher_selftest:
+            os.environ["WFST_DIST_BACKEND"] = "gloo"   # inherited by the launched ranks
         if args.gpus > n_dev and os.environ.get("WFST_DIST_BACKEND", "nccl") == "nccl":
             sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {n_dev} CUDA device(s) visible\n")
             sys.exit(2)
@@ -636,6 +672,8 @@ def main(argv=None):
             port = so.getsockname()[1]
         argv = sys.argv[1:] if argv is None else list(argv)
         sys.exit(subprocess.call(launcher_cmd(argv, args.gpus, port)))
+    if args.launcher_selftest:
+        return launcher_selftest(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world != args.gpus and int(os.environ.get("RANK", "0")) == 0:
         sys.stderr.write(f"bench.py: --gpus {args.gpus} under a launcher of {world} rank(s): using {world}\n")

@@ -84,3 +84,21 @@ def test_traffic_only_for_this_build(tmp_path, monkeypatch):
     (tmp_path / "paper_1910_10032_b200" / "csrc" / "k.cu").write_text("kernel v2")
     t, src = bench.measured_traffic("c3", "clean")
     assert t is None and "no ncu capture" in src
+
+
+def test_bench_launcher_two_ranks_gloo():
+    """`bench.py --gpus 2` launches its own two ranks (torch.distributed.run, gloo here): C5's
+    4096 streams are split 2048/2048 (strong scaling), C3 is weak-scaled (512 per rank); each
+    rank's stand-in results reach rank 0's gather exactly once, equal to a single process's."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for cfg, n, scaling in (("c5", 4096, "strong"), ("c3", 1024, "weak")):
+        out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--config", cfg,
+                              "--launcher-selftest"], capture_output=True, text=True, timeout=600, cwd=root)
+        assert out.returncode == 0, out.stderr[-2000:]
+        line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+        assert line == {"selftest": "launcher", "config": cfg, "world": 2, "streams": n, "expected_streams": n,
+                        "scaling": scaling, "ok": True}
