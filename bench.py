@@ -527,7 +527,8 @@ def gpu_arm(args):
                      "kernel_ms": round(kmean, 3), "kernel_share_of_step": round(kmean / (ms_max / args.steps), 3),
                      "peak_source": peak_src},
         "counters_per_step": {k: v / args.steps for k, v in st.items()
-                              if k not in ("device_bytes", "records_used_max", "phase_cycles", "phase_cycles_alpha")},
+                              if k not in ("device_bytes", "records_used_max", "phase_cycles", "phase_cycles_alpha",
+                                           "records_per_stream", "record_bytes")},
         # per-phase SM cycles (clock64 marks of thread 0; -DWFST_PHASES=0 builds have none)
         "phase_share": {k: round(v / max(1, sum(st["phase_cycles"].values())), 4) for k, v in st["phase_cycles"].items()}
         if sum(st["phase_cycles"].values()) else None,
