@@ -123,3 +123,36 @@ def test_gc_excludes_lattice(W):
         W.Decoder(G, 2, 10.0, 100, gc_frames=8, lattice=1, lattice_beam=8.0)
     with pytest.raises(W.WfstError):
         W.Decoder(G, 2, 10.0, 100, gc_frames=-1)
+
+
+def test_c5_other_full_size_with_gc(W, torch, oracle_mod):
+    """C5 "other" on ONE GPU (4096 streams, 500 frames, 50-frame chunks, flat posteriors with
+    max-active binding every frame): without traceback GC its records do not fit (some streams
+    never settle); with partial results + reclaim + GC after every chunk it runs
+    to completion, and sampled streams' partial outputs + final tails equal the oracle's paths."""
+    import bench
+    wl = bench.make_workload("c5", "other")
+    T, B, P = wl["T"], wl["B"], wl["P"]
+    G = W.Graph.from_arrays(wl["graph"])
+    D = W.Decoder(G, B, wl["beam"], wl["alpha"], reclaim=1, gc_frames=50)
+    ll = bench.device_loglikes(W, torch, wl, "cuda:0")
+    og = oracle_mod.OracleGraph(wl["graph"])
+    c = wl["c"]
+    sample = (1, 1777, 4094)
+    D.reset()
+    acc = {b: [] for b in range(B)}
+    for t0 in range(0, T, c["chunk"]):
+        D.decode_frames(ll[t0:t0 + c["chunk"]])
+        pp = D.partial_paths(cap=4 * T + 64)
+        for b in sample:
+            acc[b] += pp["arcs"][b].tolist()
+    res = D.best_paths(cap=4 * T + 64)
+    assert res["rc"] == 0
+    st = D.stats()
+    assert st["records_used_max"] < st["records_per_stream"]
+    for b in sample:
+        llh = I.loglikes_stream(c["ll_seed"], b, T, P, wl["planted"][:, b], **wl["preset"])
+        r = og.decode(llh, wl["beam"], wl["alpha"])
+        tail = list(res["arcs"][b, :res["n_arcs"][b]])
+        assert acc[b] + tail == list(r.arcs), b
+        assert res["cost"][b] == r.cost32, b
