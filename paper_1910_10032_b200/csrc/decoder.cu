@@ -354,7 +354,7 @@ cudaError_t launch_gc(wfst_decoder_t d, int32_t B, cudaStream_t st) {
   gp.layer_info = d->kp.layer_info;
   gp.TMAX = d->TMAX;
   gp.settled = d->d_settled;
-  gp.wcap = 53248;   // 208 KB: two (epsilon, emitting) source-set pairs of 4k + 22.5k slots
+  gp.wcap = 53248 / kGcCtas;   // two (epsilon, emitting) source-set pairs in the SM's shared memory
   const size_t smem = (size_t)gp.wcap * 4;
   if (d->gc_smem != smem) {
     cudaError_t e = cudaFuncSetAttribute(gc_kernel<kGcThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -41,7 +41,14 @@ struct GcParams {
   int32_t wcap;             // shared set capacity (slots)
 };
 
-constexpr int kGcThreads = 1024;   // the walk is latency-bound: 1024 threads x 4 records in flight
+#ifndef WFST_GC_THREADS
+#define WFST_GC_THREADS 1024
+#endif
+#ifndef WFST_GC_CTAS
+#define WFST_GC_CTAS 2
+#endif
+constexpr int kGcThreads = WFST_GC_THREADS;   // the walk is latency-bound: many records in flight
+constexpr int kGcCtas = WFST_GC_CTAS;         // resident CTAs (streams) per SM
 constexpr int32_t kLive = (int32_t)0x80000000;
 
 template <int BS>
@@ -75,7 +82,7 @@ __device__ __forceinline__ int gc_block_excl_scan(int v, int* s_w, int& total) {
 }
 
 template <int BS>
-__global__ void __launch_bounds__(BS, 1) gc_kernel(GcParams p) {
+__global__ void __launch_bounds__(BS, kGcCtas) gc_kernel(GcParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* set = (uint32_t*)smem_raw;   // wanted source states
   __shared__ int s_w[33];
@@ -97,7 +104,7 @@ __global__ void __launch_bounds__(BS, 1) gc_kernel(GcParams p) {
   // marks them and puts their own arcs' sources; a pass over layer k-1 marks the states in P.
   // Records are read UNR per thread before any is used (the walk is latency-bound).
   constexpr int UNR = 4;
-  constexpr uint32_t kE = 4096;                        // epsilon-source set (few live tokens are entered by epsilon)
+  constexpr uint32_t kE = kGcCtas > 1 ? 2048 : 4096;  // epsilon-source set (few live tokens are entered by epsilon)
   const uint32_t kP = (uint32_t)p.wcap / 2 - kE;       // emitting-source set
   // two (E, P) pairs: the current layer's sources (looked up) and the next layer's (built)
   uint32_t* Ebuf[2] = {set, set + p.wcap / 2};
