@@ -1270,6 +1270,8 @@ wfst_status wfst_get_lattice(wfst_decoder_t d, int32_t stream, int32_t* seg_n, i
   return WFST_OK;
 }
 
+constexpr int kTraceThreads = 256, kTraceMinBlocks = 6;
+
 wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
                                       int32_t* olabels, int32_t cap, int32_t* n_arcs, int32_t* n_olabels,
                                       int32_t* settled_frames, int32_t* status) {
@@ -1304,6 +1306,7 @@ wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, 
   pp.n_olab_out = p + 2 * n;
   pp.layer_out = p + 3 * n;
   pp.status_out = p + 4 * n;
+  pp.root_out = p + 5 * n;
   pp.arcs_out = p + 6 * n;
   pp.olab_out = pp.arcs_out + (size_t)n * cp;
   // shared memory: a set of wanted source states (1.5 slots per token) + one flag per token
@@ -1311,14 +1314,17 @@ wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, 
   pp.fcap = 16384;
   const size_t smem = (size_t)pp.wcap * 4 + (size_t)pp.fcap;
   if (d->partial_smem != smem) {
-    e = cudaFuncSetAttribute(partial_kernel<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(partial_root_kernel<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "partial kernel attribute");
     d->partial_smem = smem;
   }
   for (int i = 0; i < n; i++) h[i] = streams ? streams[i] : i;
   e = cudaMemcpyAsync(p, h, 4 * (size_t)n, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_fail(e, "ids");
-  partial_kernel<512, 2><<<n, 512, smem, st>>>(pp);
+  // the walk back to the new settle point needs the shared sets (two 512-thread CTAs per SM);
+  // the trace of the newly settled arcs needs none and runs as 256-thread CTAs, several per SM
+  partial_root_kernel<512, 2><<<n, 512, smem, st>>>(pp);
+  partial_trace_kernel<kTraceThreads, kTraceMinBlocks><<<n, kTraceThreads, 0, st>>>(pp);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = mark_work(d, st);   // the kernel may move the lanes' reclaim floors
   if (e == cudaSuccess) e = cudaMemcpyAsync(h, p, 4 * 5 * (size_t)n, cudaMemcpyDeviceToHost, st);

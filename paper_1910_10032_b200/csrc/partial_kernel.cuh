@@ -8,13 +8,19 @@
 // a token r entered by an emitting arc (or the start token): the deepest layer whose survivor
 // paths all pass through one such "root".
 //
-// One CTA per stream walks back from L: S = the layer's tokens on some survivor path (all of
-// layer L at first), closed under epsilon predecessors inside the layer; the roots of S (tokens
-// entered by an emitting arc or the start) are found; one root -> done, else S = the roots'
-// predecessors in the layer below.  Predecessors are found by state: the wanted source states
-// go into a small shared-memory set and the layer's records are scanned against it.  The walk
-// stops at the previous settle point at the latest (all paths pass through it), and only the
-// arcs settled since then are returned -- the stream's output grows incrementally.
+// Two launches per call, one CTA per stream each:
+// * partial_root_kernel walks back from L: S = the layer's tokens on some survivor path (all of
+//   layer L at first), closed under epsilon predecessors inside the layer; the roots of S (tokens
+//   entered by an emitting arc or the start) are found; one root -> done, else S = the roots'
+//   predecessors in the layer below.  Predecessors are found by state: the wanted source states
+//   go into a small shared-memory set and the layer's records are scanned against it.  The walk
+//   stops at the previous settle point at the latest (all paths pass through it).
+// * partial_trace_kernel returns only the arcs settled since the previous call (the stream's
+//   output grows incrementally): from the new root back to the old settle point, one record per
+//   step, each found by a scan of its layer for the arc's source state (a layer holds one token
+//   per state).  It needs no shared tables, so it runs as small CTAs, many per SM: the walk is a
+//   chain of dependent memory round trips, and resident CTAs are what hide them.
+// Every pass over a layer's records issues U loads per thread before using any of them.
 #pragma once
 #include "frame_kernel.cuh"
 
@@ -35,19 +41,21 @@ struct PartialParams {
   int32_t* olab_out;        // [n][cap] their non-zero olabels
   int32_t* n_arcs_out;      // [n]
   int32_t* n_olab_out;      // [n]
-  int32_t* layer_out;       // [n] layer (= frames) of the settle point
+  int32_t* layer_out;       // [n] layer (= frames) of the settle point (root kernel: the root's layer)
   int32_t* status_out;      // [n]
+  int32_t* root_out;        // [n] root kernel -> trace kernel: record index of the new settle point
   int32_t wcap;             // shared set capacity (slots)
   int32_t fcap;             // shared flag capacity (tokens of one layer)
   int32_t reclaim;          // 1: records and layers below the new settle point are released
   LaneState* lanes_rw;      // (same array as lanes_st; written only to move the floors)
 };
 
-__device__ __forceinline__ void pset_put(uint32_t* set, uint32_t cap, uint32_t q) {
+__device__ __forceinline__ bool pset_put(uint32_t* set, uint32_t cap, uint32_t q) {   // true: q is new
   uint32_t b = __umulhi(q * 0x9E3779B1u, cap);
   while (true) {
     const uint32_t old = atomicCAS(set + b, 0xFFFFFFFFu, q);
-    if (old == 0xFFFFFFFFu || old == q) return;
+    if (old == 0xFFFFFFFFu) return true;
+    if (old == q) return false;
     b = (b + 1 == cap) ? 0 : b + 1;
   }
 }
@@ -61,12 +69,56 @@ __device__ __forceinline__ bool pset_has(const uint32_t* set, uint32_t cap, uint
   }
 }
 
+constexpr int kPU = 8;   // record loads in flight per thread in the layer passes
+
+// one walk-back pass over the n records of a layer starting at logical index x0: f(i, rec, arc)
+// for every i with want(i), with the record's arc (arc id >= 0) loaded too; kPU record loads are
+// issued before any is used, then the arc loads
+template <int BS, typename Want, typename Fn>
+__device__ __forceinline__ void layer_pass_arcs(const int4* __restrict__ arcs, const int2* rec, uint32_t R_cap,
+                                                int64_t x0, int n, Want want, Fn f) {
+  for (int i0 = 0; i0 < n; i0 += BS * kPU) {
+    int2 r[kPU];
+    int4 a[kPU];
+#pragma unroll
+    for (int u = 0; u < kPU; u++) {
+      const int i = i0 + u * BS + (int)threadIdx.x;
+      r[u] = i < n && want(i) ? __ldcg(rec + (uint32_t)(x0 + i) % R_cap) : make_int2(-3, -1);
+    }
+#pragma unroll
+    for (int u = 0; u < kPU; u++) a[u] = r[u].x >= 0 ? __ldg(arcs + r[u].x) : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < kPU; u++)
+      if (r[u].x != -3) f(i0 + u * BS + (int)threadIdx.x, r[u], a[u]);
+  }
+}
+
+// f(i, rec) over the records of a layer in batches of BS * kPU (cheapest first), until done()
+// holds after a batch; ends with a barrier, so done()'s inputs can be reset right after
+template <int BS, typename Fn, typename Done>
+__device__ __forceinline__ void layer_scan_until(const int2* rec, uint32_t R_cap, int64_t x0, int n, Fn f, Done done) {
+  for (int i0 = 0; i0 < n; i0 += BS * kPU) {
+    int2 r[kPU];
+#pragma unroll
+    for (int u = 0; u < kPU; u++) {
+      const int i = i0 + u * BS + (int)threadIdx.x;
+      r[u] = i < n ? __ldcg(rec + (uint32_t)(x0 + i) % R_cap) : make_int2(-3, -1);
+    }
+#pragma unroll
+    for (int u = 0; u < kPU; u++)
+      if (r[u].x != -3) f(i0 + u * BS + (int)threadIdx.x, r[u]);
+    __syncthreads();
+    if (done()) break;
+  }
+  __syncthreads();
+}
+
 template <int BS, int MINB>
-__global__ void __launch_bounds__(BS, MINB) partial_kernel(PartialParams p) {
+__global__ void __launch_bounds__(BS, MINB) partial_root_kernel(PartialParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* set = (uint32_t*)smem_raw;                       // wanted source states
   unsigned char* flag = (unsigned char*)(set + p.wcap);      // tokens of the current layer in S
-  __shared__ int s_changed, s_roots, s_root, s_status, s_len, s_idx, s_arc, s_layer, s_nw, s_nflag;
+  __shared__ int s_changed[2], s_roots, s_root, s_status, s_nflag, s_nwant, s_found, s_hi;
   // the wanted-state set is sized to what can be wanted (1.5x the tokens flagged), so that
   // clearing it costs O(flagged tokens), not O(capacity), per step
   auto set_cap = [&](int n) { return (uint32_t)min(p.wcap, max(64, n + n / 2 + 1)); };   // load <= 2/3
@@ -75,75 +127,81 @@ __global__ void __launch_bounds__(BS, MINB) partial_kernel(PartialParams p) {
   const LaneState* Lp = p.lanes_st + ln;
   const int Lcur = __ldcg(&Lp->frames);
   const int2* rec = p.rec + (size_t)ln * p.R_cap;
+  const uint32_t Rc = (uint32_t)p.R_cap;   // record ring (32-bit: R_cap < 2^31)
   const int2* linfo_base = p.layer_info + (size_t)ln * (p.TMAX + 1);
   auto linfo_at = [&](int k) { return linfo_base[k % (p.TMAX + 1)]; };   // layer index ring
-  auto R = [&](int64_t i) { return (uint32_t)i % (uint32_t)p.R_cap; };   // record ring (32-bit: R_cap < 2^31)
   const int2 prev = p.settled[ln];
   if (tid == 0) {
     s_status = __ldcg(&Lp->status) != WFST_OK ? __ldcg(&Lp->status)
                : !__ldcg(&Lp->initialized)    ? WFST_ERR_STATE
                : Lcur - __ldcg(&Lp->layer_floor) > p.TMAX ? WFST_ERR_CAPACITY
                                               : WFST_OK;
-    s_len = 0;
+    s_changed[0] = s_changed[1] = 0;
   }
   __syncthreads();
-  auto finish = [&](int n_arcs, int layer) {
+  auto finish = [&](int status, int root, int layer) {
     if (tid == 0) {
-      p.status_out[blockIdx.x] = s_status;
-      p.n_arcs_out[blockIdx.x] = n_arcs;
+      p.status_out[blockIdx.x] = status;
+      p.root_out[blockIdx.x] = root;
       p.layer_out[blockIdx.x] = layer;
     }
   };
   if (s_status != WFST_OK) {
-    if (tid == 0) p.n_olab_out[blockIdx.x] = 0;
-    finish(0, prev.x < 0 ? 0 : prev.x);
+    finish(s_status, -1, prev.x < 0 ? 0 : prev.x);
     return;
   }
   // ---- walk back from the current layer to the deepest single root
   int k = Lcur;
   int2 Lk = linfo_at(k);
   if (Lk.y > p.fcap) {
-    if (tid == 0) {
-      s_status = WFST_ERR_CAPACITY;
-      p.n_olab_out[blockIdx.x] = 0;
-    }
-    __syncthreads();
-    finish(0, 0);
+    finish(WFST_ERR_CAPACITY, -1, prev.x < 0 ? 0 : prev.x);
     return;
   }
   for (int i = tid; i < Lk.y; i += BS) flag[i] = 1;
-  if (tid == 0) s_nflag = Lk.y;
+  if (tid == 0) {
+    s_nflag = Lk.y;
+    s_hi = Lk.y;
+  }
   __syncthreads();
   int root = -1;   // record index of the settle point
+  int par = 0;     // s_changed[par]: this epsilon pass; the other one is cleared for the next
+  // Tokens on survivor paths are cheap and the layers are stored cheapest bins first, so past
+  // the first layer the flagged tokens sit near the front: passes over flagged tokens stop at
+  // s_hi (one past the last flagged index), and a search for a known number of wanted states
+  // stops once all are found.
   while (true) {
     // epsilon predecessors inside layer k (chains are short; repeat until nothing new)
     while (true) {
       const uint32_t wc = set_cap(s_nflag);
       for (uint32_t i = tid; i < wc; i += BS) set[i] = 0xFFFFFFFFu;
       if (tid == 0) {
-        s_changed = 0;
-        s_nw = 0;
+        s_nwant = 0;
+        s_found = 0;
       }
       __syncthreads();
-      for (int i = tid; i < Lk.y; i += BS) {
-        if (!flag[i]) continue;
-        const int a = __ldcg(&rec[R((int64_t)Lk.x + i)].x);
-        if (a >= 0 && __ldg(&p.arcs[a].z) < 0) {
-          pset_put(set, wc, (uint32_t)(__ldg(&p.arcs[a].w) & 0x7FFFFFFF));
-          s_nw = 1;
-        }
-      }
+      // s_changed[par ^ 1] was last read at the end of the previous pass: every thread is past it
+      if (tid == 0) s_changed[par ^ 1] = 0;
+      const int hi = s_hi;
+      layer_pass_arcs<BS>(p.arcs, rec, Rc, Lk.x, hi, [&](int i) { return flag[i] != 0; }, [&](int, int2 r, int4 a) {
+        if (r.x >= 0 && a.z < 0 && pset_put(set, wc, (uint32_t)(a.w & 0x7FFFFFFF))) atomicAdd(&s_nwant, 1);
+      });
       __syncthreads();
-      if (!s_nw) break;
-      for (int i = tid; i < Lk.y; i += BS)
-        if (!flag[i] && pset_has(set, wc, (uint32_t)__ldcg(&rec[R((int64_t)Lk.x + i)].y))) {
-          flag[i] = 1;
-          s_changed = 1;
-          atomicAdd(&s_nflag, 1);
+      const int nwant = s_nwant;
+      if (nwant == 0) break;
+      // every wanted source is a token of this layer (flagged or not): stop when all are seen
+      layer_scan_until<BS>(rec, Rc, Lk.x, Lk.y, [&](int i, int2 r) {
+        if (pset_has(set, wc, (uint32_t)r.y)) {
+          atomicAdd(&s_found, 1);
+          if (!flag[i]) {
+            flag[i] = 1;
+            s_changed[par] = 1;
+            atomicAdd(&s_nflag, 1);
+            atomicMax(&s_hi, i + 1);
+          }
         }
-      __syncthreads();
-      const bool more = s_changed != 0;
-      __syncthreads();   // read by every thread before thread 0 clears it for the next pass
+      }, [&]() { return s_found >= nwant; });
+      const bool more = s_changed[par] != 0;
+      par ^= 1;
       if (!more) break;
     }
     // roots: tokens of S entered by an emitting arc or the start
@@ -152,111 +210,193 @@ __global__ void __launch_bounds__(BS, MINB) partial_kernel(PartialParams p) {
       s_root = -1;
     }
     __syncthreads();
-    for (int i = tid; i < Lk.y; i += BS) {
-      if (!flag[i]) continue;
-      const int a = __ldcg(&rec[R((int64_t)Lk.x + i)].x);
-      if (a < 0 || __ldg(&p.arcs[a].z) >= 0) {
+    const int hi = s_hi;
+    layer_pass_arcs<BS>(p.arcs, rec, Rc, Lk.x, hi, [&](int i) { return flag[i] != 0; }, [&](int i, int2 r, int4 a) {
+      if (r.x < 0 || a.z >= 0) {
         atomicAdd(&s_roots, 1);
         atomicMax(&s_root, Lk.x + i);   // used only when there is exactly one root
       }
-    }
+    });
     __syncthreads();
-    if (s_roots == 1 || k == 0 || (prev.x >= 0 && k <= prev.x)) {
-      root = s_roots == 1 ? s_root : -2;
+    const int n_roots = s_roots;
+    if (n_roots == 1 || k == 0 || (prev.x >= 0 && k <= prev.x)) {
+      root = n_roots == 1 ? s_root : -2;
       break;
     }
     // predecessors of the roots in layer k-1
-    const uint32_t wc = set_cap(s_roots);
+    const uint32_t wc = set_cap(n_roots);
     for (uint32_t i = tid; i < wc; i += BS) set[i] = 0xFFFFFFFFu;
-    if (tid == 0) s_nflag = 0;
+    if (tid == 0) s_nwant = 0;
     __syncthreads();
-    for (int i = tid; i < Lk.y; i += BS) {
-      if (!flag[i]) continue;
-      const int a = __ldcg(&rec[R((int64_t)Lk.x + i)].x);
-      if (a >= 0 && __ldg(&p.arcs[a].z) >= 0)
-        pset_put(set, wc, (uint32_t)(__ldg(&p.arcs[a].w) & 0x7FFFFFFF));
-    }
-    __syncthreads();
+    layer_pass_arcs<BS>(p.arcs, rec, Rc, Lk.x, hi, [&](int i) { return flag[i] != 0; }, [&](int, int2 r, int4 a) {
+      if (r.x >= 0 && a.z >= 0 && pset_put(set, wc, (uint32_t)(a.w & 0x7FFFFFFF))) atomicAdd(&s_nwant, 1);
+    });
+    __syncthreads();   // flags of layer k read: layer k-1's may be written
     k--;
     Lk = linfo_at(k);
     if (Lk.y > p.fcap) {
       if (tid == 0) s_status = WFST_ERR_CAPACITY;
       break;
     }
-    for (int i = tid; i < Lk.y; i += BS) {
-      const bool f = pset_has(set, wc, (uint32_t)__ldcg(&rec[R((int64_t)Lk.x + i)].y));
-      flag[i] = f;
-      if (f) atomicAdd(&s_nflag, 1);
+    for (int i = tid; i < Lk.y; i += BS) flag[i] = 0;
+    if (tid == 0) {
+      s_nflag = 0;
+      s_hi = 0;
+      s_found = 0;
     }
     __syncthreads();
+    const int nwant = s_nwant;
+    layer_scan_until<BS>(rec, Rc, Lk.x, Lk.y, [&](int i, int2 r) {
+      if (pset_has(set, wc, (uint32_t)r.y)) {
+        flag[i] = 1;
+        atomicAdd(&s_found, 1);
+        atomicAdd(&s_nflag, 1);
+        atomicMax(&s_hi, i + 1);
+      }
+    }, [&]() { return s_found >= nwant; });
   }
   __syncthreads();
-  if (s_status != WFST_OK || root == -2) {   // (-2: the walk met the old settle point unresolved)
+  if (s_status != WFST_OK || root == -2)   // (-2: the walk met the old settle point unresolved)
+    finish(s_status != WFST_OK ? s_status : WFST_ERR_STATE, -1, prev.x < 0 ? 0 : prev.x);
+  else
+    finish(WFST_OK, root, k);
+}
+
+// block-wide exclusive prefix sum of 0/1 flags (all threads call it); returns the total
+template <int BS>
+__device__ __forceinline__ int block_excl_scan01(bool f, int& excl, int* s_w) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned m = __ballot_sync(0xffffffffu, f);
+  if (lane == 0) s_w[w] = __popc(m);
+  __syncthreads();
+  int base = 0, tot = 0;
+#pragma unroll
+  for (int j = 0; j < BS / 32; j++) {
+    const int c = s_w[j];
+    base += j < w ? c : 0;
+    tot += c;
+  }
+  excl = base + __popc(m & ((1u << lane) - 1u));
+  __syncthreads();
+  return tot;
+}
+
+constexpr int kTraceSmem = 2048;   // settled arcs kept on chip per call (longer: serial fallback)
+
+template <int BS, int MINB>
+__global__ void __launch_bounds__(BS, MINB) partial_trace_kernel(PartialParams p) {
+  __shared__ int s_idx[3], s_arc[3], s_src[3], s_emit[3];
+  __shared__ int s_path[kTraceSmem];
+  __shared__ int s_w[BS / 32];
+  const int tid = threadIdx.x;
+  const int ln = p.lanes[blockIdx.x];
+  const int2* rec = p.rec + (size_t)ln * p.R_cap;
+  const uint32_t Rc = (uint32_t)p.R_cap;
+  const int2* linfo_base = p.layer_info + (size_t)ln * (p.TMAX + 1);
+  const int2 prev = p.settled[ln];
+  const int root = p.root_out[blockIdx.x];
+  int status = p.status_out[blockIdx.x];
+  const int k = p.layer_out[blockIdx.x];
+  int32_t* out = p.arcs_out + (size_t)blockIdx.x * p.cap;
+  if (status != WFST_OK) {   // the root kernel wrote the status and the old settle layer
     if (tid == 0) {
-      if (s_status == WFST_OK) s_status = WFST_ERR_STATE;
+      p.n_arcs_out[blockIdx.x] = 0;
       p.n_olab_out[blockIdx.x] = 0;
     }
-    __syncthreads();
-    finish(0, prev.x < 0 ? 0 : prev.x);
     return;
   }
-  // ---- arcs from the old settle point to the new one (traceback walk, layer scans)
+  // ---- arcs from the new settle point back to the old one.  Step j reads slot j%3 (the record
+  // found by step j-1: index, arc, the arc's source state and kind), its scan fills slot
+  // (j+1)%3, and thread 0 clears slot (j+2)%3, last read in step j-1: one barrier per step.
   const int stop = prev.x < 0 ? -1 : prev.y;   // record index of the old settle point
-  int32_t* out = p.arcs_out + (size_t)blockIdx.x * p.cap;
+  auto load_step = [&](int slot, int idx, int2 r) {   // (one thread: the record's finder)
+    s_idx[slot] = idx;
+    s_arc[slot] = r.x;
+    if (r.x >= 0) {
+      const int4 a = __ldg(&p.arcs[r.x]);
+      s_src[slot] = a.w & 0x7FFFFFFF;
+      s_emit[slot] = a.z >= 0;
+    }
+  };
   if (tid == 0) {
-    s_idx = root;
-    s_layer = k;
+    load_step(0, root, __ldcg(rec + (uint32_t)root % Rc));
+    s_idx[1] = -1;
   }
   __syncthreads();
+  int len = 0, layer = k, j = 0;
   while (true) {
-    const int idx = s_idx;
-    if (idx == stop) break;
-    const int arc = __ldcg(&rec[R(idx)].x);
-    if (arc < 0) break;   // the start token
-    __syncthreads();
-    if (tid == 0) {
-      if (s_len < p.cap) out[s_len] = arc;
-      s_len++;
-      s_arc = __ldg(&p.arcs[arc].w) & 0x7FFFFFFF;   // source state
-      if (__ldg(&p.arcs[arc].z) >= 0) s_layer--;
-      s_idx = -1;
-    }
-    __syncthreads();
-    const int2 info = linfo_at(s_layer);
-    const int want = s_arc;
-    for (int i = tid; i < info.y; i += BS)
-      if (__ldcg(&rec[R((int64_t)info.x + i)].y) == want) s_idx = info.x + i;
-    __syncthreads();
-    if (s_idx < 0) {
-      if (tid == 0) s_status = WFST_ERR_STATE;
+    const int cur = j % 3, nxt = (j + 1) % 3;
+    const int idx = s_idx[cur], arc = s_arc[cur];
+    if (idx < 0) {   // the previous scan found no record of the source state
+      status = WFST_ERR_STATE;
       break;
     }
+    if (idx == stop || arc < 0) break;   // the old settle point / the start token
+    if (tid == 0) {
+      if (len < p.cap) out[len] = arc;
+      if (len < kTraceSmem) s_path[len] = arc;
+      s_idx[(j + 2) % 3] = -1;
+    }
+    len++;
+    layer -= s_emit[cur];
+    const int want = s_src[cur];
+    const int2 info = linfo_base[layer % (p.TMAX + 1)];
+    // the path's tokens are cheap and a layer is stored cheapest bins first: the scan usually
+    // ends in its first batch (the barrier after each batch is the step's barrier)
+    int i0 = 0;
+    do {
+      int2 r[kPU];
+#pragma unroll
+      for (int u = 0; u < kPU; u++) {
+        const int i = i0 + u * BS + tid;
+        r[u] = i < info.y ? __ldcg(rec + (uint32_t)((int64_t)info.x + i) % Rc) : make_int2(-3, -1);
+      }
+#pragma unroll
+      for (int u = 0; u < kPU; u++)
+        if (r[u].y == want && r[u].x != -3) load_step(nxt, info.x + i0 + u * BS + tid, r[u]);
+      __syncthreads();
+      i0 += BS * kPU;
+    } while (i0 < info.y && s_idx[nxt] < 0);
+    j++;
   }
   __syncthreads();
-  if (tid == 0) {
-    const int m = min(s_len, p.cap);
+  // ---- reverse into path order, gather the non-zero olabels (in parallel when on chip)
+  const int m = min(len, p.cap);
+  int nol = 0;
+  if (m <= kTraceSmem) {
+    for (int x = tid; x < m; x += BS) out[x] = s_path[m - 1 - x];
+    for (int x0 = 0; x0 < m; x0 += BS) {
+      const int x = x0 + tid;
+      const int32_t ol = x < m ? __ldg(p.olabel + s_path[m - 1 - x]) : 0;
+      int e = 0;
+      const int tot = block_excl_scan01<BS>(ol != 0, e, s_w);
+      if (ol != 0) p.olab_out[(size_t)blockIdx.x * p.cap + nol + e] = ol;
+      nol += tot;
+    }
+  } else if (tid == 0) {   // serial fallback (more than kTraceSmem arcs settled in one call)
     for (int x = 0; x < m / 2; x++) {
       const int32_t t = out[x];
       out[x] = out[m - 1 - x];
       out[m - 1 - x] = t;
     }
-    int nol = 0;
     for (int x = 0; x < m; x++) {
       const int32_t ol = __ldg(p.olabel + out[x]);
       if (ol != 0) p.olab_out[(size_t)blockIdx.x * p.cap + nol++] = ol;
     }
+  }
+  if (tid == 0) {
     p.n_olab_out[blockIdx.x] = nol;
-    if (s_status == WFST_OK && s_len <= p.cap) {
+    if (status == WFST_OK && len <= p.cap) {
       p.settled[ln] = make_int2(k, root);
       if (p.reclaim) {   // traceback GC: everything below the settle point is handed out
-        p.lanes_rw[ln].rec_floor = linfo_at(k).x;
+        p.lanes_rw[ln].rec_floor = linfo_base[k % (p.TMAX + 1)].x;
         p.lanes_rw[ln].layer_floor = k;
       }
     }
-    if (s_status == WFST_OK && s_len > p.cap) s_status = WFST_ERR_INVALID_ARG;
+    if (status == WFST_OK && len > p.cap) status = WFST_ERR_INVALID_ARG;
+    p.status_out[blockIdx.x] = status;
+    p.n_arcs_out[blockIdx.x] = len;
   }
-  __syncthreads();
-  finish(s_len, k);
 }
 
 }  // namespace wfst_dev

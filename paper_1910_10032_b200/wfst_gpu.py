@@ -166,6 +166,30 @@ def _ids(streams):
 
 
 # ------------------------------------------------------------------ host-only helpers
+class _Rows:
+    """Sequence of per-stream row views rows[i, :n[i]] of a result matrix, built on access (a
+    4096-stream result costs no per-stream Python work unless the rows are read)."""
+    __slots__ = ("_a", "_n")
+
+    def __init__(self, a, n):
+        self._a, self._n = a, n
+
+    def __len__(self):
+        return len(self._n)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        return self._a[i, :self._n[i]]
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+
 def eq1_bytes(n_states, n_arcs, n_emitting) -> int:
     """Eq. 1 (P:113): 12|Q| + 8|E| + 4|E_E|."""
     return int(lib().wfst_eq1_bytes(n_states, n_arcs, n_emitting))
@@ -361,9 +385,8 @@ class Decoder:
         status = np.zeros(n, np.int32)
         rc = lib().wfst_get_partial_paths_ex(self.h, _ptr(ids), n, _ptr(arcs), _ptr(ols), cap, _ptr(nar), _ptr(nol),
                                              _ptr(fr), _ptr(status))
-        if rc == 0:   # views into this call's fresh buffers (no per-stream copies: this runs every chunk)
-            return dict(arcs=[arcs[i, :nar[i]] for i in range(n)], olabels=[ols[i, :nol[i]] for i in range(n)],
-                        settled_frames=fr, status=status)
+        if rc == 0:   # row views into this call's fresh buffers, made on access (this runs every chunk)
+            return dict(arcs=_Rows(arcs, nar), olabels=_Rows(ols, nol), settled_frames=fr, status=status)
         # per stream: OK streams advanced their settle point (their arcs must not be dropped);
         # streams whose new arcs exceeded cap kept theirs and are fetched again with a larger cap
         big = (status == 1) & (nar > cap)

@@ -20,3 +20,19 @@ def oracle_mod():
     import oracle
     oracle.build()
     return oracle
+
+
+@pytest.fixture(autouse=True)
+def _release_gpu_memory(request):
+    """After every GPU test: drop its decoders/graphs and torch's cached blocks, so that the next
+    test's default record arena (sized from the free device memory at decoder creation) does not
+    depend on what earlier tests left behind (a full-size C5 run caches ~47 GB of posteriors)."""
+    yield
+    if request.node.get_closest_marker("gpu") is None:
+        return
+    import gc
+    gc.collect()
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_available():
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()

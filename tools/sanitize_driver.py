@@ -31,6 +31,18 @@ def run(g, T, B, P, beam, alpha, preset="clean", **opts):
     print("ok", g.n_states, B, T, int(res["rc"]), flush=True)
 
 
+def run_chunks(g, T, B, P, beam, alpha, chunk, **opts):   # partial results after every chunk
+    pl = I.planted_walks(g, B, T, seed=5)
+    ll = torch.from_numpy(I.loglikes(6, range(B), T, P, pl, **I.preset("clean"))).cuda()
+    D = W.Decoder(W.Graph.from_arrays(g), B, beam, alpha, **opts)
+    D.reset()
+    for t0 in range(0, T, chunk):
+        D.decode_frames(ll[t0:t0 + chunk].contiguous())
+        D.partial_paths(cap=8)   # small cap: the over-capacity path too
+    D.sync()
+    print("ok chunks", g.n_states, B, T, flush=True)
+
+
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 c1 = I.c1_graph()
 c2s = I.hclg_graph(20000, 6.0, 400, seed=2)
@@ -44,6 +56,9 @@ if which in ("all", "lat"):
 if which in ("all", "gc"):   # traceback GC (gc_kernel) with partial results and reclaim
     run(c2s, 12, 4, 400, 10.0, 300, gc_frames=3)
     run(c2s, 12, 3, 400, 10.0, 300, gc_frames=4, reclaim=1)
+if which in ("all", "partial"):
+    run_chunks(c2s, 24, 5, 400, 10.0, 300, 4)
+    run_chunks(c2s, 24, 3, 400, 10.0, 300, 5, reclaim=1)
 if which in ("all", "eps") and hasattr(I, "hclg_graph_eps"):
     run(I.hclg_graph_eps(20000, 5.0, 400, seed=6), 12, 4, 400, 10.0, 300)
 print("done", flush=True)
