@@ -283,6 +283,18 @@ wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, 
                                       int32_t* olabels, int32_t cap, int32_t* n_arcs, int32_t* n_olabels,
                                       int32_t* settled_frames, int32_t* status);
 
+/* Same results, packed: stream i's new arcs are arcs[offsets[i] .. offsets[i] + min(n_arcs[i],
+ * cap)) and its olabels olabels[offsets[i] .. + n_olabels[i]) (the streams' ranges do not
+ * overlap; their order in the buffers is unspecified).  arcs/olabels: host, total_cap entries
+ * each (nullable); total_cap must be >= n * cap (INVALID_ARG before any work otherwise), cap is
+ * the per-stream limit as above; *total: entries used.  Only the used entries are copied and
+ * written, so an online caller pays for the arcs that settled, not for n * cap (a fresh n * cap
+ * host buffer is touched only where arcs land).  Other arguments as wfst_get_partial_paths_ex. */
+wfst_status wfst_get_partial_paths_packed(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
+                                          int32_t* olabels, int64_t total_cap, int32_t cap, int64_t* offsets,
+                                          int64_t* total, int32_t* n_arcs, int32_t* n_olabels,
+                                          int32_t* settled_frames, int32_t* status);
+
 /* ---- lattice (row f1 of SURVEY §8, NEXT) ----------------
  * With opts.lattice = 1 every reset and decode call also builds, per stream and frame, the lattice
  * segment of that frame (one extra launch after the frame kernel, same CUDA stream): every arc

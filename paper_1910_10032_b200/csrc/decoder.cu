@@ -1272,10 +1272,19 @@ wfst_status wfst_get_lattice(wfst_decoder_t d, int32_t stream, int32_t* seg_n, i
 
 constexpr int kTraceThreads = 256, kTraceMinBlocks = 6;
 
-wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
-                                      int32_t* olabels, int32_t cap, int32_t* n_arcs, int32_t* n_olabels,
-                                      int32_t* settled_frames, int32_t* status) {
+wfst_status wfst_get_partial_paths_packed(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
+                                          int32_t* olabels, int64_t total_cap, int32_t cap, int64_t* offsets,
+                                          int64_t* total_out, int32_t* n_arcs, int32_t* n_olabels,
+                                          int32_t* settled_frames, int32_t* status) {
   if (!d || n < 0 || !n_arcs || !settled_frames || cap < 0) return fail(WFST_ERR_INVALID_ARG, "bad argument");
+  if ((arcs || olabels) && (!offsets || total_cap < (int64_t)n * cap))
+    return fail(WFST_ERR_INVALID_ARG, "packed partial paths: offsets needed and total_cap >= n * cap");
+  if (total_out) *total_out = 0;
+  for (int i = 0; i < n; i++) {   // (a call that fails before the results reports nothing)
+    n_arcs[i] = 0;
+    if (n_olabels) n_olabels[i] = 0;
+    if (offsets) offsets[i] = 0;
+  }
   if (n == 0) return WFST_OK;
   DeviceGuard dg(d->device);
   for (int i = 0; i < n; i++) {
@@ -1284,7 +1293,7 @@ wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, 
     if (!d->h_initialized[s]) return fail(WFST_ERR_STATE, "stream " + std::to_string(s) + " not reset");
   }
   const int cp = std::max(cap, 1);
-  cudaError_t e = ensure_path(d, (size_t)n * (6 + 2 * (size_t)cp));
+  cudaError_t e = ensure_path(d, (size_t)n * (6 + 3 * (size_t)cp) + 1);
   if (e != cudaSuccess) return cuda_fail(e, "path buffer");
   cudaStream_t st = d->work_stream;   // after the decoder's last decode, on its stream
   int32_t* p = d->d_path;
@@ -1308,7 +1317,9 @@ wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, 
   pp.status_out = p + 4 * n;
   pp.root_out = p + 5 * n;
   pp.arcs_out = p + 6 * n;
-  pp.olab_out = pp.arcs_out + (size_t)n * cp;
+  pp.packed_arcs = pp.arcs_out + (size_t)n * cp;
+  pp.packed_olab = pp.packed_arcs + (size_t)n * cp;
+  pp.packed_count = pp.packed_olab + (size_t)n * cp;
   // shared memory: a set of wanted source states (1.5 slots per token) + one flag per token
   pp.wcap = 24576;   // 1.5 x fcap: two 512-thread CTAs per SM fit in shared memory
   pp.fcap = 16384;
@@ -1320,6 +1331,7 @@ wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, 
   }
   for (int i = 0; i < n; i++) h[i] = streams ? streams[i] : i;
   e = cudaMemcpyAsync(p, h, 4 * (size_t)n, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(pp.packed_count, 0, 4, st);
   if (e != cudaSuccess) return cuda_fail(e, "ids");
   // the walk back to the new settle point needs the shared sets (two 512-thread CTAs per SM);
   // the trace of the newly settled arcs needs none and runs as 256-thread CTAs, several per SM
@@ -1327,28 +1339,23 @@ wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, 
   partial_trace_kernel<kTraceThreads, kTraceMinBlocks><<<n, kTraceThreads, 0, st>>>(pp);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = mark_work(d, st);   // the kernel may move the lanes' reclaim floors
-  if (e == cudaSuccess) e = cudaMemcpyAsync(h, p, 4 * 5 * (size_t)n, cudaMemcpyDeviceToHost, st);
+  // per stream {n_arcs, n_olabels, settled layer, status, packed offset} and the packed total
+  const size_t hp_tot = 6 * (size_t)n + 3 * (size_t)n * cp;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h + n, p + n, 4 * 5 * (size_t)n, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h + hp_tot, pp.packed_count, 4, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "partial kernel");
-  // copy only the columns some stream used (a few frames' worth of arcs per call, not cap)
-  int mx_a = 0, mx_o = 0;
-  for (int i = 0; i < n; i++) {
-    mx_a = std::max(mx_a, std::min(h[n + i], cp));
-    mx_o = std::max(mx_o, std::min(h[2 * n + i], cp));
-  }
-  const size_t pitch = 4 * (size_t)cp;
-  int32_t* h_arcs = h + 6 * n;
-  int32_t* h_ol = h_arcs + (size_t)n * cp;
-  if (arcs && cap > 0 && mx_a > 0)
-    e = cudaMemcpy2DAsync(h_arcs, pitch, pp.arcs_out, pitch, 4 * (size_t)mx_a, n, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess && olabels && cap > 0 && mx_o > 0)
-    e = cudaMemcpy2DAsync(h_ol, pitch, pp.olab_out, pitch, 4 * (size_t)mx_o, n, cudaMemcpyDeviceToHost, st);
+  const size_t total = (size_t)h[hp_tot];
+  if (total_out) *total_out = (int64_t)total;
+  // straight into the caller's buffers (pageable memory is staged by the driver)
+  if (total > 0 && arcs && cap > 0)
+    e = cudaMemcpyAsync(arcs, pp.packed_arcs, 4 * total, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && total > 0 && olabels && cap > 0)
+    e = cudaMemcpyAsync(olabels, pp.packed_olab, 4 * total, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "partial D2H");
-  if (arcs && cap > 0 && mx_a > 0)
-    for (int i = 0; i < n; i++) memcpy(arcs + (size_t)i * cp, h_arcs + (size_t)i * cp, 4 * (size_t)mx_a);
-  if (olabels && cap > 0 && mx_o > 0)
-    for (int i = 0; i < n; i++) memcpy(olabels + (size_t)i * cp, h_ol + (size_t)i * cp, 4 * (size_t)mx_o);
+  if (offsets)
+    for (int i = 0; i < n; i++) offsets[i] = h[5 * n + i];
   wfst_status first = WFST_OK;
   for (int i = 0; i < n; i++) {
     n_arcs[i] = h[n + i];
@@ -1362,6 +1369,27 @@ wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, 
     }
   }
   return first;
+}
+
+wfst_status wfst_get_partial_paths_ex(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,
+                                      int32_t* olabels, int32_t cap, int32_t* n_arcs, int32_t* n_olabels,
+                                      int32_t* settled_frames, int32_t* status) {
+  if (!d || n < 0 || !n_arcs || !settled_frames || cap < 0) return fail(WFST_ERR_INVALID_ARG, "bad argument");
+  // the packed call, then each stream's range into its row
+  const size_t tc = (size_t)n * (size_t)std::max(cap, 0);
+  std::vector<int32_t> pa(arcs && cap > 0 ? tc : 0), po(olabels && cap > 0 ? tc : 0);
+  std::vector<int64_t> off(n);
+  std::vector<int32_t> nol(n);
+  wfst_status r = wfst_get_partial_paths_packed(d, streams, n, pa.empty() ? nullptr : pa.data(),
+                                                po.empty() ? nullptr : po.data(), (int64_t)tc, cap, off.data(),
+                                                nullptr, n_arcs, nol.data(), settled_frames, status);
+  for (int i = 0; i < n; i++) {
+    if (n_olabels) n_olabels[i] = nol[i];
+    const int na = std::max(0, std::min(n_arcs[i], cap)), no = std::max(0, std::min(nol[i], cap));
+    if (!pa.empty() && na) memcpy(arcs + (size_t)i * cap, pa.data() + off[i], 4 * (size_t)na);
+    if (!po.empty() && no) memcpy(olabels + (size_t)i * cap, po.data() + off[i], 4 * (size_t)no);
+  }
+  return r;
 }
 
 wfst_status wfst_get_partial_paths(wfst_decoder_t d, const int32_t* streams, int32_t n, int32_t* arcs,

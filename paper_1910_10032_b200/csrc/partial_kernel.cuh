@@ -37,13 +37,16 @@ struct PartialParams {
   int32_t TMAX;
   int2* settled;            // [lane] {layer, record index} of the last settle point (-1: start)
   int32_t cap;              // per-stream output capacity (arcs)
-  int32_t* arcs_out;        // [n][cap] newly settled arcs, in order
-  int32_t* olab_out;        // [n][cap] their non-zero olabels
+  int32_t* arcs_out;        // [n][cap] scratch rows (the walk's arcs when they do not fit on chip)
+  int32_t* packed_arcs;     // newly settled arcs, in order, stream after stream at root_out[b]
+  int32_t* packed_olab;     // their non-zero olabels, at the same offsets
+  int32_t* packed_count;    // arcs packed so far (zeroed before the launch)
   int32_t* n_arcs_out;      // [n]
   int32_t* n_olab_out;      // [n]
   int32_t* layer_out;       // [n] layer (= frames) of the settle point (root kernel: the root's layer)
   int32_t* status_out;      // [n]
-  int32_t* root_out;        // [n] root kernel -> trace kernel: record index of the new settle point
+  int32_t* root_out;        // [n] root kernel -> trace kernel: record index of the new settle point;
+                            //     trace kernel -> host: the stream's offset in the packed outputs
   int32_t wcap;             // shared set capacity (slots)
   int32_t fcap;             // shared flag capacity (tokens of one layer)
   int32_t reclaim;          // 1: records and layers below the new settle point are released
@@ -77,13 +80,15 @@ constexpr int kPU = 8;   // record loads in flight per thread in the layer passe
 template <int BS, typename Want, typename Fn>
 __device__ __forceinline__ void layer_pass_arcs(const int4* __restrict__ arcs, const int2* rec, uint32_t R_cap,
                                                 int64_t x0, int n, Want want, Fn f) {
+  const uint32_t b0 = (uint32_t)(x0 % R_cap);   // the layer's first record in the ring
   for (int i0 = 0; i0 < n; i0 += BS * kPU) {
     int2 r[kPU];
     int4 a[kPU];
 #pragma unroll
     for (int u = 0; u < kPU; u++) {
       const int i = i0 + u * BS + (int)threadIdx.x;
-      r[u] = i < n && want(i) ? __ldcg(rec + (uint32_t)(x0 + i) % R_cap) : make_int2(-3, -1);
+      const uint32_t x = b0 + (uint32_t)i;
+      r[u] = i < n && want(i) ? __ldcg(rec + (x >= R_cap ? x - R_cap : x)) : make_int2(-3, -1);
     }
 #pragma unroll
     for (int u = 0; u < kPU; u++) a[u] = r[u].x >= 0 ? __ldg(arcs + r[u].x) : make_int4(0, 0, 0, 0);
@@ -94,34 +99,41 @@ __device__ __forceinline__ void layer_pass_arcs(const int4* __restrict__ arcs, c
 }
 
 // f(i, rec) over the records of a layer in batches of BS * kPU (cheapest first), until done()
-// holds after a batch; ends with a barrier, so done()'s inputs can be reset right after
+// holds after a batch (one decision for the whole CTA); ends with a barrier, so done()'s inputs
+// can be reset right after
 template <int BS, typename Fn, typename Done>
 __device__ __forceinline__ void layer_scan_until(const int2* rec, uint32_t R_cap, int64_t x0, int n, Fn f, Done done) {
+  const uint32_t b0 = (uint32_t)(x0 % R_cap);
   for (int i0 = 0; i0 < n; i0 += BS * kPU) {
     int2 r[kPU];
 #pragma unroll
     for (int u = 0; u < kPU; u++) {
       const int i = i0 + u * BS + (int)threadIdx.x;
-      r[u] = i < n ? __ldcg(rec + (uint32_t)(x0 + i) % R_cap) : make_int2(-3, -1);
+      const uint32_t x = b0 + (uint32_t)i;
+      r[u] = i < n ? __ldcg(rec + (x >= R_cap ? x - R_cap : x)) : make_int2(-3, -1);
     }
 #pragma unroll
     for (int u = 0; u < kPU; u++)
       if (r[u].x != -3) f(i0 + u * BS + (int)threadIdx.x, r[u]);
-    __syncthreads();
-    if (done()) break;
+    __syncthreads();   // the batch's updates are visible ...
+    const bool d = done();
+    if (__syncthreads_or(d)) break;   // ... and read by every thread before the next batch changes them
   }
   __syncthreads();
 }
+
+constexpr uint32_t kPredTag = 0x80000000u;   // set entries: state (epsilon source) | state + tag (emitting source)
 
 template <int BS, int MINB>
 __global__ void __launch_bounds__(BS, MINB) partial_root_kernel(PartialParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* set = (uint32_t*)smem_raw;                       // wanted source states
-  unsigned char* flag = (unsigned char*)(set + p.wcap);      // tokens of the current layer in S
-  __shared__ int s_changed[2], s_roots, s_root, s_status, s_nflag, s_nwant, s_found, s_hi;
-  // the wanted-state set is sized to what can be wanted (1.5x the tokens flagged), so that
-  // clearing it costs O(flagged tokens), not O(capacity), per step
-  auto set_cap = [&](int n) { return (uint32_t)min(p.wcap, max(64, n + n / 2 + 1)); };   // load <= 2/3
+  unsigned char* flag = (unsigned char*)(set + p.wcap);      // tokens of the current layer in S:
+                                                             // 2 unclassified, 1 classified
+  __shared__ int s_roots, s_root, s_status, s_nwe, s_nwp, s_found, s_hi;
+  // the wanted-state set of a layer holds at most one entry per token of S, so it is sized to
+  // the layer (load <= 2/3) and clearing it costs O(layer), not O(capacity)
+  auto set_cap = [&](int n) { return (uint32_t)min(p.wcap, max(64, n + n / 2 + 1)); };
   const int tid = threadIdx.x;
   const int ln = p.lanes[blockIdx.x];
   const LaneState* Lp = p.lanes_st + ln;
@@ -131,13 +143,11 @@ __global__ void __launch_bounds__(BS, MINB) partial_root_kernel(PartialParams p)
   const int2* linfo_base = p.layer_info + (size_t)ln * (p.TMAX + 1);
   auto linfo_at = [&](int k) { return linfo_base[k % (p.TMAX + 1)]; };   // layer index ring
   const int2 prev = p.settled[ln];
-  if (tid == 0) {
+  if (tid == 0)
     s_status = __ldcg(&Lp->status) != WFST_OK ? __ldcg(&Lp->status)
                : !__ldcg(&Lp->initialized)    ? WFST_ERR_STATE
                : Lcur - __ldcg(&Lp->layer_floor) > p.TMAX ? WFST_ERR_CAPACITY
                                               : WFST_OK;
-    s_changed[0] = s_changed[1] = 0;
-  }
   __syncthreads();
   auto finish = [&](int status, int root, int layer) {
     if (tid == 0) {
@@ -157,103 +167,89 @@ __global__ void __launch_bounds__(BS, MINB) partial_root_kernel(PartialParams p)
     finish(WFST_ERR_CAPACITY, -1, prev.x < 0 ? 0 : prev.x);
     return;
   }
-  for (int i = tid; i < Lk.y; i += BS) flag[i] = 1;
+  uint32_t wc = set_cap(Lk.y);
+  for (int i = tid; i < Lk.y; i += BS) flag[i] = 2;
+  for (uint32_t i = tid; i < wc; i += BS) set[i] = 0xFFFFFFFFu;
   if (tid == 0) {
-    s_nflag = Lk.y;
     s_hi = Lk.y;
+    s_roots = 0;
+    s_root = -1;
+    s_nwe = s_nwp = 0;
   }
   __syncthreads();
   int root = -1;   // record index of the settle point
-  int par = 0;     // s_changed[par]: this epsilon pass; the other one is cleared for the next
-  // Tokens on survivor paths are cheap and the layers are stored cheapest bins first, so past
-  // the first layer the flagged tokens sit near the front: passes over flagged tokens stop at
-  // s_hi (one past the last flagged index), and a search for a known number of wanted states
-  // stops once all are found.
+  // Every token of S is classified once, by the arc that entered it: an epsilon arc puts its
+  // source (a token of the same layer) into the set, an emitting arc makes it a root and puts
+  // its source (a token of the layer below) into the set with kPredTag, the start token is a
+  // root.  Epsilon sources join S and are classified in turn.  Tokens on survivor paths are
+  // cheap and a layer is stored cheapest bins first, so past the first layer S sits near the
+  // front: passes over S stop at s_hi (one past its last index), and a search for a known number
+  // of wanted states stops once all are found.
   while (true) {
-    // epsilon predecessors inside layer k (chains are short; repeat until nothing new)
     while (true) {
-      const uint32_t wc = set_cap(s_nflag);
-      for (uint32_t i = tid; i < wc; i += BS) set[i] = 0xFFFFFFFFu;
-      if (tid == 0) {
-        s_nwant = 0;
-        s_found = 0;
-      }
-      __syncthreads();
-      // s_changed[par ^ 1] was last read at the end of the previous pass: every thread is past it
-      if (tid == 0) s_changed[par ^ 1] = 0;
       const int hi = s_hi;
-      layer_pass_arcs<BS>(p.arcs, rec, Rc, Lk.x, hi, [&](int i) { return flag[i] != 0; }, [&](int, int2 r, int4 a) {
-        if (r.x >= 0 && a.z < 0 && pset_put(set, wc, (uint32_t)(a.w & 0x7FFFFFFF))) atomicAdd(&s_nwant, 1);
+      if (tid == 0) s_found = 0;   // (last read before the barrier that ended the previous search)
+      bool adde = false;
+      layer_pass_arcs<BS>(p.arcs, rec, Rc, Lk.x, hi, [&](int i) { return flag[i] == 2; }, [&](int i, int2 r, int4 a) {
+        flag[i] = 1;
+        if (r.x < 0 || a.z >= 0) {
+          atomicAdd(&s_roots, 1);
+          atomicMax(&s_root, Lk.x + i);   // used only when there is exactly one root
+          if (r.x >= 0 && pset_put(set, wc, (uint32_t)(a.w & 0x7FFFFFFF) | kPredTag)) atomicAdd(&s_nwp, 1);
+        } else if (pset_put(set, wc, (uint32_t)(a.w & 0x7FFFFFFF))) {
+          atomicAdd(&s_nwe, 1);
+          adde = true;
+        }
       });
-      __syncthreads();
-      const int nwant = s_nwant;
-      if (nwant == 0) break;
-      // every wanted source is a token of this layer (flagged or not): stop when all are seen
+      if (!__syncthreads_or(adde)) break;   // no new epsilon source wanted
+      const int nwe = s_nwe;
+      bool newf = false;
+      // every wanted epsilon source is a token of this layer: stop when all are seen
       layer_scan_until<BS>(rec, Rc, Lk.x, Lk.y, [&](int i, int2 r) {
         if (pset_has(set, wc, (uint32_t)r.y)) {
           atomicAdd(&s_found, 1);
           if (!flag[i]) {
-            flag[i] = 1;
-            s_changed[par] = 1;
-            atomicAdd(&s_nflag, 1);
+            flag[i] = 2;
             atomicMax(&s_hi, i + 1);
+            newf = true;
           }
         }
-      }, [&]() { return s_found >= nwant; });
-      const bool more = s_changed[par] != 0;
-      par ^= 1;
-      if (!more) break;
+      }, [&]() { return s_found >= nwe; });
+      if (!__syncthreads_or(newf)) break;
     }
-    // roots: tokens of S entered by an emitting arc or the start
-    if (tid == 0) {
-      s_roots = 0;
-      s_root = -1;
-    }
-    __syncthreads();
-    const int hi = s_hi;
-    layer_pass_arcs<BS>(p.arcs, rec, Rc, Lk.x, hi, [&](int i) { return flag[i] != 0; }, [&](int i, int2 r, int4 a) {
-      if (r.x < 0 || a.z >= 0) {
-        atomicAdd(&s_roots, 1);
-        atomicMax(&s_root, Lk.x + i);   // used only when there is exactly one root
-      }
-    });
-    __syncthreads();
     const int n_roots = s_roots;
     if (n_roots == 1 || k == 0 || (prev.x >= 0 && k <= prev.x)) {
       root = n_roots == 1 ? s_root : -2;
       break;
     }
-    // predecessors of the roots in layer k-1
-    const uint32_t wc = set_cap(n_roots);
-    for (uint32_t i = tid; i < wc; i += BS) set[i] = 0xFFFFFFFFu;
-    if (tid == 0) s_nwant = 0;
-    __syncthreads();
-    layer_pass_arcs<BS>(p.arcs, rec, Rc, Lk.x, hi, [&](int i) { return flag[i] != 0; }, [&](int, int2 r, int4 a) {
-      if (r.x >= 0 && a.z >= 0 && pset_put(set, wc, (uint32_t)(a.w & 0x7FFFFFFF))) atomicAdd(&s_nwant, 1);
-    });
-    __syncthreads();   // flags of layer k read: layer k-1's may be written
+    // S = the tokens of layer k-1 whose states the roots came from
+    const int nwp = s_nwp;
     k--;
     Lk = linfo_at(k);
     if (Lk.y > p.fcap) {
       if (tid == 0) s_status = WFST_ERR_CAPACITY;
       break;
     }
+    __syncthreads();   // s_roots, s_root, s_nwp read
     for (int i = tid; i < Lk.y; i += BS) flag[i] = 0;
     if (tid == 0) {
-      s_nflag = 0;
       s_hi = 0;
       s_found = 0;
+      s_roots = 0;
+      s_root = -1;
+      s_nwe = s_nwp = 0;
     }
     __syncthreads();
-    const int nwant = s_nwant;
     layer_scan_until<BS>(rec, Rc, Lk.x, Lk.y, [&](int i, int2 r) {
-      if (pset_has(set, wc, (uint32_t)r.y)) {
-        flag[i] = 1;
+      if (pset_has(set, wc, (uint32_t)r.y | kPredTag)) {
+        flag[i] = 2;
         atomicAdd(&s_found, 1);
-        atomicAdd(&s_nflag, 1);
         atomicMax(&s_hi, i + 1);
       }
-    }, [&]() { return s_found >= nwant; });
+    }, [&]() { return s_found >= nwp; });
+    wc = set_cap(Lk.y);
+    for (uint32_t i = tid; i < wc; i += BS) set[i] = 0xFFFFFFFFu;
+    __syncthreads();
   }
   __syncthreads();
   if (s_status != WFST_OK || root == -2)   // (-2: the walk met the old settle point unresolved)
@@ -288,6 +284,7 @@ __global__ void __launch_bounds__(BS, MINB) partial_trace_kernel(PartialParams p
   __shared__ int s_idx[3], s_arc[3], s_src[3], s_emit[3];
   __shared__ int s_path[kTraceSmem];
   __shared__ int s_w[BS / 32];
+  __shared__ int s_off;
   const int tid = threadIdx.x;
   const int ln = p.lanes[blockIdx.x];
   const int2* rec = p.rec + (size_t)ln * p.R_cap;
@@ -302,6 +299,7 @@ __global__ void __launch_bounds__(BS, MINB) partial_trace_kernel(PartialParams p
     if (tid == 0) {
       p.n_arcs_out[blockIdx.x] = 0;
       p.n_olab_out[blockIdx.x] = 0;
+      p.root_out[blockIdx.x] = 0;
     }
     return;
   }
@@ -344,48 +342,59 @@ __global__ void __launch_bounds__(BS, MINB) partial_trace_kernel(PartialParams p
     // the path's tokens are cheap and a layer is stored cheapest bins first: the scan usually
     // ends in its first batch (the barrier after each batch is the step's barrier)
     int i0 = 0;
+    const uint32_t b0 = (uint32_t)info.x % Rc;   // (R_cap < 2^31; no modulo per record)
     do {
       int2 r[kPU];
 #pragma unroll
       for (int u = 0; u < kPU; u++) {
         const int i = i0 + u * BS + tid;
-        r[u] = i < info.y ? __ldcg(rec + (uint32_t)((int64_t)info.x + i) % Rc) : make_int2(-3, -1);
+        const uint32_t x = b0 + (uint32_t)i;
+        r[u] = i < info.y ? __ldcg(rec + (x >= Rc ? x - Rc : x)) : make_int2(-3, -1);
       }
+      bool found = false;
 #pragma unroll
       for (int u = 0; u < kPU; u++)
-        if (r[u].y == want && r[u].x != -3) load_step(nxt, info.x + i0 + u * BS + tid, r[u]);
-      __syncthreads();
+        if (r[u].y == want && r[u].x != -3) {
+          load_step(nxt, info.x + i0 + u * BS + tid, r[u]);
+          found = true;
+        }
+      if (__syncthreads_or(found)) break;   // one decision for the CTA (the finder's writes are visible)
       i0 += BS * kPU;
-    } while (i0 < info.y && s_idx[nxt] < 0);
+    } while (i0 < info.y);
     j++;
   }
   __syncthreads();
-  // ---- reverse into path order, gather the non-zero olabels (in parallel when on chip)
+  // ---- reverse into path order, gather the non-zero olabels (in parallel when on chip), and
+  // pack both at this stream's offset: the host copies back exactly the arcs that settled
   const int m = min(len, p.cap);
+  if (tid == 0) s_off = m > 0 ? atomicAdd(p.packed_count, m) : 0;
+  __syncthreads();
+  const int off = s_off;
+  int32_t* pa = p.packed_arcs + off;
+  int32_t* po = p.packed_olab + off;
   int nol = 0;
   if (m <= kTraceSmem) {
-    for (int x = tid; x < m; x += BS) out[x] = s_path[m - 1 - x];
     for (int x0 = 0; x0 < m; x0 += BS) {
       const int x = x0 + tid;
-      const int32_t ol = x < m ? __ldg(p.olabel + s_path[m - 1 - x]) : 0;
+      const int32_t arc = x < m ? s_path[m - 1 - x] : 0;
+      const int32_t ol = x < m ? __ldg(p.olabel + arc) : 0;
+      if (x < m) pa[x] = arc;
       int e = 0;
       const int tot = block_excl_scan01<BS>(ol != 0, e, s_w);
-      if (ol != 0) p.olab_out[(size_t)blockIdx.x * p.cap + nol + e] = ol;
+      if (ol != 0) po[nol + e] = ol;
       nol += tot;
     }
   } else if (tid == 0) {   // serial fallback (more than kTraceSmem arcs settled in one call)
-    for (int x = 0; x < m / 2; x++) {
-      const int32_t t = out[x];
-      out[x] = out[m - 1 - x];
-      out[m - 1 - x] = t;
-    }
     for (int x = 0; x < m; x++) {
-      const int32_t ol = __ldg(p.olabel + out[x]);
-      if (ol != 0) p.olab_out[(size_t)blockIdx.x * p.cap + nol++] = ol;
+      const int32_t arc = out[m - 1 - x];
+      pa[x] = arc;
+      const int32_t ol = __ldg(p.olabel + arc);
+      if (ol != 0) po[nol++] = ol;
     }
   }
   if (tid == 0) {
     p.n_olab_out[blockIdx.x] = nol;
+    p.root_out[blockIdx.x] = off;
     if (status == WFST_OK && len <= p.cap) {
       p.settled[ln] = make_int2(k, root);
       if (p.reclaim) {   // traceback GC: everything below the settle point is handed out

@@ -25,7 +25,7 @@ SYMBOLS = ["wfst_load_graph", "wfst_graph_from_arrays", "wfst_graph_info", "wfst
            "wfst_get_best_paths", "wfst_decoder_stats", "wfst_decoder_reset_stats", "wfst_decoder_frame_stats",
            "wfst_debug_layer", "wfst_synth_loglikes", "wfst_last_error", "wfst_status_string",
            "wfst_abi_version", "wfst_get_lattice", "wfst_get_partial_paths", "wfst_graph_replicate",
-           "wfst_get_best_paths_ex", "wfst_get_partial_paths_ex"]
+           "wfst_get_best_paths_ex", "wfst_get_partial_paths_ex", "wfst_get_partial_paths_packed"]
 
 
 class WfstError(RuntimeError):
@@ -109,6 +109,7 @@ def lib():
             "wfst_get_partial_paths": [P, P, I32, P, P, I32, P, P, P],
             "wfst_get_best_paths_ex": [P, P, I32, P, P, P, P, I32, P, P, P],
             "wfst_get_partial_paths_ex": [P, P, I32, P, P, I32, P, P, P, P],
+            "wfst_get_partial_paths_packed": [P, P, I32, P, P, I64, I32, P, P, P, P, P, P],
             "wfst_graph_replicate": [P, C.c_int, P],
         }
         for name, args in sig.items():
@@ -167,12 +168,12 @@ def _ids(streams):
 
 # ------------------------------------------------------------------ host-only helpers
 class _Rows:
-    """Sequence of per-stream row views rows[i, :n[i]] of a result matrix, built on access (a
-    4096-stream result costs no per-stream Python work unless the rows are read)."""
-    __slots__ = ("_a", "_n")
+    """Sequence of per-stream views a[off[i] : off[i] + min(n[i], cap)] of a packed result, built
+    on access (a 4096-stream result costs no per-stream Python work unless the rows are read)."""
+    __slots__ = ("_a", "_n", "_off", "_cap")
 
-    def __init__(self, a, n):
-        self._a, self._n = a, n
+    def __init__(self, a, n, off, cap):
+        self._a, self._n, self._off, self._cap = a, n, off, cap
 
     def __len__(self):
         return len(self._n)
@@ -184,7 +185,8 @@ class _Rows:
             i += len(self)
         if not 0 <= i < len(self):
             raise IndexError(i)
-        return self._a[i, :self._n[i]]
+        o = int(self._off[i])
+        return self._a[o:o + min(int(self._n[i]), self._cap)]
 
     def __iter__(self):
         return (self[i] for i in range(len(self)))
@@ -379,19 +381,24 @@ class Decoder:
         (e.result holds them); raise_on_error=False returns them with status instead."""
         ids = np.arange(self.n_streams, dtype=np.int32) if streams is None else _np(streams, np.int32)
         n = ids.size
-        arcs = np.empty((n, cap), np.int32)
-        ols = np.empty((n, cap), np.int32)
+        # packed outputs (wfst_get_partial_paths_packed): only the settled arcs are copied and
+        # written, so the n * cap buffers are touched only where arcs land (this runs every chunk)
+        arcs = np.empty(n * cap, np.int32)
+        ols = np.empty(n * cap, np.int32)
+        off = np.zeros(n, np.int64)
+        tot = np.zeros(1, np.int64)
         nar, nol, fr = np.zeros(n, np.int32), np.zeros(n, np.int32), np.zeros(n, np.int32)
         status = np.zeros(n, np.int32)
-        rc = lib().wfst_get_partial_paths_ex(self.h, _ptr(ids), n, _ptr(arcs), _ptr(ols), cap, _ptr(nar), _ptr(nol),
-                                             _ptr(fr), _ptr(status))
-        if rc == 0:   # row views into this call's fresh buffers, made on access (this runs every chunk)
-            return dict(arcs=_Rows(arcs, nar), olabels=_Rows(ols, nol), settled_frames=fr, status=status)
+        rc = lib().wfst_get_partial_paths_packed(self.h, _ptr(ids), n, _ptr(arcs), _ptr(ols), C.c_int64(n * cap), cap,
+                                                 _ptr(off), _ptr(tot), _ptr(nar), _ptr(nol), _ptr(fr), _ptr(status))
+        arcs, ols = _Rows(arcs, nar, off, cap), _Rows(ols, nol, off, cap)
+        if rc == 0:   # per-stream views, made on access
+            return dict(arcs=arcs, olabels=ols, settled_frames=fr, status=status)
         # per stream: OK streams advanced their settle point (their arcs must not be dropped);
         # streams whose new arcs exceeded cap kept theirs and are fetched again with a larger cap
         big = (status == 1) & (nar > cap)
-        out_a = [arcs[i, :nar[i]].copy() if status[i] == 0 else None for i in range(n)]
-        out_o = [ols[i, :nol[i]].copy() if status[i] == 0 else None for i in range(n)]
+        out_a = [arcs[i].copy() if status[i] == 0 else None for i in range(n)]
+        out_o = [ols[i].copy() if status[i] == 0 else None for i in range(n)]
         if big.any():
             again = self.partial_paths(ids[big], cap=int(nar.max()) + 64, raise_on_error=False)
             for k, i in enumerate(np.nonzero(big)[0]):

@@ -175,3 +175,43 @@ def test_reclaim_long_streams_c3_graph(W, torch, oracle_mod):
         tail = list(res["arcs"][b, :res["n_arcs"][b]])
         assert acc[b] + tail == list(r.arcs), b
         assert res["cost"][b] == r.cost32
+
+
+def test_row_and_packed_apis_agree(W, torch):
+    """wfst_get_partial_paths_ex (rows [n][cap]) and wfst_get_partial_paths_packed (ranges at
+    offsets) return the same arcs, olabels, counts and settle points on two decoders fed the same
+    chunks; the packed ranges do not overlap and *total is their sum."""
+    import ctypes as C
+    g = I.hclg_graph(3000, 6, 200, seed=4)
+    T, B, P, cap = 40, 9, 200, 64
+    pl = I.planted_walks(g, B, T, seed=2)
+    t = torch.from_numpy(I.loglikes(5, range(B), T, P, pl, 1.0, 4.0)).cuda()
+    G = W.Graph.from_arrays(g)
+    D1, D2 = W.Decoder(G, B, 10.0, 300), W.Decoder(G, B, 10.0, 300)
+    D1.reset()
+    D2.reset()
+    L = W.lib()
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    for t0 in range(0, T, 8):
+        D1.decode_frames(t[t0:t0 + 8])
+        D2.decode_frames(t[t0:t0 + 8])
+        ids = np.arange(B, dtype=np.int32)
+        ra, ro = np.full((B, cap), -7, np.int32), np.full((B, cap), -7, np.int32)
+        rn, rno, rf, rs = (np.zeros(B, np.int32) for _ in range(4))
+        assert L.wfst_get_partial_paths_ex(D1.h, p(ids), B, p(ra), p(ro), cap, p(rn), p(rno), p(rf), p(rs)) == 0
+        pa, po = np.full(B * cap, -7, np.int32), np.full(B * cap, -7, np.int32)
+        off, tot = np.zeros(B, np.int64), np.zeros(1, np.int64)
+        pn, pno, pf, ps = (np.zeros(B, np.int32) for _ in range(4))
+        assert L.wfst_get_partial_paths_packed(D2.h, p(ids), B, p(pa), p(po), C.c_int64(B * cap), cap, p(off), p(tot),
+                                               p(pn), p(pno), p(pf), p(ps)) == 0
+        assert (rn == pn).all() and (rno == pno).all() and (rf == pf).all() and (rs == ps).all()
+        assert int(tot[0]) == int(pn.sum())
+        spans = sorted((int(off[i]), int(off[i]) + int(pn[i])) for i in range(B) if pn[i])
+        assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+        for i in range(B):
+            assert list(ra[i, :rn[i]]) == list(pa[off[i]:off[i] + pn[i]])
+            assert list(ro[i, :rno[i]]) == list(po[off[i]:off[i] + pno[i]])
+    # total_cap below n * cap is rejected before any work
+    rc = L.wfst_get_partial_paths_packed(D2.h, p(ids), B, p(pa), p(po), C.c_int64(B * cap - 1), cap, p(off), p(tot),
+                                         p(pn), p(pno), p(pf), p(ps))
+    assert rc == 1
