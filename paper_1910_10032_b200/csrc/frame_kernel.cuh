@@ -46,6 +46,11 @@ constexpr int kPlace = 64;         // coarse cost bins ordering the next frontie
 #define WFST_SMALLCLAIMS 2048
 #endif
 constexpr int kSmallClaims = WFST_SMALLCLAIMS;   // frames with at most this many claims use an on-chip claim list
+#ifndef WFST_EPSWARP
+#define WFST_EPSWARP 32
+#endif
+constexpr int kEpsWarp = WFST_EPSWARP > 0 ? WFST_EPSWARP : 1;   // epsilon worklists up to this size: warp 0 alone
+constexpr bool kEpsWarpOn = WFST_EPSWARP > 0;
 
 struct LaneState {
   int32_t status;       // wfst_status, sticky
@@ -113,6 +118,8 @@ struct SmemCtl {
   int32_t theta;
   int32_t n_claim, n_claim_emit, n_ovf, n_oclaim, n_surv, n_in, n_wl, n_big, next_group;
   int32_t wlc[3];   // epsilon worklist counters (rotating)
+  int32_t eps_r, eps_cur;           // where the warp-synchronous epsilon iterations stopped
+  uint32_t swl[2][kEpsWarp];        // the first kEpsWarp entries of the epsilon worklists
 #ifdef WFST_COUNT
   unsigned long long dbgc[4];   // alpha-bound frames: claims above k_alpha by (0,0.5], (0.5,2], (2,5], >5
 #endif
@@ -568,7 +575,10 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     if (seed) {   // claimed states with epsilon arcs seed the closure (no table scan later)
       const bool e = claimed && eps_flag;
       const int idx = warp_append(e, SA(n_wl));
-      if (e) wl0[idx] = (uint32_t)slot;
+      if (e) {
+        wl0[idx] = (uint32_t)slot;
+        if (idx < kEpsWarp) S.swl[0][idx] = (uint32_t)slot;
+      }
     }
     const int leader = __ffs(m) - 1;
     int base = atom_add_s_if(lane == leader, SA(n_claim), __popc(m));
@@ -1225,6 +1235,56 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   }
 
   // ---- row a5: epsilon closure under the fixed cutoff (reading R7) ----
+  // relax the epsilon arcs of worklist entry `slot` (-1: none); warp-collective.  Improved
+  // tokens with epsilon arcs are appended to worklist `wn` (counter wlc[rn]); the first
+  // kEpsWarp entries are mirrored on chip for the warp-synchronous iterations.
+  __device__ __forceinline__ void relax_eps(int slot, float cut_b, float cut_a, int rn, uint32_t* Wn, int wn,
+                                            long long& relax) {
+    int e0 = 0, e1 = 0;
+    float cp = 0.f;
+    if (slot >= 0) {
+      const u64 v = read_slot(slot);
+      cp = key_cost(v);
+      if (cp < cut_b && cp <= cut_a) {   // only kept tokens relax (R7)
+        const int4 si = __ldg(p.state_info + ((uint32_t)v & 0x7FFFFFFFu));
+        e0 = si.y;
+        e1 = si.z;
+      }
+    }
+    // each thread relaxes its token's epsilon arcs (epsilon out-degrees are small)
+    const int n_more = e1 - e0;
+    int maxd = n_more;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxd = max(maxd, __shfl_xor_sync(0xffffffffu, maxd, o));
+    for (int k = 0; k < maxd; k++) {
+      const bool v = k < n_more;
+      int4 arc = make_int4(0, 0, 0, 0);
+      bool claimed = false, logit = false, strict = false;
+      int sl = -1;
+      if (v) {
+        arc = __ldg(p.arcs + e0 + k);
+        const float c = __fadd_rn(__fadd_rn(cp, __int_as_float(arc.y)), 0.0f);
+        relax++;
+        if (c < cut_b && c <= cut_a) {
+          const uint32_t o = ord_of(c);
+          const uint32_t q = (uint32_t)arc.x | ((uint32_t)arc.w & 0x80000000u);   // state | has-eps
+          sl = insert(q, ((u64)o << 32) | q, claimed, logit, strict);
+          if (sl >= 0 && logit) red_min_g64(win + sl, ((u64)o << 32) | (uint32_t)(e0 + k));
+          if (sl < 0) claimed = strict = false;
+        }
+      }
+      const uint32_t has_eps = (uint32_t)arc.w >> 31;
+      add_claim(sl, claimed, has_eps, -1, false);
+      const bool push = strict && has_eps;
+      const int wi = warp_append(push, SAI(wlc, rn));
+      if (push) {
+        if (wi < p.FCAP) Wn[wi] = (uint32_t)sl;
+        else S.status = WFST_ERR_CAPACITY;
+        if (wi < kEpsWarp) S.swl[wn][wi] = (uint32_t)sl;
+      }
+    }
+  }
+
   __device__ void eps_closure() {
     const int tid = threadIdx.x;
     const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
@@ -1236,10 +1296,37 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     if (tid == 0) {
       S.wlc[0] = S.n_wl;
       S.wlc[1] = S.wlc[2] = 0;
+      S.eps_r = 0;
+      S.eps_cur = 0;
     }
     __syncthreads();
-    int cur = 0, r = 0;
     long long relax = 0;
+    // Small worklists (the usual case: a few back-off arcs per frame): warp 0 alone runs the
+    // iterations, entries from the on-chip mirror, __syncwarp between iterations -- no CTA
+    // barrier and no global worklist read per iteration.  A worklist that outgrows a warp is
+    // handed to the CTA-wide loop below (the global worklists always hold every entry).
+    if (kEpsWarpOn && S.n_wl > 0 && S.n_wl <= kEpsWarp) {
+      if (tid < 32) {
+        int cur = 0, r = 0;
+        while (true) {
+          const int n_wl = S.wlc[r];
+          if (n_wl == 0 || n_wl > kEpsWarp) break;
+          const int rn = r == 2 ? 0 : r + 1;
+          if (tid == 0) S.wlc[rn == 2 ? 0 : rn + 1] = 0;
+          relax_eps(tid < n_wl ? (int)S.swl[cur][tid] : -1, cut_b, cut_a, rn, wl0 + (size_t)(cur ^ 1) * p.FCAP, cur ^ 1,
+                    relax);
+          __syncwarp();
+          cur ^= 1;
+          r = rn;
+        }
+        if (tid == 0) {
+          S.eps_r = r;
+          S.eps_cur = cur;
+        }
+      }
+      __syncthreads();
+    }
+    int cur = S.eps_cur, r = S.eps_r;
     while (true) {
       const int n_wl = min(S.wlc[r], p.FCAP);
       if (n_wl == 0) break;
@@ -1249,48 +1336,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       uint32_t* Wn = wl0 + (size_t)(cur ^ 1) * p.FCAP;
       for (int i0 = 0; i0 < n_wl; i0 += BS) {
         const int i = i0 + tid;
-        int e0 = 0, e1 = 0;
-        float cp = 0.f;
-        if (i < n_wl) {
-          const u64 v = read_slot((int)__ldcg(W + i));
-          cp = key_cost(v);
-          if (cp < cut_b && cp <= cut_a) {   // only kept tokens relax (R7)
-            const int4 si = __ldg(p.state_info + ((uint32_t)v & 0x7FFFFFFFu));
-            e0 = si.y;
-            e1 = si.z;
-          }
-        }
-        // each thread relaxes its token's epsilon arcs (epsilon out-degrees are small)
-        const int n_more = e1 - e0;
-        int maxd = n_more;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) maxd = max(maxd, __shfl_xor_sync(0xffffffffu, maxd, o));
-        for (int k = 0; k < maxd; k++) {
-          const bool v = k < n_more;
-          int4 arc = make_int4(0, 0, 0, 0);
-          bool claimed = false, logit = false, strict = false;
-          int slot = -1;
-          if (v) {
-            arc = __ldg(p.arcs + e0 + k);
-            const float c = __fadd_rn(__fadd_rn(cp, __int_as_float(arc.y)), 0.0f);
-            relax++;
-            if (c < cut_b && c <= cut_a) {
-              const uint32_t o = ord_of(c);
-              const uint32_t q = (uint32_t)arc.x | ((uint32_t)arc.w & 0x80000000u);   // state | has-eps
-              slot = insert(q, ((u64)o << 32) | q, claimed, logit, strict);
-              if (slot >= 0 && logit) red_min_g64(win + slot, ((u64)o << 32) | (uint32_t)(e0 + k));
-              if (slot < 0) claimed = strict = false;
-            }
-          }
-          const uint32_t has_eps = (uint32_t)arc.w >> 31;
-          add_claim(slot, claimed, has_eps, -1, false);
-          const bool push = strict && has_eps;
-          const int wi = warp_append(push, SAI(wlc, rn));
-          if (push) {
-            if (wi < p.FCAP) Wn[wi] = (uint32_t)slot;
-            else S.status = WFST_ERR_CAPACITY;
-          }
-        }
+        relax_eps(i < n_wl ? (int)__ldcg(W + i) : -1, cut_b, cut_a, rn, Wn, cur ^ 1, relax);
       }
       __syncthreads();
       cur ^= 1;
