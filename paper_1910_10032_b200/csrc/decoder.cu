@@ -35,11 +35,15 @@ namespace {
 #define WFST_BP_THREADS 512
 #endif
 constexpr int kBestPathThreads = WFST_BP_THREADS;   // (<= 1024: s_fin / s_any hold one entry per warp)
+constexpr int kPathSmem = 4096;                      // path arcs kept on chip during the walk
 __global__ void __launch_bounds__(kBestPathThreads) best_path_kernel(KParams p, const int32_t* __restrict__ olabel, const int32_t* __restrict__ lanes,
                                  int32_t n, int32_t cap, float* cost_out, int32_t* reached_out, int32_t* n_arcs_out,
                                  int32_t* arcs_out, int32_t* olab_out, int32_t* n_olab_out, int32_t* status_out) {
   __shared__ u64 s_fin[32], s_any[32];
-  __shared__ int s_idx, s_arc, s_layer, s_len, s_nol, s_status;
+  __shared__ int s_idx;
+  __shared__ int s_w_arc[3], s_w_src[3], s_w_emit[3], s_w_found[3];
+  __shared__ int s_path[kPathSmem];
+  __shared__ int s_wsum[kBestPathThreads / 32];
   const int li = blockIdx.x;
   const int lane = lanes[li];
   const int tid = threadIdx.x;
@@ -81,12 +85,7 @@ __global__ void __launch_bounds__(kBestPathThreads) best_path_kernel(KParams p, 
     s_fin[tid >> 5] = kf;
     s_any[tid >> 5] = ka;
   }
-  if (tid == 0) {
-    s_idx = -1;
-    s_len = 0;
-    s_nol = 0;
-    s_status = WFST_OK;
-  }
+  if (tid == 0) s_idx = -1;
   __syncthreads();
   kf = kEmpty;
   ka = kEmpty;
@@ -110,74 +109,111 @@ __global__ void __launch_bounds__(kBestPathThreads) best_path_kernel(KParams p, 
     }
     return;
   }
+  // ---- walk back.  Step j reads slot j%3 (the record found by step j-1: its arc, the arc's
+  // source state and kind), its scan of the source's layer fills slot (j+1)%3 and thread 0 clears
+  // slot (j+2)%3, last read in step j-1: one barrier per step.  The path's tokens are cheap and
+  // a layer is stored cheapest bins first, so a scan usually ends in its first batch.  The arcs
+  // are kept on chip (kPathSmem of them; longer walks also go to arcs_out) and reversed and
+  // labelled in parallel at the end.
+  int32_t* out = arcs_out + (size_t)li * cap;
+  auto load_step = [&](int slot, int arc) {   // (one thread: the record's finder)
+    s_w_arc[slot] = arc;
+    s_w_found[slot] = 1;
+    if (arc >= 0) {
+      const int4 a = __ldg(p.arcs + arc);
+      s_w_src[slot] = a.w & 0x7FFFFFFF;
+      s_w_emit[slot] = a.z >= 0;
+    }
+  };
   if (tid == 0) {
     cost_out[li] = float_of_ord((uint32_t)(kb >> 32));
     reached_out[li] = reached ? 1 : 0;
-    s_arc = __ldcg(&rec[rix(s_idx)].x);
-    s_layer = L.frames;
+    load_step(0, __ldcg(&rec[rix(s_idx)].x));
+    s_w_found[1] = 0;
   }
   __syncthreads();
-  // walk back: arcs are stored from the end of this lane's output row (reversed afterwards)
-  int32_t* out = arcs_out + (size_t)li * cap;
+  int len = 0, layer = L.frames, j = 0, nol_far = 0, status = WFST_OK;
   const long long max_steps = (long long)L.rec_used + 2;
-  for (long long step = 0; step < max_steps; step++) {
-    const int arc = s_arc;
-    const int cur_layer = s_layer;
-    __syncthreads();   // every thread has read s_arc / s_layer / s_idx before thread 0 rewrites them
-    if (arc < 0) break;
-    // traceback GC (row f2): below the settle point the path was already handed out by
-    // wfst_get_partial_paths -- stop at the settled root (entered by an emitting arc)
-    if (cur_layer == L.layer_floor && L.layer_floor > 0 && __ldg(&p.arcs[arc].z) >= 0) break;
-    int src = 0, layer = 0;
-    if (tid == 0) {
-      const int4 a = __ldg(p.arcs + arc);
-      src = a.w & 0x7FFFFFFF;
-      layer = a.z >= 0 ? s_layer - 1 : s_layer;
-      if (s_len < cap) out[s_len] = arc;
-      s_len++;
-      if (__ldg(olabel + arc) != 0) s_nol++;   // counted over the whole walk (the size a caller needs)
-      s_idx = -1;
-      s_layer = layer;
-      s_arc = src;   // temporarily: the state to look for
-    }
-    __syncthreads();
-    const int want = s_arc;
-    layer = s_layer;
-    const int2 info = __ldcg(&linfo[layer % (p.TMAX + 1)]);
-    __syncthreads();
-    const int64_t r0 = (uint32_t)info.x % (uint32_t)p.R_cap;   // record ring (row f2 GC)
-    for (int i = tid; i < info.y; i += blockDim.x) {
-      const int64_t ri = r0 + i;
-      const int2 r = __ldcg(rec + (ri >= p.R_cap ? ri - p.R_cap : ri));
-      if (r.y == want) {
-        s_idx = info.x + i;
-        s_arc = r.x;
-      }
-    }
-    __syncthreads();
-    if (s_idx < 0) {
-      if (tid == 0) s_status = WFST_ERR_STATE;   // broken chain (must not happen)
+  for (; j < max_steps; j++) {
+    const int cur = j % 3, nxt = (j + 1) % 3;
+    if (!s_w_found[cur]) {   // the previous scan found no record of the source state
+      status = WFST_ERR_STATE;   // (broken chain: must not happen)
       break;
     }
+    const int arc = s_w_arc[cur];
+    if (arc < 0) break;   // the start token
+    // traceback GC (row f2): below the settle point the path was already handed out by
+    // wfst_get_partial_paths -- stop at the settled root (entered by an emitting arc)
+    if (layer == L.layer_floor && L.layer_floor > 0 && s_w_emit[cur]) break;
+    if (tid == 0) {
+      if (len < cap) out[len] = arc;
+      if (len < kPathSmem) s_path[len] = arc;
+      else if (__ldg(olabel + arc) != 0) nol_far++;   // counted over the whole walk
+      s_w_found[(j + 2) % 3] = 0;
+    }
+    len++;
+    layer -= s_w_emit[cur];
+    const int want = s_w_src[cur];
+    const int2 info = __ldcg(&linfo[layer % (p.TMAX + 1)]);
+    const uint32_t Rc = (uint32_t)p.R_cap, b0 = (uint32_t)info.x % Rc;   // record ring (row f2 GC)
+    for (int i0 = 0; i0 < max(info.y, 1); i0 += kBestPathThreads * kPU) {
+      int2 r[kPU];
+#pragma unroll
+      for (int u = 0; u < kPU; u++) {
+        const int i = i0 + u * kBestPathThreads + tid;
+        const uint32_t x = b0 + (uint32_t)i;
+        r[u] = i < info.y ? __ldcg(rec + (x >= Rc ? x - Rc : x)) : make_int2(-3, -1);
+      }
+      bool found = false;
+#pragma unroll
+      for (int u = 0; u < kPU; u++)
+        if (r[u].y == want && r[u].x != -3) {
+          load_step(nxt, r[u].x);
+          found = true;
+        }
+      if (__syncthreads_or(found)) break;   // one decision for the CTA (the finder's writes are visible)
+    }
   }
+  if (j >= max_steps) status = WFST_ERR_STATE;
   __syncthreads();
-  if (tid != 0) return;
-  const int len = s_len;
-  n_arcs_out[li] = len;
-  // reverse in place to forward order, then olabels
+  n_arcs_out[li] = len;   // (every thread holds the same len)
   const int m = min(len, cap);
-  for (int k = 0; k < m / 2; k++) {
-    const int32_t t = out[k];
-    out[k] = out[m - 1 - k];
-    out[m - 1 - k] = t;
+  int nol = 0, nol_all = 0;
+  if (m <= kPathSmem) {   // reverse to forward order, olabels compacted in path order
+    for (int x0 = 0; x0 < m; x0 += kBestPathThreads) {
+      const int x = x0 + tid;
+      const int32_t arc = x < m ? s_path[m - 1 - x] : 0;
+      const int32_t ol = x < m ? __ldg(olabel + arc) : 0;
+      if (x < m) out[x] = arc;
+      int e = 0;
+      const int tot = block_excl_scan01<kBestPathThreads>(ol != 0, e, s_wsum);
+      if (ol != 0) olab_out[(size_t)li * cap + nol + e] = ol;
+      nol += tot;
+    }
+    // olabels of the walk's arcs beyond cap (a truncated path still reports the size it needs)
+    for (int x0 = m; x0 < min(len, kPathSmem); x0 += kBestPathThreads) {
+      const int x = x0 + tid;
+      int e = 0;
+      nol_all += block_excl_scan01<kBestPathThreads>(x < min(len, kPathSmem) && __ldg(olabel + s_path[x]) != 0, e,
+                                                     s_wsum);
+    }
+    nol_all += nol;
+  } else if (tid == 0) {   // serial fallback (cap and the walk both beyond kPathSmem)
+    for (int k = 0; k < m / 2; k++) {
+      const int32_t t = out[k];
+      out[k] = out[m - 1 - k];
+      out[m - 1 - k] = t;
+    }
+    for (int k = 0; k < m; k++) {
+      const int32_t ol = __ldg(olabel + out[k]);
+      if (ol != 0) olab_out[(size_t)li * cap + nol++] = ol;
+    }
+    for (int x = 0; x < kPathSmem; x++) nol_all += __ldg(olabel + s_path[x]) != 0;   // the walk's first arcs
+    // (arcs beyond kPathSmem are in nol_far)
   }
-  int nol = 0;
-  for (int k = 0; k < m; k++) {
-    const int32_t ol = __ldg(olabel + out[k]);
-    if (ol != 0 && nol < cap) olab_out[(size_t)li * cap + nol++] = ol;
-  }
-  n_olab_out[li] = s_nol;   // every olabel of the path, also when the arcs were truncated
-  status_out[li] = s_status != WFST_OK ? s_status : (len > cap ? WFST_ERR_INVALID_ARG : WFST_OK);
+  if (tid != 0) return;
+  n_olab_out[li] = nol_all + nol_far;   // every olabel of the path, also when the arcs were truncated
+  status_out[li] = status != WFST_OK ? status : (len > cap ? WFST_ERR_INVALID_ARG : WFST_OK);
 }
 
 }  // namespace
