@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(BS, kGcCtas) gc_kernel(GcParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* set = (uint32_t*)smem_raw;   // wanted source states
   __shared__ int s_w[33];
-  __shared__ int s_nw, s_nlive, s_nlive_next, s_stop, s_wide;
+  __shared__ int s_nw, s_nlive, s_nlive_next, s_stop, s_wide, s_np[2], s_found;
   const int tid = threadIdx.x;
   const int ln = p.lanes[blockIdx.x];
   LaneState* Lp = p.lanes_st + ln;
@@ -110,30 +110,41 @@ __global__ void __launch_bounds__(BS, kGcCtas) gc_kernel(GcParams p) {
   uint32_t* Ebuf[2] = {set, set + p.wcap / 2};
   uint32_t* Pbuf[2] = {set + kE, set + p.wcap / 2 + kE};
   // visit the records [0, n) of a layer, UNR loads in flight per thread
-  auto visit = [&](int2 L, auto&& f) {
+  // (ring position of record i of a layer: b0 + i, wrapped by one conditional subtraction)
+  const uint32_t Rc = (uint32_t)p.R_cap;
+  auto RI = [&](uint32_t b0, int i) { const uint32_t x = b0 + (uint32_t)i; return x >= Rc ? x - Rc : x; };
+  // done() (evaluated by every thread after each batch; one decision for the CTA) ends the visit
+  auto visit_until = [&](int2 L, auto&& f, auto&& done) {
+    const uint32_t b0 = R((int64_t)L.x);
     for (int i0 = 0; i0 < L.y; i0 += BS * UNR) {
       int2 r[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; u++) {
         const int i = i0 + u * BS + tid;
-        r[u] = i < L.y ? __ldcg(&rec[R((int64_t)L.x + i)]) : make_int2(-1, 0x7FFFFFFF);
+        r[u] = i < L.y ? __ldcg(&rec[RI(b0, i)]) : make_int2(-1, 0x7FFFFFFF);
       }
 #pragma unroll
       for (int u = 0; u < UNR; u++) {
         const int i = i0 + u * BS + tid;
-        if (i < L.y) f(i, r[u]);
+        if (i < L.y) f(RI(b0, i), r[u]);
       }
+      __syncthreads();
+      const bool d = done();
+      if (__syncthreads_or(d)) break;
     }
   };
+  auto visit = [&](int2 L, auto&& f) { visit_until(L, f, [] { return false; }); };
   // bounded insert: a full set flags the walk as too wide to track (s_wide)
-  auto put = [&](uint32_t* st, uint32_t cap, uint32_t q) {
+  auto put = [&](uint32_t* st, uint32_t cap, uint32_t q) {   // true: q is new
     uint32_t b = __umulhi(q * 0x9E3779B1u, cap);
     for (uint32_t n = 0; n < cap; n++) {
       const uint32_t old = atomicCAS(st + b, 0xFFFFFFFFu, q);
-      if (old == 0xFFFFFFFFu || old == q) return;
+      if (old == 0xFFFFFFFFu) return true;
+      if (old == q) return false;
       b = (b + 1 == cap) ? 0 : b + 1;
     }
     s_wide = 1;
+    return false;
   };
   // bounded lookup (a set filled by a failed put must not loop)
   auto has = [&](const uint32_t* st, uint32_t cap, uint32_t q) {
@@ -147,15 +158,17 @@ __global__ void __launch_bounds__(BS, kGcCtas) gc_kernel(GcParams p) {
     return false;
   };
   // a live record (arc a) sends its source state to E (epsilon arc: same layer) or P (layer below)
-  auto put_src = [&](int a, uint32_t* e, uint32_t* pp) {
+  // (s_np[w]: distinct states in P of pair w -- the pass over the layer below stops once it has
+  // found them all: a layer holds one token per state, and live tokens sit in its cheap front)
+  auto put_src = [&](int a, uint32_t* e, uint32_t* pp, int w) {
     if (a < 0) return;
     const int4 arc = __ldg(&p.arcs[a]);
     const uint32_t src = (uint32_t)(arc.w & 0x7FFFFFFF);
     if (arc.z < 0) {
       put(e, kE, src);
       s_nw = 1;
-    } else {
-      put(pp, kP, src);
+    } else if (put(pp, kP, src)) {
+      atomicAdd(&s_np[w], 1);
     }
   };
   auto clear = [&](int w) {
@@ -172,11 +185,12 @@ __global__ void __launch_bounds__(BS, kGcCtas) gc_kernel(GcParams p) {
     s_stop = F;
     s_wide = 0;
     s_nw = 0;
+    s_np[0] = s_np[1] = 0;
   }
   __syncthreads();
-  visit(Lk, [&](int i, int2 r) {
-    rec[R((int64_t)Lk.x + i)].y = r.y | kLive;
-    put_src(r.x, Ebuf[0], Pbuf[0]);
+  visit(Lk, [&](uint32_t x, int2 r) {
+    rec[x].y = r.y | kLive;
+    put_src(r.x, Ebuf[0], Pbuf[0], 0);
   });
   __syncthreads();
   int cur = 0;
@@ -191,29 +205,33 @@ __global__ void __launch_bounds__(BS, kGcCtas) gc_kernel(GcParams p) {
     const int2 Lb = LI(k - 1);
     const int nx = cur ^ 1;
     clear(nx);
+    const int np = s_np[cur];   // (complete: the pass that filled P ended with a barrier)
     if (tid == 0) {
       s_nlive_next = 0;
       s_nw = 0;
+      s_found = 0;
+      s_np[nx] = 0;
     }
     __syncthreads();
-    visit(Lb, [&](int i, int2 r) {
+    visit_until(Lb, [&](uint32_t x, int2 r) {
       if (has(Pbuf[cur], kP, (uint32_t)(r.y & 0x7FFFFFFF))) {
-        rec[R((int64_t)Lb.x + i)].y = r.y | kLive;
+        rec[x].y = r.y | kLive;
         atomicAdd(&s_nlive_next, 1);
-        put_src(r.x, Ebuf[nx], Pbuf[nx]);
+        atomicAdd(&s_found, 1);
+        put_src(r.x, Ebuf[nx], Pbuf[nx], nx);
       }
-    });
+    }, [&] { return !s_wide && s_found >= np; });
     __syncthreads();
     // epsilon predecessors inside layer k-1, to a fixed point
     while (s_nw && !s_wide) {
       __syncthreads();
       if (tid == 0) s_nw = 0;
       __syncthreads();
-      visit(Lb, [&](int i, int2 r) {
+      visit(Lb, [&](uint32_t x, int2 r) {
         if (r.y >= 0 && has(Ebuf[nx], kE, (uint32_t)r.y)) {
-          rec[R((int64_t)Lb.x + i)].y = r.y | kLive;
+          rec[x].y = r.y | kLive;
           atomicAdd(&s_nlive_next, 1);
-          put_src(r.x, Ebuf[nx], Pbuf[nx]);
+          put_src(r.x, Ebuf[nx], Pbuf[nx], nx);
         }
       });
       __syncthreads();
@@ -237,13 +255,14 @@ __global__ void __launch_bounds__(BS, kGcCtas) gc_kernel(GcParams p) {
   for (int k = k0; k <= Lc; k++) {
     const int2 Lq = LI(k);
     const int64_t nb = cursor;
+    const uint32_t qb = R((int64_t)Lq.x);
     for (int i0 = 0; i0 < Lq.y; i0 += BS) {
       const int i = i0 + tid;
       int2 r = make_int2(0, 0);
       float c = 0.0f;
       if (i < Lq.y) {
-        r = __ldcg(&rec[R((int64_t)Lq.x + i)]);
-        if (rc) c = __ldcg(&rc[R((int64_t)Lq.x + i)]);
+        r = __ldcg(&rec[RI(qb, i)]);
+        if (rc) c = __ldcg(&rc[RI(qb, i)]);
       }
       const bool live = i < Lq.y && r.y < 0;
       int total;
