@@ -33,6 +33,9 @@ constexpr int kModeFrames = 0, kModeInit = 1;
 #ifndef WFST_KBIG
 #define WFST_KBIG 64
 #endif
+#ifndef WFST_OWNER_BSEARCH
+#define WFST_OWNER_BSEARCH 1   // owner of each flattened arc by a shuffle binary search (else head flags + max-scan)
+#endif
 constexpr int kBig = WFST_KBIG;    // tokens with more emitting arcs are expanded CTA-wide
 #ifndef WFST_THSHIFT
 #define WFST_THSHIFT 10
@@ -766,6 +769,26 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
 #pragma unroll
         for (int u = 0; u < R; u++) {
           const int w0 = r0 + u * 32;
+#if WFST_OWNER_BSEARCH
+          // owner of arc j = the last token t with excl_t <= j (excl is non-decreasing; a token
+          // without arcs shares its excl with the next token, so it is never the last): a binary
+          // search over the warp's prefix sums, 5 shuffles
+          {
+            const int j = w0 + lane;
+            int lo = 0;
+#pragma unroll
+            for (int st = 16; st >= 1; st >>= 1) {
+              const int e = __shfl_sync(0xffffffffu, excl, lo + st);
+              if (e <= j) lo += st;
+            }
+            own[u] = lo;
+            v[u] = j < total;
+            const int eb_o = __shfl_sync(0xffffffffu, eb, lo);
+            const int ex_o = __shfl_sync(0xffffffffu, excl, lo);
+            a[u] = eb_o + (j - ex_o);
+            continue;
+          }
+#endif
           if (deg > 0 && excl >= w0 && excl < w0 + 32) wbuf[excl - w0] = lane;
           const unsigned cm = __ballot_sync(0xffffffffu, deg > 0 && excl <= w0 && w0 < incl);
           __syncwarp();
