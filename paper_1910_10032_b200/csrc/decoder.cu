@@ -494,7 +494,8 @@ wfst_status wfst_decoder_create_ex(wfst_graph_t g, int32_t n_streams, float beam
     return fail(WFST_ERR_INVALID_ARG, "unsupported (threads, ctas_per_sm, max_active_mode) combination");
   }
   // on-chip table: what is left of the SM's shared memory per resident CTA
-  const size_t static_smem = sizeof(SmemCtl) + 4 * (size_t)d->threads + (size_t)(d->threads / 32) * kStage * 16 + 1024;
+  const size_t static_smem = sizeof(SmemCtl) + (WFST_OWNER_BSEARCH ? 128 : 4 * (size_t)d->threads) +
+                             (size_t)(d->threads / 32) * kStage * 16 + 1024;
   const size_t per_cta = std::min((size_t)prop.sharedMemPerBlockOptin,
                                   (size_t)prop.sharedMemPerMultiprocessor / d->ctas_per_sm);
   // the staged log-likelihood row: columns 0..max_pdf (+16 B alignment slack on each side)

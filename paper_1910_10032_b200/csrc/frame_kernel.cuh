@@ -318,7 +318,7 @@ __device__ __forceinline__ int insert_s(uint32_t tab_sa, uint32_t nb, uint32_t q
 #pragma unroll
     for (int j = 0; j < kBucket; j++) {
       mq |= (uint32_t)((uint32_t)x[j] == q) << j;
-      me |= (uint32_t)(x[j] == kEmpty) << j;
+      me |= (uint32_t)((uint32_t)x[j] == 0xFFFFFFFFu) << j;   // (no state word is all ones: state ids < 2^31 - 1)
     }
     int j;
     if (mq) {
@@ -1773,7 +1773,7 @@ template <int BS, int R, int MINB, int AM>
 __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SmemCtl S;
-  __shared__ int s_wbuf[BS];
+  __shared__ int s_wbuf[WFST_OWNER_BSEARCH ? 32 : BS];   // owner buffers (head-flag owner map only)
   __shared__ __align__(16) int4 s_stage[(BS / 32) * kStage];
   u64* tab = (u64*)smem_raw;
   int* hist = (int*)(tab + p.C);
@@ -1781,7 +1781,7 @@ __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
   const int tid = threadIdx.x;
   const uint32_t tab_sa = saddr(tab);
   for (int i = tid; i < p.C; i += BS) sts64(tab_sa + 8u * i, kEmpty);
-  s_wbuf[tid] = -1;
+  if (!WFST_OWNER_BSEARCH || tid < 32) s_wbuf[tid] = -1;
   if (tid < 12) S.ph[tid] = 0;
   if (tid == 0) {
     S.status = WFST_OK;
@@ -1792,7 +1792,7 @@ __global__ void __launch_bounds__(BS, MINB) frame_kernel(KParams p) {
   }
   __syncthreads();
   static_assert((BS / 32) * kStage * 4 >= kNB, "selection scratch lives in the stage buffers");
-  Frame<BS, R, AM> fr(p, S, tab_sa, hist, s_wbuf + (tid & ~31), saddr(s_stage + (tid >> 5) * kStage), saddr(rowmem),
+  Frame<BS, R, AM> fr(p, S, tab_sa, hist, s_wbuf + (WFST_OWNER_BSEARCH ? 0 : (tid & ~31)), saddr(s_stage + (tid >> 5) * kStage), saddr(rowmem),
                       (int*)s_stage);
   fr.bind_scratch();
   while (true) {
