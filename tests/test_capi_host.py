@@ -87,3 +87,21 @@ def test_loader_errors_without_device(W, tmp_path):
     with pytest.raises(W.WfstError) as e:
         W.Graph.from_arrays(g)
     assert e.value.status == "GRAPH_INVALID"
+
+
+def test_packed_row_views(W):
+    """The binding's per-stream views over a packed partial-paths result (wfst_get_partial_paths_packed):
+    stream i is a[off[i] : off[i] + min(n[i], cap)], in any packing order; indexing, negative indices,
+    slices, iteration and len behave like a list of arrays."""
+    a = np.array([7, 8, 9, 1, 2, 3, 4, 5], np.int32)
+    off = np.array([3, 0, 8, 5], np.int64)   # stream 0 at 3, stream 1 at 0, stream 2 empty, stream 3 at 5
+    n = np.array([2, 3, 0, 9], np.int32)     # stream 3 overflowed cap = 3: only cap entries were stored
+    rows = W._Rows(a, n, off, 3)
+    assert len(rows) == 4
+    assert rows[0].tolist() == [1, 2] and rows[1].tolist() == [7, 8, 9] and rows[2].tolist() == []
+    assert rows[3].tolist() == [3, 4, 5]     # (over cap: the cap entries that were stored)
+    assert rows[-3].tolist() == [7, 8, 9]
+    assert [r.tolist() for r in rows[1:3]] == [[7, 8, 9], []]
+    assert [r.size for r in rows] == [2, 3, 0, 3]
+    with pytest.raises(IndexError):
+        rows[4]
