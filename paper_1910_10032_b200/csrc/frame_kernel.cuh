@@ -33,6 +33,9 @@ constexpr int kModeFrames = 0, kModeInit = 1;
 #ifndef WFST_KBIG
 #define WFST_KBIG 64
 #endif
+#ifndef WFST_EARLY_CURSORS
+#define WFST_EARLY_CURSORS 1   // warp 0 places the contraction's cursors before an earlier barrier
+#endif
 #ifndef WFST_OWNER_BSEARCH
 #define WFST_OWNER_BSEARCH 1   // owner of each flattened arc by a shuffle binary search (else head flags + max-scan)
 #endif
@@ -122,6 +125,7 @@ struct SmemCtl {
   int32_t n_claim, n_claim_emit, n_ovf, n_oclaim, n_surv, n_in, n_wl, n_big, next_group;
   int32_t wlc[3];   // epsilon worklist counters (rotating)
   int32_t eps_r, eps_cur;           // where the warp-synchronous epsilon iterations stopped
+  int32_t cursors_done;             // warp 0 placed the contraction's cursors early this frame
   uint32_t swl[2][kEpsWarp];        // the first kEpsWarp entries of the epsilon worklists
 #ifdef WFST_COUNT
   unsigned long long dbgc[4];   // alpha-bound frames: claims above k_alpha by (0,0.5], (0.5,2], (2,5], >5
@@ -990,9 +994,12 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   }
 
   // ---- row a3: beam + exact max-active (readings R5, R6) ----
-  __device__ void select_cutoff() {
+  // beam_cut: the frame's beam cutoff (every thread computes it from the final best: no barrier
+  // publishes S.beam_cut before this call).  Every path below ends with a barrier, which also
+  // publishes thread 0's S.beam_cut and the epsilon worklist counters (eps_init).
+  __device__ void select_cutoff(float beam_cut) {
     const int tid = threadIdx.x;
-    const float beam_cut = S.beam_cut;
+    if (tid == 0) eps_init();
     const int n_claim = min(S.n_claim, p.FCAP);
     if (p.alpha <= 0 || n_claim <= p.alpha) {   // max-active cannot bind (n_in <= n_claim)
       if (tid == 0) {
@@ -1000,11 +1007,19 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         S.use_alpha = 0;
         S.kalpha = INFINITY;
       }
+#if WFST_EARLY_CURSORS
+      // no epsilon seeds: the table is final, so warp 0 places the contraction's cursors now and
+      // this barrier publishes them (the contraction skips its own scan and barrier)
+      if (tid < 32 && S.n_wl == 0) {
+        place_cursors(min(pbin(beam_cut), pbin(INFINITY)));   // (the contraction's bc with cut_a = inf)
+        if (tid == 0) S.cursors_done = 1;
+      }
+#endif
       __syncthreads();
       return;
     }
     if constexpr (AM == 1) {
-      select_hist();
+      select_hist(beam_cut);
       return;
     }
     // Fast path: hist holds the exact count of live entries per fine cost bin.  bin_of is
@@ -1210,9 +1225,8 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
   // one pass counts the in-beam entries into kNB bins of width beam/kNB over [best, best+beam);
   // b = the first bin whose cumulative count reaches alpha; keep c < best + (b+1)*beam/kNB.
   // Same fp32 operations as the oracle's hist_cutoff.
-  __device__ void select_hist() {
+  __device__ void select_hist(float beam_cut) {
     const int tid = threadIdx.x;
-    const float beam_cut = S.beam_cut;
     const float best = float_of_ord(S.best_ord);
     const float inv = __fdiv_rn((float)kNB, p.beam), wd = __fdiv_rn(p.beam, (float)kNB);
     for (int i = tid; i < kNB; i += BS) sel[i] = 0;
@@ -1308,21 +1322,22 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     }
   }
 
+  // thread 0, once the seeds are final and before a barrier that precedes eps_closure
+  __device__ __forceinline__ void eps_init() {
+    S.wlc[0] = S.n_wl;
+    S.wlc[1] = S.wlc[2] = 0;
+    S.eps_r = 0;
+    S.eps_cur = 0;
+  }
+
+  // seed: the emitting phase listed every claimed state with epsilon arcs (flag in bit 31 of
+  // the state word) in worklist 0; the ones the cutoff drops are skipped below
+  // Worklist counters rotate over three words: iteration i reads wlc[i%3], appends to
+  // wlc[(i+1)%3] and clears wlc[(i+2)%3] (read in iteration i-1, appended to in i+1), so one
+  // barrier per iteration suffices.  (Initialised by eps_init before a preceding barrier.)
   __device__ void eps_closure() {
     const int tid = threadIdx.x;
     const float cut_b = S.beam_cut, cut_a = S.use_alpha ? S.kalpha : INFINITY;
-    // seed: the emitting phase listed every claimed state with epsilon arcs (flag in bit 31 of
-    // the state word) in worklist 0; the ones the cutoff drops are skipped below
-    // Worklist counters rotate over three words: iteration i reads wlc[i%3], appends to
-    // wlc[(i+1)%3] and clears wlc[(i+2)%3] (read in iteration i-1, appended to in i+1), so one
-    // barrier per iteration suffices.
-    if (tid == 0) {
-      S.wlc[0] = S.n_wl;
-      S.wlc[1] = S.wlc[2] = 0;
-      S.eps_r = 0;
-      S.eps_cur = 0;
-    }
-    __syncthreads();
     long long relax = 0;
     // Small worklists (the usual case: a few back-off arcs per frame): warp 0 alone runs the
     // iterations, entries from the on-chip mirror, __syncwarp between iterations -- no CTA
@@ -1346,6 +1361,13 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
           S.eps_r = r;
           S.eps_cur = cur;
         }
+#if WFST_EARLY_CURSORS
+        if (S.wlc[r] == 0) {   // closed in warp mode: the table is final, place the cursors now
+          __syncwarp();
+          place_cursors(min(pbin(cut_b), pbin(cut_a)));
+          if (tid == 0) S.cursors_done = 1;
+        }
+#endif
       }
       __syncthreads();
     }
@@ -1384,8 +1406,20 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     // lies above bc: their counts give exact cursors, and the survivors of bin bc are appended
     // after them.  One pass over the table, no counting pass.
     const int bc = min(pbin(cut_b), pbin(cut_a));
+    if (!S.cursors_done) {   // (else warp 0 computed them before an earlier barrier of this frame)
+      if (tid < 32) place_cursors(bc);
+      __syncthreads();
+    }
+    mark(6);   // cursors ready
+    contract_drain(cut_b, cut_a, bc);
+  }
+
+  // warp 0: exclusive scan of the coarse placement bins below bc (the contraction's cursors) from
+  // the exact histogram -- valid once no insert can change the table any more
+  __device__ __forceinline__ void place_cursors(int bc) {
+    const int lane = threadIdx.x & 31;
     static_assert(kPlace == 64 && kNB == 1024, "warp 0 scans two coarse (32 fine) bins per lane");
-    if (tid < 32) {   // exclusive scan of the bins below bc (per-frame critical path: no serial loop)
+    {   // (per-frame critical path: no serial loop)
       const int b0 = 2 * lane, b1 = b0 + 1;
       const int f0 = lds_sum<4>(hist_sa + 128u * (uint32_t)lane);         // coarse bin b0
       const int f1 = lds_sum<4>(hist_sa + 128u * (uint32_t)lane + 64u);   // coarse bin b1
@@ -1404,8 +1438,10 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         S.warp_tmp[0] = -1;   // min survivor cost, orderable (0xFFFFFFFF: none)
       }
     }
-    __syncthreads();
-    mark(6);   // cursors ready
+  }
+
+  __device__ void contract_drain(float cut_b, float cut_a, int bc) {
+    const int tid = threadIdx.x, lane = tid & 31;
     const int n_ub = S.n_surv;
     const int32_t rb = S.L.rec_used;
     if (n_ub > p.FCAP || (long long)rb + n_ub - S.L.rec_floor > p.R_cap || (long long)rb + n_ub > INT32_MAX) {
@@ -1489,7 +1525,8 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     mark(8);   // placement done
   }
 
-  __device__ void begin_frame(float beam_cut_fixed, bool emitting) {
+  // sync = false: the caller's next barrier publishes the frame's initial state (row_wait)
+  __device__ void begin_frame(float beam_cut_fixed, bool emitting, bool sync = true) {
     const int tid = threadIdx.x;
     for (int i = tid; i < kNB; i += BS) hist[i] = 0;
     if (tid < kPlace) S.bcnt[tid] = 0;
@@ -1513,6 +1550,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       S.n_big = 0;
       S.next_group = 0;
       S.next_chunk = 0;
+      S.cursors_done = 0;
 #ifdef WFST_COUNT
       S.dbgc[0] = S.dbgc[1] = S.dbgc[2] = S.dbgc[3] = 0;
 #endif
@@ -1529,7 +1567,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
       S.ref = S.L.front_best - half;
       S.inv_w = (float)kNB / (4.0f * half);
     }
-    __syncthreads();
+    if (sync) __syncthreads();
   }
 
   __device__ void clear_all() {
@@ -1625,9 +1663,11 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
         else claimed = false;
       }
       add_claim(slot, claimed, flag, -1);
+      __syncwarp();   // (the seed append of add_claim is visible to lane 0)
       if (tid == 0) {
         S.best_ord = o;
         S.n_claim_emit = 1;
+        eps_init();
       }
     }
     __syncthreads();
@@ -1708,7 +1748,7 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
 #if WFST_ROWSMEM
     if (tid == 0 && !S.row_pending) row_issue(row_ptr(t));   // first frame of a work item
 #endif
-    begin_frame(INFINITY, true);
+    begin_frame(INFINITY, true, !WFST_ROWSMEM);   // (row_wait's barrier publishes it)
     tick(t0, 5);
 #if WFST_ROWSMEM
     row_wait();
@@ -1726,19 +1766,27 @@ struct Frame {   // AM: max-active rule, 0 exact (R6), 1 histogram (R16) -- a te
     if (tid == 0 && t_next >= 0) row_issue(row_ptr(t_next));   // overlaps the frame's tail
 #endif
     tick(t0, 0);
-    if (tid == 0) {
-      S.n_claim_emit = S.n_claim;
-      if (S.best_ord == 0xFFFFFFFFu) S.status = WFST_ERR_NO_SURVIVOR;
-      else S.beam_cut = __fadd_rn(float_of_ord(S.best_ord), p.beam);
-    }
-    __syncthreads();
-    if (S.status != WFST_OK) {
-      if (tid == 0) S.n_surv = 0;
+    // expand() ends with a barrier: the best cost, the claim count and the status are final, so
+    // every thread derives the cutoff itself (select_cutoff's barrier publishes thread 0's copies)
+    const uint32_t best_o = S.best_ord;
+    const bool bad = best_o == 0xFFFFFFFFu || S.status != WFST_OK;
+    const float beam_cut = bad ? INFINITY : __fadd_rn(float_of_ord(best_o), p.beam);
+    if (bad) {
+      __syncthreads();   // every thread has read S.status before thread 0 may set it
+      if (tid == 0) {
+        if (best_o == 0xFFFFFFFFu && S.status == WFST_OK) S.status = WFST_ERR_NO_SURVIVOR;
+        S.n_claim_emit = S.n_claim;
+        S.n_surv = 0;
+      }
       __syncthreads();
       finish_frame(t, true);   // wipes the tables
       return;
     }
-    select_cutoff();
+    if (tid == 0) {
+      S.n_claim_emit = S.n_claim;
+      S.beam_cut = beam_cut;
+    }
+    select_cutoff(beam_cut);
     tick(t0, 1);
     eps_closure();
     tick(t0, 2);
