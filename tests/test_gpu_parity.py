@@ -347,6 +347,29 @@ def test_tie_heavy_dyadic(W, torch, oracle_mod):
 
 
 @pytest.mark.slow
+@pytest.mark.slow
+def test_c4_full_size_all_streams(W, torch, oracle_mod):
+    """C4 (BASELINE configs[3]) at its bench size and launch configuration: 1024 streams x 500
+    frames on the ~50M-state / ~150M-arc graph, decoded in 50-frame chunks -- the final paths of
+    EVERY stream against the oracle, element by element."""
+    import bench
+    wl = bench.make_workload("c4", "clean")
+    T, B = wl["T"], wl["B"]
+    c = wl["c"]
+    G = W.Graph.from_arrays(wl["graph"])
+    D = W.Decoder(G, B, wl["beam"], wl["alpha"])
+    ll = bench.device_loglikes(W, torch, wl, "cuda:0")
+    D.reset()
+    for t0 in range(0, T, c["chunk"]):
+        D.decode_frames(ll[t0:t0 + c["chunk"]])
+    res = D.best_paths(cap=4 * T + 64)
+    assert res["rc"] == 0
+    del ll
+    og = oracle_mod.OracleGraph(wl["graph"])
+    gen = lambda b: I.loglikes_stream(c["ll_seed"], b, T, wl["P"], wl["planted"][:, b], **wl["preset"])
+    assert _all_streams_vs_oracle(og, gen, range(B), wl["beam"], wl["alpha"], res) == 1024
+
+
 def test_c4_large_graph_memory_and_chunks(W, torch, oracle_mod):
     """C4 (BASELINE configs[3]): a large-LM-shaped graph (~50M states / ~150M arcs) and 1024
     streams decoded in 50-frame chunks.  Checks the device footprint against Eq. 1
@@ -431,9 +454,9 @@ def test_c5_online_chunks_full_size(W, torch, oracle_mod):
         n = res["n_arcs"][b]
         assert list(res["arcs"][b, :n]) == list(r.arcs) and res["cost"][b] == r.cost32
         assert acc[b] == list(r.arcs[:len(acc[b])]) and len(acc[b]) > 100
-    # final paths of 512 of the 4096 streams (every 8th), all against the oracle
+    # final paths of EVERY one of the 4096 streams against the oracle
     gen = lambda b: I.loglikes_stream(c["ll_seed"], b, T, P, wl["planted"][:, b], **wl["preset"])
-    assert _all_streams_vs_oracle(og, gen, range(0, B, 8), wl["beam"], wl["alpha"], res) == 512
+    assert _all_streams_vs_oracle(og, gen, range(B), wl["beam"], wl["alpha"], res) == 4096
 
 
 def test_graph_replicate(W, torch, oracle_mod):
